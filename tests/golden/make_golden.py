@@ -1,0 +1,341 @@
+"""Generate golden vectors by running the REFERENCE (gmfkit) itself.
+
+Run in the build container only (needs /root/reference):
+
+    python tests/golden/make_golden.py
+
+The reference package is imported from /root/reference/pkg/src (its
+pure-numpy kernel backend is selected; gmfkit's own tests pin it to the
+compiled backend at 1e-13, kernels/test_kernels.py:43-55).  Outputs are
+small .npz fixtures committed under tests/golden/; nothing at test time
+reads /root/reference.
+
+Fixtures:
+  c1.npz          BASELINE config 1 exactly (Poisson, 1000x100, k=5, X=Z=1,
+                  mb 100 x all columns, 50 epochs): per-step states at
+                  checkpoints, step-0 gradients, trace, final state/objective.
+  nb_offset.npz   NB with a per-row offset (SURVEY §8c shim), p=1, q=0.
+  nb_cov_s3.npz   NB, p=2, q=1, mb_cols < m (S = 3 column blocks per epoch).
+  converge.npz    Poisson with the default-style tol: converged flag/epochs.
+  diverge.npz     rate_k0=1.2, damping=0: DivergenceError after 4 epochs; the
+                  snapshot is the state after epoch 3 (not the init).
+  seam.npz        derivs_from_mu / deviance / mean_of_eta vectors, all families.
+  project.npz     (A)+(B1) projections incl. a rank-deficient case.
+  weighted.npz    minibatch gradients with non-unit prior weights.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+os.environ.setdefault("GMFKIT_PURE_PYTHON", "1")
+
+import gmfkit as gk                      # noqa: E402
+import gmfkit.model as gmodel            # noqa: E402
+import gmfkit.optim as goptim            # noqa: E402
+from gmfkit.kernels import _ref as gref  # noqa: E402
+
+from paper_2412_20509_b200 import workloads  # noqa: E402
+
+CHECK_STEPS = (0, 1, 4, 9, 19, 49)
+
+
+def _state_arrays(prefix, st):
+    return {f"{prefix}_b": st.b.copy(), f"{prefix}_gamma": st.gamma.copy(),
+            f"{prefix}_u": st.u.copy(), f"{prefix}_v": st.v.copy(),
+            f"{prefix}_nb": np.float64(st.nb_shape), f"{prefix}_phi": np.float64(st.phi)}
+
+
+class OffsetShim:
+    """Add a per-row offset to every eta entry point of the reference."""
+
+    def __init__(self, offset):
+        self.offset = offset
+        self.saved = {}
+
+    def __enter__(self):
+        off = self.offset
+        orig_lp = gmodel.linear_predictor
+        orig_ent = goptim._entrywise_eta
+
+        def lp(state, covs, rows=None, cols=None):
+            eta = orig_lp(state, covs, rows, cols)
+            o = off if rows is None else off[np.asarray(rows)]
+            return eta + o[:, None]
+
+        def ent(state, covs, rows, cols):
+            return orig_ent(state, covs, rows, cols) + off[rows]
+
+        self.saved = {"m": orig_lp, "o": goptim.linear_predictor, "e": orig_ent}
+        gmodel.linear_predictor = lp
+        goptim.linear_predictor = lp
+        goptim._entrywise_eta = ent
+        return self
+
+    def __exit__(self, *exc):
+        gmodel.linear_predictor = self.saved["m"]
+        goptim.linear_predictor = self.saved["o"]
+        goptim._entrywise_eta = self.saved["e"]
+
+
+def _run_fit(y, x, z, init, fam, cfg, offset=None, lam=None, weights=None):
+    pen = lam or gk.PenaltyConfig()
+    data = gk.ResponseMatrix(y.astype(float), weights=weights)
+    covs = gk.CovariateSet(x=x if x.shape[1] else None, z=z if z.shape[1] else None,
+                           n=y.shape[0], m=y.shape[1])
+    steps = {}
+
+    def cb(t, st):
+        if t in CHECK_STEPS:
+            steps[t] = st.copy()
+
+    init_st = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"],
+                                    init.get("phi", 1.0), init.get("nb_shape", 1.0))
+    ctx = OffsetShim(offset) if offset is not None else None
+    if ctx:
+        ctx.__enter__()
+    try:
+        # step-0 gradient on the replayed first block
+        rng = np.random.default_rng(cfg.seed)
+        rb = goptim._partition(rng, y.shape[0], min(cfg.mb_rows, y.shape[0]))
+        cb_ = goptim._partition(rng, y.shape[1], min(cfg.mb_cols, y.shape[1]))
+        goptim._eval_entries(data, cfg.max_eval_entries, rng)
+        first = int(rng.integers(len(rb)))
+        fam_live = gk.NegBinomial(init_st.nb_shape) if fam.kind == "neg_binomial" else fam
+        g0 = gk.minibatch_gradients(init_st, data, covs, fam_live, gk.Log(), pen,
+                                    gk.Minibatch(rb[first], cb_[0]))
+        final, rep = gk.fit_asgd(data, covs, fam, gk.Log(), pen, cfg, init_st, callback=cb)
+        unproj, _ = gk.fit_asgd(data, covs, fam, gk.Log(), pen, cfg, init_st,
+                                identify_mode=None)
+    finally:
+        if ctx:
+            ctx.__exit__()
+    out = {"y": y.astype(np.int32), "x": x, "z": z, "first_block": np.int64(first),
+           "g0_g_row": g0.g_rowside, "g0_h_row": g0.h_rowside,
+           "g0_g_col": g0.g_colside, "g0_h_col": g0.h_colside,
+           "trace": np.asarray(rep.objective_trace), "nb_trace": np.asarray(rep.nb_shape_trace),
+           "final_objective": np.float64(rep.final_objective),
+           "epochs_run": np.int64(rep.epochs_run), "converged": np.bool_(rep.converged),
+           "iterations": np.int64(rep.diagnostics["iterations"]),
+           "check_steps": np.asarray(sorted(steps), dtype=np.int64),
+           "cfg": np.asarray([cfg.max_epochs, cfg.mb_rows, cfg.mb_cols, cfg.seed,
+                              cfg.max_eval_entries], dtype=np.int64),
+           "cfg_f": np.asarray([cfg.rate_k0, cfg.rate_k1, cfg.rate_tau, cfg.smooth_a1,
+                                cfg.smooth_a2, cfg.damping, cfg.tol]),
+           "lam": np.asarray([pen.lam_b, pen.lam_gamma, pen.lam_u, pen.lam_v]),
+           "family": np.asarray(fam.kind)}
+    if offset is not None:
+        out["offset"] = offset
+    if weights is not None:
+        out["w"] = weights
+    out.update(_state_arrays("init", init_st))
+    out.update(_state_arrays("final", final))
+    out.update(_state_arrays("unproj", unproj))
+    for t, st in steps.items():
+        out.update(_state_arrays(f"step{t}", st))
+    return out
+
+
+def make_c1():
+    wl = workloads.generate("c1")
+    y = wl.y_dense
+    data = gk.ResponseMatrix(y.astype(float))
+    covs = gk.CovariateSet(x=wl.x, z=wl.z)
+    init = gk.init_glm_svd(data, covs, gk.Poisson(), gk.Log(), 5, seed=0)
+    init_d = dict(b=init.b, gamma=init.gamma, u=init.u, v=init.v, phi=init.phi,
+                  nb_shape=init.nb_shape)
+    cfg = gk.SgdConfig(max_epochs=50, mb_rows=100, mb_cols=100, tol=1e-30, seed=0)
+    return _run_fit(y, wl.x, wl.z, init_d, gk.Poisson(), cfg)
+
+
+def _nb_problem(n, m, p, q, d, seed, offset):
+    rng = np.random.default_rng(seed)
+    x = np.ones((n, p))
+    if p > 1:
+        x[:, 1:] = (rng.uniform(size=(n, p - 1)) < 0.5)
+    z = np.ones((m, q))
+    u = rng.normal(0, 0.4, (n, d))
+    v = rng.normal(0, 0.4, (m, d))
+    b = rng.normal(0.3, 0.4, (m, p))
+    g = rng.normal(0, 0.3, (n, q))
+    off = rng.normal(0, 0.6, n) if offset else None
+    eta = u @ v.T + x @ b.T + (g @ z.T if q else 0) + (off[:, None] if offset else 0)
+    mu = np.exp(eta)
+    lam_ = rng.gamma(2.0, mu / 2.0)
+    y = rng.poisson(lam_).astype(np.int32)
+    init = dict(b=b + rng.normal(0, 0.05, b.shape), gamma=g + rng.normal(0, 0.05, g.shape),
+                u=u + rng.normal(0, 0.05, u.shape), v=v + rng.normal(0, 0.05, v.shape),
+                phi=1.0, nb_shape=1.5)
+    return y, x, z, off, init
+
+
+def make_nb_offset():
+    y, x, z, off, init = _nb_problem(1200, 150, 1, 0, 6, 11, True)
+    cfg = gk.SgdConfig(max_epochs=30, mb_rows=200, mb_cols=150, tol=1e-30, seed=3)
+    return _run_fit(y, x, z, init, gk.NegBinomial(1.5), cfg, offset=off)
+
+
+def make_nb_cov_s3():
+    y, x, z, _, init = _nb_problem(900, 120, 2, 1, 4, 12, False)
+    cfg = gk.SgdConfig(max_epochs=12, mb_rows=150, mb_cols=40, tol=1e-30, seed=5)
+    pen = gk.PenaltyConfig(lam=0.7, blocks=(0.1, 0.2, 1.0, 0.5))
+    return _run_fit(y, x, z, init, gk.NegBinomial(1.5), cfg, lam=pen)
+
+
+def make_converge():
+    rng = np.random.default_rng(21)
+    n, m, d = 120, 30, 2
+    u = rng.normal(0, 0.5, (n, d))
+    v = rng.normal(0, 0.5, (m, d))
+    b = rng.normal(1.0, 0.3, (m, 1))
+    y = rng.poisson(np.exp(u @ v.T + b.T)).astype(np.int32)
+    x = np.ones((n, 1))
+    z = np.ones((m, 0))
+    data = gk.ResponseMatrix(y.astype(float))
+    covs = gk.CovariateSet(x=x, m=m)
+    init = gk.init_glm_svd(data, covs, gk.Poisson(), gk.Log(), d, seed=0)
+    init_d = dict(b=init.b, gamma=init.gamma, u=init.u, v=init.v)
+    cfg = gk.SgdConfig(max_epochs=2000, seed=0, tol=1e-4, mb_rows=60, mb_cols=30,
+                       rate_k0=0.05)
+    return _run_fit(y, x, z, init_d, gk.Poisson(), cfg)
+
+
+def make_diverge():
+    rng = np.random.default_rng(22)
+    n, m, d = 60, 12, 1
+    u = rng.normal(0, 0.5, (n, d))
+    v = rng.normal(0, 0.5, (m, d))
+    b = rng.normal(1.0, 0.3, (m, 1))
+    y = rng.poisson(np.exp(u @ v.T + b.T)).astype(np.int32)
+    x = np.ones((n, 1))
+    data = gk.ResponseMatrix(y.astype(float))
+    covs = gk.CovariateSet(x=x, m=m)
+    init = gk.init_glm_svd(data, covs, gk.Poisson(), gk.Log(), d, seed=0)
+    cfg = gk.SgdConfig(max_epochs=200, seed=0, rate_k0=1.2, rate_k1=0.0, damping=0.0,
+                       mb_rows=20, mb_cols=12)
+    count = []
+    try:
+        gk.fit_asgd(data, covs, gk.Poisson(), gk.Log(), gk.PenaltyConfig(), cfg, init,
+                    callback=lambda t, s: count.append(t))
+        raise RuntimeError("expected divergence")
+    except gk.DivergenceError as err:
+        snap = err.state
+    out = {"y": y, "x": x, "z": np.ones((m, 0)), "steps_before": np.int64(len(count)),
+           "cfg": np.asarray([cfg.max_epochs, cfg.mb_rows, cfg.mb_cols, cfg.seed,
+                              cfg.max_eval_entries], dtype=np.int64),
+           "cfg_f": np.asarray([cfg.rate_k0, cfg.rate_k1, cfg.rate_tau, cfg.smooth_a1,
+                                cfg.smooth_a2, cfg.damping, cfg.tol])}
+    out.update(_state_arrays("init", init))
+    out.update(_state_arrays("snap", snap))
+    return out
+
+
+def make_seam():
+    rng = np.random.default_rng(31)
+    out = {}
+    pairs = [("poisson", "log", gk.Poisson()), ("neg_binomial", "log", gk.NegBinomial(2.3)),
+             ("gaussian", "identity", gk.Gaussian()), ("gamma", "inverse", gk.Gamma()),
+             ("inverse_gaussian", "inverse_squared", gk.InverseGaussian()),
+             ("bernoulli", "logit", gk.Bernoulli()), ("gamma", "log", gk.Gamma()),
+             ("gaussian", "log", gk.Gaussian()), ("inverse_gaussian", "log", gk.InverseGaussian())]
+    for fk, lk, fam in pairs:
+        n = 257
+        if fk == "bernoulli":
+            mu = rng.uniform(0.15, 0.85, n)
+        elif fk == "gaussian" and lk == "identity":
+            mu = rng.normal(0, 2, n)
+        else:
+            mu = rng.uniform(0.5, 5.0, n)
+        y = fam.sample(mu, rng=rng)
+        if fk in ("gamma", "inverse_gaussian"):
+            y = np.maximum(y, 1e-3)
+        if fk in ("poisson", "neg_binomial"):
+            y[:20] = 0.0
+        w = rng.uniform(0.5, 2.0, n)
+        lnk = gk.link(lk)
+        eta = lnk.eval(mu)
+        fc, lc = gk.kernels.FAMILY_CODES[fk], gk.kernels.LINK_CODES[lk]
+        alpha = getattr(fam, "nb_shape", 1.0)
+        mu_k = gref.mean_of_eta(lc, eta)
+        dd, hh = gref.derivs_from_mu(fc, lc, y, mu_k, w, 1.3, alpha)
+        dev = gref.deviance_from_mu(fc, y, mu_k, w, alpha)
+        key = f"{fk}+{lk}"
+        out[f"{key}|y"] = y
+        out[f"{key}|eta"] = eta
+        out[f"{key}|w"] = w
+        out[f"{key}|mu"] = mu_k
+        out[f"{key}|dotd"] = dd
+        out[f"{key}|ddotd"] = hh
+        out[f"{key}|dev"] = np.float64(dev)
+        out[f"{key}|codes"] = np.asarray([fc, lc], dtype=np.int64)
+        out[f"{key}|alpha"] = np.float64(alpha)
+    return out
+
+
+def make_project():
+    rng = np.random.default_rng(41)
+    out = {}
+    for k in range(3):
+        n, m, d, p, q = 25 + 5 * k, 10, 3, 2, 1
+        x = np.hstack([np.ones((n, 1)), rng.normal(size=(n, p - 1))])
+        z = np.ones((m, q))
+        covs = gk.CovariateSet(x=x, z=z)
+        st = gk.FactorizationState(b=rng.normal(size=(m, p)), gamma=rng.normal(size=(n, q)),
+                                   u=rng.normal(size=(n, d)), v=rng.normal(size=(m, d)))
+        pr = gk.project_constraints(st, covs, "B1")
+        out.update({f"{k}|x": x, f"{k}|z": z})
+        out.update(_state_arrays(f"{k}|in", st))
+        out.update(_state_arrays(f"{k}|out", pr))
+    n, m = 10, 6
+    u = rng.normal(size=(n, 2))
+    v = rng.normal(size=(m, 2))
+    st = gk.FactorizationState(np.zeros((m, 0)), np.zeros((n, 0)),
+                               np.hstack([u, u[:, :1]]), np.hstack([v, np.zeros((m, 1))]))
+    pr, info = gk.project_constraints(st, gk.CovariateSet.empty(n, m), "B1", return_info=True)
+    out.update(_state_arrays("rd|in", st))
+    out.update(_state_arrays("rd|out", pr))
+    out["rd|eff"] = np.int64(info["effective_rank"])
+    return out
+
+
+def make_weighted():
+    rng = np.random.default_rng(51)
+    n, m, d = 40, 16, 3
+    y, x, z, off, init = _nb_problem(n, m, 1, 1, d, 52, False)
+    w = rng.uniform(0.5, 2.0, (n, m))
+    data = gk.ResponseMatrix(y.astype(float), weights=w)
+    covs = gk.CovariateSet(x=x, z=z)
+    st = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], 1.0, 1.7)
+    pen = gk.PenaltyConfig(lam=0.8, blocks=(0.2, 0.1, 1.0, 0.6))
+    I = np.array([1, 4, 5, 9, 17, 30])
+    J = np.arange(m)
+    gp = gk.minibatch_gradients(st, data, covs, gk.NegBinomial(1.7), gk.Log(), pen,
+                                gk.Minibatch(I, J))
+    obj = gk.penalized_objective(st, data, covs, gk.NegBinomial(1.7), gk.Log(), pen)
+    out = {"y": y, "x": x, "z": z, "w": w, "I": I, "g_row": gp.g_rowside,
+           "h_row": gp.h_rowside, "g_col": gp.g_colside, "h_col": gp.h_colside,
+           "objective": np.float64(obj), "lam": np.asarray([0.16, 0.08, 0.8, 0.48])}
+    out.update(_state_arrays("st", st))
+    return out
+
+
+def main():
+    makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
+              "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
+              "project": make_project, "weighted": make_weighted}
+    only = sys.argv[1:] or list(makers)
+    for name in only:
+        arrs = makers[name]()
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **arrs)
+        print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+if __name__ == "__main__":
+    main()
