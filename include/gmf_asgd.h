@@ -1,0 +1,226 @@
+/*
+ * gmf_asgd.h -- C ABI of the B200-native aSGD hot path for penalized
+ * generalized matrix factorization (arXiv 2412.20509).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/gmfkit):
+ *
+ *   Level 1 (backend seam, gmfkit/kernels):
+ *     gmf_mean_of_eta      <- kernels/_ref.py:21-32  mean_of_eta(lcode, eta)
+ *                             kernels/__init__.py:57-60 block_mean
+ *     gmf_derivs_from_mu   <- kernels/_core.pyx:58-111 derivs_from_mu(fcode, lcode,
+ *                             y, mu, w, phi, alpha) -> (dotd, ddotd)
+ *                             kernels/_ref.py:65-88 (same contract)
+ *     gmf_deviance_from_mu <- kernels/_ref.py:91-108 deviance_from_mu(fcode, y, mu,
+ *                             w, alpha) -> float; kernels/__init__.py:80-90
+ *
+ *   Level 2 (fit engine behind optim.fit_asgd, optim.py:383-489):
+ *     gmf_create/gmf_destroy  own the device workspace of one fit (optim.py:409-414)
+ *     gmf_reset               t = 0, EMA zero, initial trace entry (optim.py:404-417)
+ *     gmf_minibatch_grad      gradients.py:116-132 minibatch_gradients -> GradientPair
+ *     gmf_step_local          one aSGD step, rank-local half: tracked objective
+ *                             (optim.py:283-290) + fused block gradient
+ *                             (optim.py:427-448, gradients.py:102-113)
+ *     gmf_step_apply          tracker (optim.py:301-338), EMA + adaptive update
+ *                             (optim.py:450-462), NB shape update (optim.py:469-473)
+ *     gmf_run                 n x (local + apply), captured in a CUDA graph
+ *     gmf_status/gmf_read_*   FitReport fields (optim.py:109-127)
+ *     gmf_objective_full      model.py:268-276 penalized_objective (deviance part)
+ *   Level 3 (identify.project_constraints (A)+(B1), identify.py:59-110):
+ *     gmf_cross_rows          Z = A' B over rows (Gram / cross products), fp64
+ *     gmf_rows_affine         Y <- beta Y + A M, row-local apply of a small matrix
+ *
+ * Conventions: plain pointers and sizes; device pointers unless stated; a
+ * `stream` argument is a cudaStream_t passed as void* (NULL = legacy default
+ * stream); every entry point returns GMF_OK (0) or a negative code, never
+ * throws; gmf_last_error() describes the last failure on the calling thread.
+ * A handle is single-writer; distinct handles are independent (re-entrant).
+ */
+#ifndef GMF_ASGD_H
+#define GMF_ASGD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMF_OK 0
+#define GMF_ERR_CONFIG (-1)      /* gmfkit ConfigError  (exceptions.py:12)  */
+#define GMF_ERR_DOMAIN (-2)      /* gmfkit DomainError  (exceptions.py:8)   */
+#define GMF_ERR_CUDA (-3)        /* CUDA runtime failure                    */
+#define GMF_ERR_UNSUPPORTED (-4) /* valid for gmfkit, not built here        */
+#define GMF_ERR_STATE (-5)       /* call order / handle misuse              */
+
+enum gmf_dtype { GMF_F32 = 0, GMF_F64 = 1 };
+
+/* codes match gmfkit/kernels/_ref.py:15-16 */
+enum gmf_family {
+  GMF_GAUSSIAN = 0, GMF_GAMMA = 1, GMF_INV_GAUSSIAN = 2,
+  GMF_POISSON = 3, GMF_BERNOULLI = 4, GMF_NEG_BINOMIAL = 5
+};
+enum gmf_link {
+  GMF_IDENTITY = 0, GMF_LOG = 1, GMF_LOGIT = 2, GMF_INVERSE = 3, GMF_INVERSE_SQUARED = 4
+};
+
+enum gmf_yfmt { GMF_Y_DENSE_I32 = 0, GMF_Y_CSR_I32 = 1 };
+
+/* ---------------------------------------------------------------- level 1 */
+
+/* mu = g^{-1}(eta), n entries of `dtype`. */
+int gmf_mean_of_eta(int lcode, int dtype, const void* eta, void* mu, int64_t n,
+                    void* stream);
+
+/* dotd = -w (y - mu) / (phi nu g'), ddotd = w / (phi nu g'^2) (Fisher form).
+ * w may be NULL (all ones).  Never raises on non-finite values. */
+int gmf_derivs_from_mu(int fcode, int lcode, int dtype, const void* y, const void* mu,
+                       const void* w, int64_t n, double phi, double alpha,
+                       void* dotd, void* ddotd, void* stream);
+
+/* *dev_sum (device double) = sum_k w_k D(y_k, mu_k), fixed-order reduction.
+ * `work` is device scratch of gmf_reduce_work_bytes(n) bytes. */
+int64_t gmf_reduce_work_bytes(int64_t n);
+int gmf_deviance_from_mu(int fcode, int dtype, const void* y, const void* mu,
+                         const void* w, int64_t n, double alpha, double* dev_sum,
+                         void* work, void* stream);
+
+/* ---------------------------------------------------------------- level 2 */
+
+typedef struct gmf_handle gmf_handle;
+
+typedef struct gmf_desc {
+  int64_t n;            /* rows held by this rank (block-major order)          */
+  int64_t m;            /* columns                                             */
+  int32_t p, q, d;      /* row design X (n x p), column design Z (m x q), rank */
+  int32_t dtype;        /* GMF_F32 | GMF_F64: parameters and block arithmetic  */
+  int32_t family, link; /* fused path: (POISSON|NEG_BINOMIAL, LOG)             */
+  int32_t y_format;     /* gmf_yfmt                                            */
+  int32_t has_offset;   /* per-row offset in eta (BASELINE extension)          */
+  int32_t has_weights;  /* dense n x m prior weights (dense Y only)            */
+  int32_t world_size;   /* ranks sharing every row block (1 = single GPU)      */
+  int32_t rank;
+  int32_t device;       /* CUDA device ordinal                                 */
+  int32_t reserved;
+} gmf_desc;
+
+typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py:193-226) */
+  double rate_k0, rate_k1, rate_tau;
+  double smooth_a1, smooth_a2;
+  double damping, tol;
+  double lam_b, lam_gamma, lam_u, lam_v;
+  double nb_floor, nb_ceiling;   /* optim.py:57-58 */
+  double phi;                    /* fixed dispersion (Poisson / NB under "auto") */
+  double eval_scale;             /* total / cap of the tracked sample (optim.py:271) */
+  int64_t max_epochs;
+  int32_t est_alpha;             /* NB shape estimated (optim.py:156-168) */
+  int32_t snapshot_stride;       /* 4 (optim.py:309) */
+} gmf_config;
+
+typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
+  const int32_t* y_dense;     /* n x m                          (DENSE_I32) */
+  const int64_t* csr_ptr;     /* n + 1                          (CSR_I32)   */
+  const int32_t* csr_col;     /* nnz, sorted within a row                   */
+  const int32_t* csr_val;     /* nnz                                        */
+  const void* weights;        /* n x m or NULL                              */
+  const void* x;              /* n x p                                      */
+  const void* z;              /* m x q                                      */
+  const void* offset;         /* n or NULL                                  */
+  void* theta_row;            /* n x (q+d): [gamma | u]                     */
+  void* theta_col;            /* m x (p+d): [b | v]                         */
+  void* gbar_row;             /* n x (q+d)  EMA of gradients               */
+  void* hbar_row;
+  void* gbar_col;             /* m x (p+d)                                  */
+  void* hbar_col;
+  void* snap_row;             /* n x (q+d) divergence snapshot              */
+  void* snap_col;             /* m x (p+d)                                  */
+  const int64_t* row_block_ptr;   /* R + 1 offsets of the local row blocks  */
+  const double* row_block_scale;  /* R: n_global / |I_r global| (s_col)     */
+  int64_t n_row_blocks;           /* R                                      */
+  const int32_t* col_idx;         /* m: column blocks concatenated          */
+  const int64_t* col_block_ptr;   /* S + 1                                  */
+  const int32_t* col_pos;         /* m: position of column j in its block   */
+  const int32_t* col_block_of;    /* m: block of column j                   */
+  int64_t n_col_blocks;           /* S                                      */
+  const int32_t* block_seq;       /* max_steps row-block draws (host RNG)   */
+  int64_t max_steps;              /* max_epochs * S                         */
+  const int64_t* eval_row;        /* E local tracked-objective entries      */
+  const int32_t* eval_col;
+  int64_t n_eval;
+} gmf_buffers;
+
+typedef struct gmf_status {
+  int64_t t;              /* steps applied                                    */
+  int64_t trace_len;      /* objective_trace entries (epochs_run + 1)         */
+  int64_t snapshot_trace_len;
+  double nb_shape;
+  double phi;
+  double last_objective;
+  int32_t converged;
+  int32_t diverged;       /* non-finite objective after an epoch              */
+  int32_t diverged_init;  /* non-finite at the initial state                  */
+  int32_t stopped;        /* converged | diverged | max_epochs reached        */
+} gmf_status;
+
+int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* bufs,
+               gmf_handle** out);
+int gmf_destroy(gmf_handle* h);
+
+/* Start a fit: t = 0, EMA zeroed, trace cleared, dirty marks reset,
+ * per-block row-norm sums recomputed. */
+int gmf_reset(gmf_handle* h, double nb_shape, void* stream);
+
+/* Standalone fused block gradient (no state change).  Outputs in dtype:
+ * g_row/h_row (|I_r| x (q+d)), g_col/h_col (|J_s| x (p+d)); nb_sums (device,
+ * 2 doubles, may be NULL) = (sum w mu^2, sum w((y-mu)^2 - mu)).
+ * nb_shape is the NB alpha used for the block (ignored for Poisson). */
+int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, double nb_shape,
+                       void* g_row, void* h_row, void* g_col, void* h_col,
+                       double* nb_sums, void* stream);
+
+/* One aSGD step split at the cross-rank exchange.  After gmf_step_local the
+ * rank record (gmf_record_ptr, gmf_record_bytes) holds this rank's column-side
+ * partials, NB sums and objective partials.  gmf_step_apply takes the records
+ * of all ranks concatenated in rank order (`gathered`; NULL when world_size
+ * is 1).  Both are no-ops once the fit has stopped. */
+int gmf_step_local(gmf_handle* h, void* stream);
+int gmf_step_apply(gmf_handle* h, const void* gathered, void* stream);
+void* gmf_record_ptr(gmf_handle* h);
+int64_t gmf_record_bytes(gmf_handle* h);
+/* device-to-device copy of this rank's record into `dst` (record_bytes) */
+int gmf_record_copy(gmf_handle* h, void* dst, void* stream);
+
+/* Single-rank convenience: n_steps x (local + apply), replayed from a CUDA
+ * graph captured on first use (chunk of `graph_steps` steps). */
+int gmf_run(gmf_handle* h, int64_t n_steps, void* stream);
+
+int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream);   /* syncs stream */
+/* host copies of the first n trace entries (objective, nb shape) */
+int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);
+
+/* Deviance half of penalized_objective over ALL local entries at the current
+ * state: *dev_sum (device double) = sum_ij w_ij D(y_ij, mu_ij). */
+int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream);
+
+/* ---------------------------------------------------------------- level 3 */
+
+/* out (host or device, a x b doubles, row-major) = A' B where A is rows x a
+ * (row stride lda, column offset a0) and B is rows x b (ldb, b0); dtype
+ * elements, fp64 accumulation, fixed-order reduction.  `work` is device
+ * scratch of gmf_cross_work_bytes(a, b) bytes. */
+int64_t gmf_cross_work_bytes(int32_t a, int32_t b);
+int gmf_cross_rows(int dtype, int64_t rows, const void* A, int64_t lda, int32_t a0, int32_t a,
+                   const void* B, int64_t ldb, int32_t b0, int32_t b, double* out_device,
+                   void* work, void* stream);
+
+/* Y[:, y0:y0+c] <- beta * Y[:, y0:y0+c] + A[:, a0:a0+a] @ M   (M: a x c doubles,
+ * device, row-major); row-local, so Y may alias A. */
+int gmf_rows_affine(int dtype, int64_t rows, void* Y, int64_t ldy, int32_t y0, int32_t c,
+                    double beta, const void* A, int64_t lda, int32_t a0, int32_t a,
+                    const double* M, void* stream);
+
+const char* gmf_last_error(void);
+const char* gmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMF_ASGD_H */

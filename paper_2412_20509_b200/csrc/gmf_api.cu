@@ -1,0 +1,398 @@
+// Level-2 C ABI: the aSGD fit engine handle (create / reset / step / run /
+// status), replacing the step loop of gmfkit optim.fit_asgd (optim.py:383-489).
+#include <math.h>
+#include <string.h>
+
+#include <map>
+#include <vector>
+
+#include "gmf_engine.cuh"
+
+namespace gmf {
+int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
+                double xalpha);
+int prepare_grad(int dtype, int fam, int NK);
+int grad_bucket(int KA);
+int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc);
+int launch_obj(const Params& P, int dtype, cudaStream_t st);
+int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t st);
+int launch_blocknorm(const Params& P, int dtype, cudaStream_t st);
+int launch_gradout(const Params& P, int dtype, long long blk, long long sidx, int64_t nI,
+                   int64_t nJ, void* g_row, void* h_row, void* g_col, void* h_col,
+                   double* nb_sums, cudaStream_t st);
+int launch_objfull(const Params& P, int dtype, double alpha, double* part, unsigned int* ticket,
+                   double* out, cudaStream_t st);
+}  // namespace gmf
+
+using namespace gmf;
+
+struct gmf_handle {
+  gmf_desc desc;
+  gmf_config cfg;
+  gmf_buffers bufs;
+  Params P;
+  int NK;
+  int tsz;
+  void* ws = nullptr;
+  double* full_part = nullptr;
+  unsigned int* full_ticket = nullptr;
+  Ctrl* host_ctrl = nullptr;   // pinned
+  cudaStream_t internal = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::map<int64_t, cudaGraphExec_t> graphs;
+  std::vector<int64_t> rbp_host, cbp_host;
+  bool reset_done = false;
+};
+
+namespace {
+
+int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
+
+int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
+  if (!d || !c || !b) { set_error("null descriptor"); return GMF_ERR_CONFIG; }
+  if (d->m < 1 || d->n < 0) { set_error("bad shape n=%lld m=%lld", (long long)d->n, (long long)d->m); return GMF_ERR_CONFIG; }
+  if (d->p < 0 || d->q < 0 || d->d < 0) { set_error("negative p/q/d"); return GMF_ERR_CONFIG; }
+  if (d->dtype != GMF_F32 && d->dtype != GMF_F64) { set_error("unknown dtype %d", d->dtype); return GMF_ERR_CONFIG; }
+  if (d->link != GMF_LOG || (d->family != GMF_POISSON && d->family != GMF_NEG_BINOMIAL)) {
+    set_error("fused aSGD path supports poisson/neg_binomial with log link (family %d, link %d)",
+              d->family, d->link);
+    return GMF_ERR_UNSUPPORTED;
+  }
+  if (d->y_format == GMF_Y_DENSE_I32) {
+    if (!b->y_dense && d->n > 0) { set_error("dense Y pointer is NULL"); return GMF_ERR_CONFIG; }
+  } else if (d->y_format == GMF_Y_CSR_I32) {
+    if (!b->csr_ptr) { set_error("CSR row pointer is NULL"); return GMF_ERR_CONFIG; }
+  } else { set_error("unknown y_format %d", d->y_format); return GMF_ERR_CONFIG; }
+  if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) { set_error("bad rank/world"); return GMF_ERR_CONFIG; }
+  if (b->n_row_blocks < 1 || b->n_col_blocks < 1 || b->max_steps < 0) { set_error("empty schedule"); return GMF_ERR_CONFIG; }
+  if (c->smooth_a1 <= 0 || c->smooth_a1 > 1 || c->smooth_a2 <= 0 || c->smooth_a2 > 1) { set_error("smoothing out of (0,1]"); return GMF_ERR_CONFIG; }
+  if (c->tol <= 0 || c->damping < 0 || c->phi <= 0) { set_error("need tol > 0, damping >= 0, phi > 0"); return GMF_ERR_CONFIG; }
+  if (c->snapshot_stride < 1) { set_error("snapshot_stride < 1"); return GMF_ERR_CONFIG; }
+  return GMF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* bufs,
+               gmf_handle** out) {
+  if (!out) { set_error("null out"); return GMF_ERR_CONFIG; }
+  *out = nullptr;
+  int rc = validate(desc, cfg, bufs);
+  if (rc) return rc;
+  GMF_CUDA(cudaSetDevice(desc->device));
+  gmf_handle* h = new gmf_handle();
+  h->desc = *desc;
+  h->cfg = *cfg;
+  h->bufs = *bufs;
+  const int p = desc->p, q = desc->q, d = desc->d;
+  const int Kr = q + d, Kc = p + d, KA = p + q + d;
+  h->NK = grad_bucket(KA);
+  if (h->NK < 0) {
+    set_error("p+q+d = %d exceeds the fused kernel's 32-feature limit", KA);
+    delete h;
+    return GMF_ERR_UNSUPPORTED;
+  }
+  h->tsz = desc->dtype == GMF_F64 ? 8 : 4;
+  const int64_t R = bufs->n_row_blocks, S = bufs->n_col_blocks;
+  h->rbp_host.resize(R + 1);
+  h->cbp_host.resize(S + 1);
+  GMF_CUDA(cudaMemcpy(h->rbp_host.data(), bufs->row_block_ptr, (R + 1) * 8, cudaMemcpyDeviceToHost));
+  GMF_CUDA(cudaMemcpy(h->cbp_host.data(), bufs->col_block_ptr, (S + 1) * 8, cudaMemcpyDeviceToHost));
+  int64_t nstar_max = 1, jmax = 1;
+  for (int64_t r = 0; r < R; ++r) {
+    const int64_t sz = h->rbp_host[r + 1] - h->rbp_host[r];
+    if (sz < 0) { set_error("row_block_ptr not monotone"); delete h; return GMF_ERR_CONFIG; }
+    nstar_max = sz > nstar_max ? sz : nstar_max;
+  }
+  if (h->rbp_host[R] != desc->n) { set_error("row blocks cover %lld rows, n = %lld", (long long)h->rbp_host[R], (long long)desc->n); delete h; return GMF_ERR_CONFIG; }
+  for (int64_t s = 0; s < S; ++s) {
+    const int64_t sz = h->cbp_host[s + 1] - h->cbp_host[s];
+    if (sz < 1) { set_error("empty column block"); delete h; return GMF_ERR_CONFIG; }
+    jmax = sz > jmax ? sz : jmax;
+  }
+  int col_identity = 0;
+  if (S == 1 && h->cbp_host[1] == desc->m) {
+    std::vector<int32_t> ci(desc->m);
+    GMF_CUDA(cudaMemcpy(ci.data(), bufs->col_idx, desc->m * 4, cudaMemcpyDeviceToHost));
+    col_identity = 1;
+    for (int64_t j = 0; j < desc->m; ++j)
+      if (ci[j] != (int32_t)j) { col_identity = 0; break; }
+  }
+  if (!col_identity && (!bufs->col_idx || !bufs->col_pos || !bufs->col_block_of)) {
+    set_error("column block maps are NULL"); delete h; return GMF_ERR_CONFIG;
+  }
+
+  Params& P = h->P;
+  memset(&P, 0, sizeof(P));
+  P.n = desc->n; P.m = desc->m; P.p = p; P.q = q; P.d = d; P.KA = KA; P.Kr = Kr; P.Kc = Kc;
+  P.fam = desc->family; P.yfmt = desc->y_format; P.has_w = desc->has_weights && bufs->weights;
+  P.has_off = desc->has_offset && bufs->offset;
+  P.y = bufs->y_dense; P.rp = bufs->csr_ptr; P.ci = bufs->csr_col; P.cv = bufs->csr_val;
+  P.w = bufs->weights; P.x = bufs->x; P.z = bufs->z; P.off = bufs->offset;
+  P.th_row = bufs->theta_row; P.th_col = bufs->theta_col;
+  P.gb_row = bufs->gbar_row; P.hb_row = bufs->hbar_row; P.gb_col = bufs->gbar_col; P.hb_col = bufs->hbar_col;
+  P.sn_row = bufs->snap_row; P.sn_col = bufs->snap_col;
+  P.rbp = bufs->row_block_ptr; P.rbscale = bufs->row_block_scale; P.R = R;
+  P.cidx = bufs->col_idx; P.cbp = bufs->col_block_ptr; P.cpos = bufs->col_pos; P.cbof = bufs->col_block_of;
+  P.S = S; P.col_identity = col_identity;
+  P.bseq = bufs->block_seq; P.max_steps = bufs->max_steps;
+  P.erow = bufs->eval_row; P.ecol = bufs->eval_col; P.E = bufs->n_eval;
+  P.a1 = cfg->smooth_a1; P.a2 = cfg->smooth_a2; P.damp = cfg->damping; P.tol = cfg->tol;
+  P.lam_b = cfg->lam_b; P.lam_g = cfg->lam_gamma; P.lam_u = cfg->lam_u; P.lam_v = cfg->lam_v;
+  P.nbfloor = cfg->nb_floor; P.nbceil = cfg->nb_ceiling; P.escale = cfg->eval_scale; P.phi = cfg->phi;
+  P.est_alpha = cfg->est_alpha && desc->family == GMF_NEG_BINOMIAL;
+  P.snap_stride = cfg->snapshot_stride; P.world = desc->world_size;
+
+  P.CT = (int)((jmax + TC - 1) / TC);
+  const int64_t nchunks = (nstar_max + TR - 1) / TR;
+  int64_t RS = (2 * kSMs + P.CT - 1) / P.CT;
+  if (RS > nchunks) RS = nchunks;
+  if (RS < 1) RS = 1;
+  P.RS = (int)RS;
+  P.nstar_max = nstar_max;
+  P.jmax = jmax;
+  int64_t nrc = (nstar_max * Kr + kThreads - 1) / kThreads;
+  P.n_row_ctas = (int)(nrc > 0 ? nrc : 1);
+  int64_t ncc = (desc->m * Kc + kThreads - 1) / kThreads;
+  P.n_col_ctas = (int)(ncc > 0 ? ncc : 1);
+  int64_t noc = (bufs->n_eval + kThreads - 1) / kThreads;
+  P.n_obj_ctas = (int)(noc < 1 ? 1 : (noc > 2 * kSMs ? 2 * kSMs : noc));
+
+  // ---- workspace carve-up ----
+  const int64_t max_epochs = cfg->max_epochs;
+  const int64_t ms = bufs->max_steps > 0 ? bufs->max_steps : 1;
+  const int64_t rec_bytes = align256((int64_t)REC_HDR * 8 + jmax * 2 * Kc * h->tsz);
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) { int64_t o = off; off = align256(off + bytes); return o; };
+  const int64_t o_ctrl = take(sizeof(Ctrl));
+  const int64_t o_tobj = take((max_epochs + 2) * 8);
+  const int64_t o_tnb = take((max_epochs + 2) * 8);
+  const int64_t o_rowp = take((int64_t)P.CT * nstar_max * 2 * Kr * h->tsz);
+  const int64_t o_colp = take((int64_t)P.CT * P.RS * TC * 2 * Kc * h->tsz);
+  const int64_t o_nbp = take((int64_t)P.CT * P.RS * 2 * 8);
+  const int64_t o_tick = take((int64_t)(2 * P.CT + 4) * 4);
+  const int64_t o_rec = take(rec_bytes);
+  const int64_t o_objp = take((int64_t)P.n_obj_ctas * 8);
+  const int64_t o_rnp = take((int64_t)P.n_row_ctas * 2 * 8);
+  const int64_t o_bs = take(R * 2 * 8);
+  const int64_t o_lm = take(R * 8);
+  const int64_t o_rho = take(ms * 8);
+  const int64_t o_alp = take(ms * 8);
+  const int64_t o_fp = take(2 * kSMs * 8);
+  const int64_t o_ft = take(64);
+  cudaError_t e = cudaMalloc(&h->ws, off);
+  if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
+  char* base = (char*)h->ws;
+  P.ctrl = (Ctrl*)(base + o_ctrl);
+  P.trace_obj = (double*)(base + o_tobj);
+  P.trace_nb = (double*)(base + o_tnb);
+  P.rowpart = base + o_rowp;
+  P.colpart = base + o_colp;
+  P.nbpart = (double*)(base + o_nbp);
+  P.tickets = (unsigned int*)(base + o_tick);
+  P.rec = (double*)(base + o_rec);
+  P.rec_stride = rec_bytes;
+  P.objpart = (double*)(base + o_objp);
+  P.rnpart = (double*)(base + o_rnp);
+  P.blocksum = (double*)(base + o_bs);
+  P.last_mod = (long long*)(base + o_lm);
+  P.rho_tab = (double*)(base + o_rho);
+  P.alpt_tab = (double*)(base + o_alp);
+  h->full_part = (double*)(base + o_fp);
+  h->full_ticket = (unsigned int*)(base + o_ft);
+  GMF_CUDA(cudaMemset(h->ws, 0, off));
+
+  // learning-rate and bias-correction tables, host libm (optim.py:130-148)
+  std::vector<double> rho(ms), alp(ms);
+  for (int64_t t = 0; t < ms; ++t) {
+    rho[t] = cfg->rate_k0 / pow(1.0 + cfg->rate_k0 * cfg->rate_k1 * (double)t, cfg->rate_tau);
+    const double tt = (double)(t + 1);
+    alp[t] = cfg->smooth_a1 == cfg->smooth_a2
+                 ? 1.0
+                 : (1.0 - pow(cfg->smooth_a2, tt)) / (1.0 - pow(cfg->smooth_a1, tt));
+  }
+  GMF_CUDA(cudaMemcpy((void*)P.rho_tab, rho.data(), ms * 8, cudaMemcpyHostToDevice));
+  GMF_CUDA(cudaMemcpy((void*)P.alpt_tab, alp.data(), ms * 8, cudaMemcpyHostToDevice));
+
+  GMF_CUDA(cudaMallocHost(&h->host_ctrl, sizeof(Ctrl)));
+  GMF_CUDA(cudaStreamCreateWithFlags(&h->internal, cudaStreamNonBlocking));
+  GMF_CUDA(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+  GMF_CUDA(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+  rc = prepare_grad(desc->dtype, desc->family, h->NK);
+  if (rc) { gmf_destroy(h); return rc; }
+  *out = h;
+  return GMF_OK;
+}
+
+int gmf_destroy(gmf_handle* h) {
+  if (!h) return GMF_OK;
+  cudaSetDevice(h->desc.device);
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  if (h->internal) cudaStreamSynchronize(h->internal);
+  if (h->ws) cudaFree(h->ws);
+  if (h->host_ctrl) cudaFreeHost(h->host_ctrl);
+  if (h->internal) cudaStreamDestroy(h->internal);
+  if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->ev_b) cudaEventDestroy(h->ev_b);
+  delete h;
+  return GMF_OK;
+}
+
+int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  if (!(nb_shape > 0)) { set_error("nb_shape must be positive"); return GMF_ERR_DOMAIN; }
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const Params& P = h->P;
+  Ctrl c;
+  memset(&c, 0, sizeof(c));
+  c.last_snap_t = -1;
+  c.nb_shape = nb_shape;
+  c.phi = h->cfg.phi;
+  GMF_CUDA(cudaStreamSynchronize(st));
+  *h->host_ctrl = c;
+  GMF_CUDA(cudaMemcpyAsync(P.ctrl, h->host_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  GMF_CUDA(cudaMemsetAsync(P.last_mod, 0xFF, P.R * 8, st));
+  GMF_CUDA(cudaMemsetAsync(P.tickets, 0, (2 * P.CT + 4) * 4, st));
+  const int64_t rb = P.n * P.Kr * h->tsz, cb = P.m * P.Kc * h->tsz;
+  if (rb) {
+    GMF_CUDA(cudaMemsetAsync(P.gb_row, 0, rb, st));
+    GMF_CUDA(cudaMemsetAsync(P.hb_row, 0, rb, st));
+  }
+  if (cb) {
+    GMF_CUDA(cudaMemsetAsync(P.gb_col, 0, cb, st));
+    GMF_CUDA(cudaMemsetAsync(P.hb_col, 0, cb, st));
+  }
+  int rc = launch_blocknorm(P, h->desc.dtype, st);
+  if (rc) return rc;
+  GMF_CUDA(cudaStreamSynchronize(st));
+  h->reset_done = true;
+  return GMF_OK;
+}
+
+int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, double nb_shape,
+                       void* g_row, void* h_row, void* g_col, void* h_col, double* nb_sums,
+                       void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  const Params& P = h->P;
+  if (row_block < 0 || row_block >= P.R || col_block < 0 || col_block >= P.S) {
+    set_error("minibatch indices out of range");
+    return GMF_ERR_CONFIG;
+  }
+  if (!(nb_shape > 0)) { set_error("nb_shape must be positive"); return GMF_ERR_DOMAIN; }
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_grad(P, h->desc.dtype, h->NK, st, row_block, col_block, nb_shape);
+  if (rc) return rc;
+  const int64_t nI = h->rbp_host[row_block + 1] - h->rbp_host[row_block];
+  const int64_t nJ = h->cbp_host[col_block + 1] - h->cbp_host[col_block];
+  return launch_gradout(P, h->desc.dtype, row_block, col_block, nI, nJ, g_row, h_row, g_col,
+                        h_col, nb_sums, st);
+}
+
+int gmf_step_local(gmf_handle* h, void* stream) {
+  if (!h || !h->reset_done) { set_error("gmf_step_local before gmf_reset"); return GMF_ERR_STATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_obj(h->P, h->desc.dtype, st);
+  if (rc) return rc;
+  return launch_grad(h->P, h->desc.dtype, h->NK, st, -1, -1, 0.0);
+}
+
+int gmf_step_apply(gmf_handle* h, const void* gathered, void* stream) {
+  if (!h || !h->reset_done) { set_error("gmf_step_apply before gmf_reset"); return GMF_ERR_STATE; }
+  if (h->desc.world_size > 1 && !gathered) { set_error("world_size > 1 needs gathered records"); return GMF_ERR_CONFIG; }
+  return launch_apply(h->P, h->desc.dtype, gathered, (cudaStream_t)stream);
+}
+
+void* gmf_record_ptr(gmf_handle* h) { return h ? (void*)h->P.rec : nullptr; }
+int64_t gmf_record_bytes(gmf_handle* h) { return h ? h->P.rec_stride : 0; }
+
+int gmf_record_copy(gmf_handle* h, void* dst, void* stream) {
+  if (!h || !dst) { set_error("null handle/dst"); return GMF_ERR_STATE; }
+  GMF_CUDA(cudaMemcpyAsync(dst, h->P.rec, h->P.rec_stride, cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
+  return GMF_OK;
+}
+
+int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
+  if (!h || !h->reset_done) { set_error("gmf_run before gmf_reset"); return GMF_ERR_STATE; }
+  if (h->desc.world_size != 1) { set_error("gmf_run is single-rank; use step_local/step_apply"); return GMF_ERR_STATE; }
+  if (n_steps <= 0) return GMF_OK;
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t user = (cudaStream_t)stream;
+  const int64_t kChunk = 16;
+  GMF_CUDA(cudaEventRecord(h->ev_a, user));
+  GMF_CUDA(cudaStreamWaitEvent(h->internal, h->ev_a, 0));
+  int64_t left = n_steps;
+  while (left > 0) {
+    const int64_t c = left < kChunk ? left : kChunk;
+    auto it = h->graphs.find(c);
+    if (it == h->graphs.end()) {
+      cudaGraph_t g;
+      GMF_CUDA(cudaStreamBeginCapture(h->internal, cudaStreamCaptureModeThreadLocal));
+      int rc = GMF_OK;
+      for (int64_t s = 0; s < c && rc == GMF_OK; ++s) {
+        rc = launch_obj(h->P, h->desc.dtype, h->internal);
+        if (!rc) rc = launch_grad(h->P, h->desc.dtype, h->NK, h->internal, -1, -1, 0.0);
+        if (!rc) rc = launch_apply(h->P, h->desc.dtype, nullptr, h->internal);
+      }
+      cudaError_t e = cudaStreamEndCapture(h->internal, &g);
+      if (rc) return rc;
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      cudaGraphExec_t ex;
+      e = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      it = h->graphs.emplace(c, ex).first;
+    }
+    GMF_CUDA(cudaGraphLaunch(it->second, h->internal));
+    left -= c;
+  }
+  GMF_CUDA(cudaEventRecord(h->ev_b, h->internal));
+  GMF_CUDA(cudaStreamWaitEvent(user, h->ev_b, 0));
+  return GMF_OK;
+}
+
+int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
+  if (!h || !out) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  GMF_CUDA(cudaMemcpyAsync(h->host_ctrl, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  const Ctrl& c = *h->host_ctrl;
+  out->t = c.t;
+  out->trace_len = c.trace_len;
+  out->snapshot_trace_len = c.snapshot_trace_len;
+  out->nb_shape = c.nb_shape;
+  out->phi = c.phi;
+  out->last_objective = c.last_obj;
+  out->converged = c.converged;
+  out->diverged = c.diverged;
+  out->diverged_init = c.diverged_init;
+  out->stopped = c.stopped;
+  return GMF_OK;
+}
+
+int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  if (n <= 0) return GMF_OK;
+  if (n > h->cfg.max_epochs + 1) n = h->cfg.max_epochs + 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (obj) GMF_CUDA(cudaMemcpyAsync(obj, h->P.trace_obj, n * 8, cudaMemcpyDeviceToHost, st));
+  if (nb) GMF_CUDA(cudaMemcpyAsync(nb, h->P.trace_nb, n * 8, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  return GMF_OK;
+}
+
+int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
+  if (!h || !dev_sum) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  gmf_status s;
+  int rc = gmf_status_read(h, &s, stream);
+  if (rc) return rc;
+  return launch_objfull(h->P, h->desc.dtype, s.nb_shape, h->full_part, h->full_ticket, dev_sum,
+                        (cudaStream_t)stream);
+}
+
+}  // extern "C"
