@@ -193,6 +193,15 @@ int gmf_record_copy(gmf_handle* h, void* dst, void* stream);
 int gmf_run(gmf_handle* h, int64_t n_steps, void* stream);
 
 int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream);   /* syncs stream */
+/* Asynchronous D2H of the raw status word (gmf_status_raw_bytes() bytes) into
+ * host memory (pinned for true asynchrony); decode later on the host. */
+int64_t gmf_status_raw_bytes(void);
+int gmf_status_copy_async(gmf_handle* h, void* host_dst, void* stream);
+int gmf_status_decode(const void* raw, gmf_status* out);
+/* Profiling hook: average device time (CUDA events on `stream`) of `iters`
+ * launches of the fused gradient kernel K1 alone on row block `row_block`,
+ * column block 0, at the current state (no state change). */
+int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_ms, void* stream);
 /* host copies of the first n trace entries (objective, nb shape) */
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);
 

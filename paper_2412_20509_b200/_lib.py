@@ -99,6 +99,10 @@ SIGNATURES = {
     "gmf_run": (C.c_int, [_P, _i64, _P]),
     "gmf_status_read": (C.c_int, [_P, C.POINTER(GmfStatus), _P]),
     "gmf_trace_read": (C.c_int, [_P, _pd, _pd, _i64, _P]),
+    "gmf_status_raw_bytes": (_i64, []),
+    "gmf_status_copy_async": (C.c_int, [_P, _P, _P]),
+    "gmf_status_decode": (C.c_int, [_P, C.POINTER(GmfStatus)]),
+    "gmf_time_grad": (C.c_int, [_P, _i64, _i32, _pd, _P]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),
     "gmf_cross_rows": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _P, _i64, _i32, _i32,

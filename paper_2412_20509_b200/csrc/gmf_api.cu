@@ -375,6 +375,59 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
   return GMF_OK;
 }
 
+int64_t gmf_status_raw_bytes(void) { return (int64_t)sizeof(Ctrl); }
+
+int gmf_status_copy_async(gmf_handle* h, void* host_dst, void* stream) {
+  if (!h || !host_dst) { set_error("null handle/dst"); return GMF_ERR_STATE; }
+  GMF_CUDA(cudaMemcpyAsync(host_dst, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+  return GMF_OK;
+}
+
+int gmf_status_decode(const void* raw, gmf_status* out) {
+  if (!raw || !out) { set_error("null raw/out"); return GMF_ERR_STATE; }
+  Ctrl c;
+  memcpy(&c, raw, sizeof(Ctrl));
+  out->t = c.t;
+  out->trace_len = c.trace_len;
+  out->snapshot_trace_len = c.snapshot_trace_len;
+  out->nb_shape = c.nb_shape;
+  out->phi = c.phi;
+  out->last_objective = c.last_obj;
+  out->converged = c.converged;
+  out->diverged = c.diverged;
+  out->diverged_init = c.diverged_init;
+  out->stopped = c.stopped;
+  return GMF_OK;
+}
+
+int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_ms, void* stream) {
+  if (!h || !avg_ms || iters < 1) { set_error("gmf_time_grad: bad arguments"); return GMF_ERR_CONFIG; }
+  if (row_block < 0 || row_block >= h->P.R) { set_error("row block out of range"); return GMF_ERR_CONFIG; }
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  gmf_status s;
+  int rc = gmf_status_read(h, &s, stream);
+  if (rc) return rc;
+  const double alpha = s.nb_shape > 0 ? s.nb_shape : 1.0;
+  cudaEvent_t a, b;
+  GMF_CUDA(cudaEventCreate(&a));
+  GMF_CUDA(cudaEventCreate(&b));
+  rc = launch_grad(h->P, h->desc.dtype, h->NK, st, row_block, 0, alpha);   // warm
+  if (rc) return rc;
+  GMF_CUDA(cudaEventRecord(a, st));
+  for (int i = 0; i < iters && rc == GMF_OK; ++i)
+    rc = launch_grad(h->P, h->desc.dtype, h->NK, st, row_block, 0, alpha);
+  GMF_CUDA(cudaEventRecord(b, st));
+  GMF_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  GMF_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *avg_ms = ms / iters;
+  return rc;
+}
+
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream) {
   if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
   if (n <= 0) return GMF_OK;
