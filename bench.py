@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py -- aSGD matrix entries/s on BASELINE.json config 4 (the north
+star's headline workload): negative-binomial GMF, 1,300,000 x 500, rank 10,
+intercept + centred log-library-size offset, CSR int32 counts (~92% zeros),
+minibatch 10,000 rows x all 500 columns, fp32.
+
+A "step" is one aSGD step of the reference semantics (optim.py:421-476):
+one drawn row block x all columns (= one epoch, S = 1), including the tracked
+objective.  ``value`` = sum_t |I_t| * m / device time with inputs resident
+in HBM; ``e2e`` streams each step's block from pinned host memory and reads
+the step's objective back.  Run:
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); every rank
+processes its slice of the same drawn block each step (row sharding with a
+per-step all-gather of the column-side partials), timed as max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "aSGD matrix entries/sec"
+UNIT = "entries/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--e2e-steps", type=int, default=400)
+    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _peak_hbm():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.idx), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.perf_counter(), line.strip()))
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        rows = [s for (ts, s) in self.samples if t0 - 0.1 <= ts <= t1 + 0.15] or \
+               [s for _, s in self.samples[-2:]]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except Exception:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws == 1:
+        return 1, 0, 0, None
+    import torch
+    import torch.distributed as dist
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(lr)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    return ws, dist.get_rank(), lr, dist.group.WORLD
+
+
+def _k1_bytes(spec, nI, nnz_I, e):
+    """Algorithmic HBM bytes of one K1 launch: the block's
+    counts, row features and offset read once, column features read once,
+    row-side and column-side gradient partials written once."""
+    p, q, d, m = spec.p, spec.q, spec.d, spec.m
+    y = 8 * nnz_I + 8 * (nI + 1) if spec.y_format == "csr" else 4 * nI * m
+    rows = nI * e * (p + q + d + (1 if spec.offset else 0)) + nI * e * 2 * (q + d)
+    cols = m * e * (p + q + d) + m * e * 2 * (p + d)
+    return y + rows + cols
+
+
+def _step_bytes(spec, nI, nnz_I, e):
+    """Algorithmic bytes of a whole step: K1 + the EMA/update
+    traffic (read gbar, hbar, theta; write them back) of rows I and columns J."""
+    kr, kc = spec.q + spec.d, spec.p + spec.d
+    return _k1_bytes(spec, nI, nnz_I, e) + nI * e * 6 * kr + spec.m * e * 6 * kc
+
+
+def _cpu_baseline(wl, steps, time_budget=25.0):
+    """The oracle port (oracle/asgd_oracle.py, numpy + OpenBLAS) on a bounded
+    row sample of the same workload: 13 row blocks of mb_rows, same block
+    shape, fully dense fp64 as the reference stores it (model.py:46-98)."""
+    from oracle import asgd_oracle as orc
+    sp = wl.spec
+    nsub = min(sp.n, 13 * sp.mb_rows)
+    rows = np.arange(nsub)
+    y = wl.dense_f64(rows)
+    off = None if wl.offset is None else wl.offset[rows]
+    pb = orc.OProblem(y, wl.x[rows], wl.z, offset=off)
+    init = wl.init_state()
+    st = orc.OState(init["b"], init["gamma"][rows], init["u"][rows], init["v"], 1.0,
+                    init["nb_shape"])
+    cfg = orc.OConfig(max_epochs=steps, mb_rows=sp.mb_rows, mb_cols=sp.m, tol=1e-30, seed=0)
+    stamps = [time.perf_counter()]
+    fam = orc.NEG_BINOMIAL if sp.family == "neg_binomial" else orc.POISSON
+
+    class _Stop(Exception):
+        pass
+
+    def cb(t, s):
+        stamps.append(time.perf_counter())
+        if stamps[-1] - stamps[0] > time_budget:
+            raise _Stop()
+
+    try:
+        orc.fit_asgd(pb, fam, orc.LOG, (0.0, 0.0, 1.0, 0.0), cfg, st, identify=False,
+                     callback=cb, final_objective=False)
+    except _Stop:
+        pass
+    dts = np.diff(stamps)[2:] if len(stamps) > 4 else np.diff(stamps)
+    step_s = float(np.median(dts))
+    try:
+        import threadpoolctl
+        threads = max((p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()), default=1)
+    except Exception:
+        threads = os.cpu_count()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": sp.mb_rows * sp.m / step_s, "unit": UNIT, "cores": int(min(cores, threads)),
+            "kind": "port",
+            "sample": (f"oracle/asgd_oracle.py fit_asgd on rows 0..{nsub} of {sp.name} "
+                       f"({nsub // sp.mb_rows} blocks of {sp.mb_rows} x {sp.m}, dense fp64, "
+                       f"tracked objective every step), median of {len(dts)} steps"),
+            "ms_per_step": step_s * 1e3}
+
+
+def run_reference(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if ws > 1 and rank != 0:
+        return
+    from paper_2412_20509_b200 import workloads
+    wl = workloads.generate(args.config, n_rows=13 * workloads.SPECS[args.config].mb_rows)
+    steps = max(3, min(args.steps, 60))
+    cb = _cpu_baseline(wl, steps + min(args.warmup, 3), time_budget=150.0)
+    sp = wl.spec
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": 0, "steps": steps, "warmup": min(args.warmup, 3),
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload_desc(args.config), "n_sample_rows": sp.n,
+                       "mb_rows": sp.mb_rows, "m": sp.m, "d": sp.d},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _workload_desc(name):
+    return {
+        "c1": "c1: Poisson GMF 1,000 x 100, k=5, X=Z=1, dense int32, mb 100 rows x all columns, fp64",
+        "c2": "c2: NB GMF 26,472 x 500, k=15, 7-group mixture, log-library offset, dense int32, mb 2,000 rows, fp64",
+        "c3": "c3: NB GMF 100,000 x 1,000, k=10, X=[1,batch], Z=1, CSR int32 ~90% zeros, mb 5,000 rows, fp32",
+        "c4": "c4: NB GMF 1,300,000 x 500, k=10, intercept + log-library offset, CSR int32 ~92% zeros, mb 10,000 rows x all 500 columns, fp32",
+    }[name]
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2412_20509_b200 as gk
+    from paper_2412_20509_b200 import _lib, workloads
+    from paper_2412_20509_b200.engine import DeviceFit, Schedule
+    from paper_2412_20509_b200.optim import _Exchange
+
+    world, rank, local, group = _dist()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    wl = workloads.generate(args.config, device=str(dev))
+    sp = wl.spec
+    if sp.y_format == "csr":
+        data = gk.ResponseMatrix(csr=wl.csr, shape=(sp.n, sp.m))
+    else:
+        data = gk.ResponseMatrix(wl.y_dense.astype(float))
+    covs = gk.CovariateSet(x=wl.x, z=wl.z if sp.q else None, m=sp.m)
+    st = gk.FactorizationState(**wl.init_state())
+    fam = gk.NegBinomial(st.nb_shape) if sp.family == "neg_binomial" else gk.Poisson()
+    W, K, E = args.warmup, args.steps, args.e2e_steps
+    cfg = gk.SgdConfig(max_epochs=W + K + E + 8, mb_rows=sp.mb_rows, mb_cols=sp.m, tol=1e-30,
+                       seed=0)
+    sched = Schedule(sp.n, sp.m, cfg)
+    fit = DeviceFit(data, covs, fam, gk.Log(), gk.PenaltyConfig(), cfg, st, schedule=sched,
+                    offset=wl.offset, dtype=sp.dtype, device=local, world=world, rank=rank,
+                    est_alpha=sp.family == "neg_binomial")
+    fit.reset()
+    ex = _Exchange(fit, group, "device") if world > 1 else None
+
+    def steps(k):
+        if ex is None:
+            fit.run(k)
+        else:
+            for _ in range(k):
+                ex.step()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up ----
+    steps(W)
+    barrier()
+    # ---- timed region: K steps, inputs resident in HBM ----
+    props = torch.cuda.get_device_properties(dev)
+    bus = "%08X:%02X:%02X.0" % (getattr(props, "pci_domain_id", 0), getattr(props, "pci_bus_id", 0),
+                                getattr(props, "pci_device_id", 0))
+    clk = Clocks(bus)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    steps(K)
+    e1.record()
+    barrier()
+    w1 = time.perf_counter()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop(w0, w1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    status = fit.status()
+    assert status.t == W + K and not status.stopped, (status.t, status.stopped)
+    sizes = np.array([b.size for b in sched.row_blocks])
+    seq = sched.block_seq
+    entries = float(sizes[seq[W:W + K]].sum()) * sp.m
+    value = entries / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1, fused gradient) ----
+    e_sz = 8 if sp.dtype == "f64" else 4
+    blk = int(seq[W + K - 1])
+    rbp = fit.rbp.cpu().numpy()
+    if fit.csr_ptr is not None:
+        cptr = fit.csr_ptr.cpu().numpy()
+        nnz_blk = int(cptr[rbp[blk + 1]] - cptr[rbp[blk]])
+    else:
+        nnz_blk = 0
+    nI_loc = int(rbp[blk + 1] - rbp[blk])
+    import ctypes as C
+    avg = C.c_double()
+    _lib.check(fit.lib.gmf_time_grad(fit.h, blk, 200, C.byref(avg), fit.stream()), "gmf_time_grad")
+    k1_ms = avg.value
+    k1_bytes = _k1_bytes(workloads.WorkloadSpec(**{**sp.__dict__}), nI_loc, nnz_blk, e_sz)
+    peak, peak_src = _peak_hbm()
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", f"k1_traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    ms_step = ms / K
+    step_bytes = _step_bytes(sp, nI_loc, nnz_blk, e_sz)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "k_grad (K1 fused gradient)",
+                "k1_ms": k1_ms, "k1_bytes": k1_bytes, "peak_source": peak_src,
+                "step_bytes": step_bytes,
+                "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak}
+
+    # ---- e2e: stream each step's block from pinned host memory ----
+    e2e = None
+    if E > 0:
+        if fit.csr_ptr is not None:
+            h_col = fit.csr_col.cpu().pin_memory()
+            h_val = fit.csr_val.cpu().pin_memory()
+            h_ptr = fit.csr_ptr.cpu().pin_memory()
+            cptr = h_ptr.numpy()
+        else:
+            h_y = fit.y_dense.cpu().pin_memory()
+        raw = torch.empty(int(fit.lib.gmf_status_raw_bytes()), dtype=torch.uint8).pin_memory()
+        barrier()
+        h2d = 0
+        e0.record()
+        for k in range(E):
+            t = W + K + k
+            b = int(seq[t])
+            r0, r1 = int(rbp[b]), int(rbp[b + 1])
+            if fit.csr_ptr is not None:
+                a0, a1 = int(cptr[r0]), int(cptr[r1])
+                fit.csr_col[a0:a1].copy_(h_col[a0:a1], non_blocking=True)
+                fit.csr_val[a0:a1].copy_(h_val[a0:a1], non_blocking=True)
+                fit.csr_ptr[r0:r1 + 1].copy_(h_ptr[r0:r1 + 1], non_blocking=True)
+                h2d += (a1 - a0) * 8 + (r1 - r0 + 1) * 8
+            else:
+                fit.y_dense[r0:r1].copy_(h_y[r0:r1], non_blocking=True)
+                h2d += (r1 - r0) * sp.m * 4
+            steps(1)
+            _lib.check(fit.lib.gmf_status_copy_async(fit.h, C.c_void_p(raw.data_ptr()),
+                                                     fit.stream()), "status copy")
+        e1.record()
+        barrier()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t_ = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t_, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t_.item())
+        st_e = _lib.GmfStatus()
+        fit.lib.gmf_status_decode(C.c_void_p(raw.data_ptr()), C.byref(st_e))
+        assert st_e.t == W + K + E, st_e.t
+        e_entries = float(sizes[seq[W + K:W + K + E]].sum()) * sp.m
+        e2e = {"value": e_entries / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": raw.numel(),
+               "steps": E, "ms_per_step": e_ms / E,
+               "path": "C-ABI gmf_run(1) per step + cudaMemcpyAsync of the drawn block from "
+                       "pinned host + async status read-back"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(wl, max(4, args.cpu_steps))
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    fit.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": sp.dtype,
+            "data": "synthetic (seeded Gamma-Poisson NB counts with BASELINE shapes)",
+            "config": {"workload": _workload_desc(args.config), "n": sp.n, "m": sp.m,
+                       "d": sp.d, "p": sp.p, "q": sp.q, "mb_rows": sp.mb_rows,
+                       "nnz": wl.meta.get("nnz"), "zero_frac": round(wl.meta.get("zero_frac", 0), 4),
+                       "y_format": sp.y_format,
+                       "l2": "inputs (CSR %.0f MB + factors) exceed the 126 MB L2; each step draws "
+                             "a random row block" % (wl.meta.get("nnz", 0) * 8 / 1e6),
+                       "parallelism": f"rows of each block split x{world}" if world > 1 else "1 GPU"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 3 * K, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -11,7 +11,10 @@
 namespace gmf {
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha);
-int prepare_grad(int dtype, int fam, int NK);
+int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int* fit_blocks_per_sm);
+int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
+int launch_eval_y(const Params& P, int32_t* out, cudaStream_t st);
+int tile_cols(int dtype);
 int grad_bucket(int KA);
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc);
 int launch_obj(const Params& P, int dtype, cudaStream_t st);
@@ -40,6 +43,8 @@ struct gmf_handle {
   cudaStream_t internal = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::map<int64_t, cudaGraphExec_t> graphs;
+  int fit_grid = 0;             // co-resident CTAs of the persistent kernel
+  int fit_rs = 0;               // its row splits (fit_grid / CT)
   std::vector<int64_t> rbp_host, cbp_host;
   bool reset_done = false;
 };
@@ -145,6 +150,8 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.est_alpha = cfg->est_alpha && desc->family == GMF_NEG_BINOMIAL;
   P.snap_stride = cfg->snapshot_stride; P.world = desc->world_size;
 
+  const int TC = tile_cols(desc->dtype);
+  P.TC = TC;
   P.CT = (int)((jmax + TC - 1) / TC);
   const int64_t nchunks = (nstar_max + TR - 1) / TR;
   int64_t RS = (2 * kSMs + P.CT - 1) / P.CT;
@@ -160,28 +167,48 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   int64_t noc = (bufs->n_eval + kThreads - 1) / kThreads;
   P.n_obj_ctas = (int)(noc < 1 ? 1 : (noc > 2 * kSMs ? 2 * kSMs : noc));
 
+  // persistent kernel geometry: every co-resident CTA, a multiple of CT
+  int fit_bps = 0;
+  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, &fit_bps);
+  if (rc) { delete h; return rc; }
+  int n_sm = kSMs;
+  GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
+  int coop = 0;
+  GMF_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc->device));
+  h->fit_grid = coop ? (fit_bps * n_sm / P.CT) * P.CT : 0;
+  h->fit_rs = h->fit_grid / (P.CT > 0 ? P.CT : 1);
+
   // ---- workspace carve-up ----
   const int64_t max_epochs = cfg->max_epochs;
   const int64_t ms = bufs->max_steps > 0 ? bufs->max_steps : 1;
   const int64_t rec_bytes = align256((int64_t)REC_HDR * 8 + jmax * 2 * Kc * h->tsz);
+  const int64_t rs_max = P.RS > h->fit_rs ? P.RS : h->fit_rs;
+  const int64_t cta_max = [&] {
+    int64_t v = P.n_row_ctas;
+    if (P.n_obj_ctas > v) v = P.n_obj_ctas;
+    if (h->fit_grid > v) v = h->fit_grid;
+    if (P.CT * rs_max > v) v = P.CT * rs_max;
+    return v;
+  }();
   int64_t off = 0;
   auto take = [&](int64_t bytes) { int64_t o = off; off = align256(off + bytes); return o; };
   const int64_t o_ctrl = take(sizeof(Ctrl));
   const int64_t o_tobj = take((max_epochs + 2) * 8);
   const int64_t o_tnb = take((max_epochs + 2) * 8);
   const int64_t o_rowp = take((int64_t)P.CT * nstar_max * 2 * Kr * h->tsz);
-  const int64_t o_colp = take((int64_t)P.CT * P.RS * TC * 2 * Kc * h->tsz);
-  const int64_t o_nbp = take((int64_t)P.CT * P.RS * 2 * 8);
+  const int64_t o_colp = take((int64_t)P.CT * rs_max * TC * 2 * Kc * h->tsz);
+  const int64_t o_nbp = take(cta_max * 2 * 8);
   const int64_t o_tick = take((int64_t)(2 * P.CT + 4) * 4);
   const int64_t o_rec = take(rec_bytes);
-  const int64_t o_objp = take((int64_t)P.n_obj_ctas * 8);
-  const int64_t o_rnp = take((int64_t)P.n_row_ctas * 2 * 8);
+  const int64_t o_objp = take(cta_max * OBJ_W * 8);
+  const int64_t o_rnp = take(cta_max * 2 * 8);
   const int64_t o_bs = take(R * 2 * 8);
   const int64_t o_lm = take(R * 8);
   const int64_t o_rho = take(ms * 8);
   const int64_t o_alp = take(ms * 8);
   const int64_t o_fp = take(2 * kSMs * 8);
   const int64_t o_ft = take(64);
+  const int64_t o_ey = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 4);
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -203,6 +230,13 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   h->full_part = (double*)(base + o_fp);
   h->full_ticket = (unsigned int*)(base + o_ft);
   GMF_CUDA(cudaMemset(h->ws, 0, off));
+  P.ey = nullptr;
+  if (bufs->n_eval > 0) {   // Y at the fixed tracked sample, looked up once
+    rc = launch_eval_y(P, (int32_t*)(base + o_ey), 0);
+    if (rc) { gmf_destroy(h); return rc; }
+    GMF_CUDA(cudaDeviceSynchronize());
+    P.ey = (const int32_t*)(base + o_ey);
+  }
 
   // learning-rate and bias-correction tables, host libm (optim.py:130-148)
   std::vector<double> rho(ms), alp(ms);
@@ -220,8 +254,6 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   GMF_CUDA(cudaStreamCreateWithFlags(&h->internal, cudaStreamNonBlocking));
   GMF_CUDA(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
   GMF_CUDA(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
-  rc = prepare_grad(desc->dtype, desc->family, h->NK);
-  if (rc) { gmf_destroy(h); return rc; }
   *out = h;
   return GMF_OK;
 }
@@ -322,6 +354,13 @@ int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
   if (n_steps <= 0) return GMF_OK;
   GMF_CUDA(cudaSetDevice(h->desc.device));
   cudaStream_t user = (cudaStream_t)stream;
+  if (h->fit_grid > 0) {
+    // one cooperative launch runs all n_steps (grid-wide barriers between phases)
+    Params P = h->P;
+    P.RS = h->fit_rs;
+    return launch_fit(P, h->desc.dtype, h->NK, h->fit_grid, n_steps, user);
+  }
+  // fallback for devices without cooperative launch: per-step kernels in CUDA graphs
   const int64_t kChunk = 16;
   GMF_CUDA(cudaEventRecord(h->ev_a, user));
   GMF_CUDA(cudaStreamWaitEvent(h->internal, h->ev_a, 0));
@@ -361,18 +400,7 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   GMF_CUDA(cudaMemcpyAsync(h->host_ctrl, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   GMF_CUDA(cudaStreamSynchronize(st));
-  const Ctrl& c = *h->host_ctrl;
-  out->t = c.t;
-  out->trace_len = c.trace_len;
-  out->snapshot_trace_len = c.snapshot_trace_len;
-  out->nb_shape = c.nb_shape;
-  out->phi = c.phi;
-  out->last_objective = c.last_obj;
-  out->converged = c.converged;
-  out->diverged = c.diverged;
-  out->diverged_init = c.diverged_init;
-  out->stopped = c.stopped;
-  return GMF_OK;
+  return gmf_status_decode(h->host_ctrl, out);
 }
 
 int64_t gmf_status_raw_bytes(void) { return (int64_t)sizeof(Ctrl); }

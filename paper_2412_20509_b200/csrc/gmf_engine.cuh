@@ -1,22 +1,27 @@
-// Device-side state and launch parameters of the aSGD fit engine.
+// Device-side state, launch parameters and the shared per-element step
+// algebra of the aSGD fit engine.
 #pragma once
 #include "gmf_common.cuh"
 
 namespace gmf {
 
-constexpr int TC = 64;                    // columns per CTA tile (K1)
 constexpr int TR = 32;                    // rows per chunk (K1)
-constexpr int NG = kThreads / TC;         // row groups in phase 1 (4)
-constexpr int NQ = kThreads / (2 * TR);   // column quarters in phase 2 (4)
+constexpr int NQ = kThreads / (2 * TR);   // column slices in K1 phase 2 (4)
 constexpr int REC_HDR = 8;                // doubles in the rank-record header
 constexpr int kSnapCtas = 32;
+constexpr int OBJ_W = 3;                  // objective partial: (deviance, ||B||^2, ||V||^2)
+
+// column tile width of K1: 128 columns for fp32 (2 row groups of 128
+// threads), 64 for fp64 (4 row groups; register/smem budget)
+template <typename T> struct Tile { static constexpr int TC = 128; };
+template <> struct Tile<double> { static constexpr int TC = 64; };
 
 // rank record header slots (doubles)
 enum { R_DEV = 0, R_NGAM = 1, R_NU = 2, R_NB = 3, R_NV = 4, R_NBNUM = 5, R_NBDEN = 6 };
 
-// Mutable fit control block, device resident.  Read by every kernel of a
-// step; written only by the last CTA of k_apply (ticket), so its value is
-// immutable while any kernel of the step reads it.
+// Fit control block.  Per-step kernels read it at entry and only the last
+// CTA of k_apply writes it; the persistent kernel keeps an identical copy in
+// every CTA (redundant, deterministic computation) and CTA 0 publishes it.
 struct Ctrl {
   long long t;                  // steps applied
   long long trace_len;          // objective_trace entries
@@ -61,6 +66,7 @@ struct Params {
   int64_t max_steps;
   const int64_t* erow;
   const int32_t* ecol;
+  const int32_t* ey;  // Y at the tracked entries (precomputed once)
   int64_t E;
   // config
   double a1, a2, damp, tol;
@@ -79,11 +85,11 @@ struct Params {
   unsigned int* tickets;   // [CT] col tiles, [CT] grad-global, [CT+1] obj, [CT+2] apply
   double* rec;         // rank record: REC_HDR doubles + [jmax][2 Kc] T
   int64_t rec_stride;  // bytes between gathered records
-  double* objpart;     // [n_obj_ctas]
+  double* objpart;     // [n_obj_ctas][OBJ_W]
   double* rnpart;      // [n_row_ctas][2]
   double* blocksum;    // [R][2] (gamma, u) squared norms per row block
   long long* last_mod; // [R]
-  int RS, CT;
+  int TC, RS, CT;
   int64_t nstar_max, jmax;
   int n_obj_ctas, n_row_ctas, n_col_ctas;
 };
@@ -92,5 +98,114 @@ template <typename T>
 GMF_D T* tptr(void* p) { return reinterpret_cast<T*>(p); }
 template <typename T>
 GMF_D const T* tptr(const void* p) { return reinterpret_cast<const T*>(p); }
+
+template <typename T>
+GMF_D T ldcg_t(const T* p);
+template <>
+GMF_D float ldcg_t<float>(const float* p) { return __ldcg(p); }
+template <>
+GMF_D double ldcg_t<double>(const double* p) { return __ldcg(p); }
+
+// block-wide sum with the result broadcast to every thread (fixed order)
+template <int NT>
+GMF_D double block_sum_all(double v, double* scr) {
+  double s = block_sum<NT>(v, scr);
+  __syncthreads();
+  if (threadIdx.x == 0) scr[0] = s;
+  __syncthreads();
+  s = scr[0];
+  __syncthreads();
+  return s;
+}
+
+// sum of n strided partials published by other CTAs, identical in every
+// thread and every CTA that calls it (fixed assignment + fixed tree)
+template <int NT>
+GMF_D double sum_parts(const double* parts, int64_t n, int64_t stride, double* scr) {
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += NT) s += __ldcg(parts + i * stride);
+  return block_sum_all<NT>(s, scr);
+}
+
+// ---------------------------------------------------------------------------
+// tracker decision (optim.py:301-338), from objective totals
+// ---------------------------------------------------------------------------
+struct Decision {
+  double obj;
+  int boundary, snap, stop, conv, div, div_init, streak;
+};
+
+GMF_D Decision decide_from(const Params& P, const Ctrl& C, double dev, double ng, double nu,
+                           double nb, double nv) {
+  Decision D;
+  D.obj = 0.0;
+  D.boundary = (C.t % P.S) == 0;
+  D.snap = 0; D.stop = 0; D.conv = C.converged; D.div = 0; D.div_init = 0; D.streak = C.streak;
+  if (D.boundary) {
+    D.obj = P.escale * dev / (2.0 * P.phi) +
+            0.5 * (P.lam_b * nb + P.lam_g * ng + P.lam_u * nu + P.lam_v * nv);
+    if (C.t == 0) {
+      if (!isfinite(D.obj)) { D.div_init = 1; D.stop = 1; }
+      else D.snap = 1;
+    } else if (!isfinite(D.obj)) {
+      D.div = 1; D.stop = 1;
+    } else {
+      if ((C.trace_len + 1) % P.snap_stride == 0) D.snap = 1;
+      const double rel = fabs(D.obj - C.last_obj) / (fabs(C.last_obj) + 1e-12);
+      D.streak = rel < P.tol ? D.streak + 1 : 0;
+      if (D.streak >= 2) { D.conv = 1; D.stop = 1; }
+    }
+  }
+  if (C.t >= P.max_steps) D.stop = 1;
+  return D;
+}
+
+// next control block after the decision (and the step, if applied)
+GMF_D Ctrl advance(const Params& P, const Ctrl& C, const Decision& D, double nb_num,
+                   double nb_den) {
+  Ctrl N = C;
+  if (D.boundary) {
+    N.trace_len = C.trace_len + 1;
+    N.last_obj = D.obj;
+    N.streak = D.streak;
+    N.converged = D.conv;
+    N.diverged = D.div;
+    N.diverged_init = D.div_init;
+  }
+  if (D.snap) {
+    N.last_snap_t = C.t;
+    N.snapshot_trace_len = N.trace_len;
+  }
+  if (!D.stop) {
+    if (P.est_alpha) {   // optim.py:205-229
+      const double rho = P.rho_tab[C.t];
+      double ah = nb_den > 0.0 ? nb_num / nb_den : P.nbceil;
+      ah = fmin(fmax(P.nbfloor, ah), P.nbceil);
+      N.nb_shape = (1.0 - rho) * C.nb_shape + rho * ah;
+    }
+    N.t = C.t + 1;
+  }
+  N.stopped = D.stop;
+  return N;
+}
+
+// ---------------------------------------------------------------------------
+// EMA + adaptive update of one coordinate (optim.py:450-462)
+// ---------------------------------------------------------------------------
+template <typename T>
+GMF_D T ema_update(const Params& P, T* th, T* gb, T* hb, T gsum, T hsum, double scale, double lam,
+                   double rho, double at) {
+  const T old = *th;
+  const T G = T(scale) * gsum + T(lam) * old;
+  const T H = T(scale) * hsum + T(lam);
+  const T gn = (T(1) - T(P.a1)) * *gb + T(P.a1) * G;
+  const T hn = (T(1) - T(P.a2)) * *hb + T(P.a2) * H;
+  *gb = gn;
+  *hb = hn;
+  const T delta = -T(at) * gn / (hn + T(P.damp));
+  const T nv = old + T(rho) * delta;
+  *th = nv;
+  return nv;
+}
 
 }  // namespace gmf

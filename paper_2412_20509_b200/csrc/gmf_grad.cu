@@ -1,58 +1,33 @@
-// K1: fused minibatch gradient for one aSGD step (sm_100a, CUDA cores).
+// K1 (fused minibatch gradient) kernels and the persistent fit kernel.
 //
-// One CTA owns a tile of TC columns of the column block J and a contiguous
-// range of row chunks (TR rows each) of the row block I.  Per entry:
-//   eta = offset_i + [x_i|u_i|gamma_i] . [b_j|v_j|z_j]       (model.py:229-256)
-//   mu  = exp(eta)                                             (_ref.py:21-32)
-//   dotD, ddotD  (Poisson / NB with log link)                  (_core.pyx:79-103)
-// Column side  sum_i dotD_ij [x_i, u_i], ddotD_ij [x_i^2, u_i^2] accumulates in
-// registers (thread == column) across all of the CTA's rows; the row side
-// sum_j dotD_ij [z_j, v_j] (and ddotD with squares) is a small smem GEMM over
-// the chunk's P tile (gradients.py:102-113).  eta and mu never leave
-// registers; P lives only in shared memory.  Cross-CTA reductions are
-// fixed-order (determinism contract): per-CTA partials plus a
-// "last CTA" ticket, never float atomics.
-#include "gmf_engine.cuh"
+//  * k_grad  -- one launch per step (multi-rank path and the standalone
+//               minibatch_gradients): K1 tiles + fixed-order reductions into
+//               the rank record via "last CTA" tickets.
+//  * k_fit   -- single-rank path: ONE cooperative launch runs many aSGD steps;
+//               every step is phase 1 (tracked objective partials + K1 tiles),
+//               a grid-wide barrier, phase 2 (tracker decision computed
+//               redundantly in every CTA, EMA/adaptive updates of rows I and
+//               columns J, NB shape), and a second barrier.  Steps are
+//               microseconds long and strictly sequential through V, so
+//               removing per-kernel launch/drain gaps is the first-order win.
+#include <cooperative_groups.h>
+
+#include "gmf_kern.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gmf {
 
-struct GradSmem {
-  int64_t rd, a, cd2, off, y, w, P, red, cp, total;
-};
-
-// byte offsets of the dynamic shared-memory carve-up (host + device)
-GMF_HD GradSmem grad_smem(int NK, int tsz, int has_w, int Kr, int Kc) {
-  GradSmem s;
-  int64_t o = 0;
-  auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
-  s.rd = o; o = al(o + (int64_t)2 * TC * NK * tsz);
-  s.P = o; o = al(o + (int64_t)2 * TC * (TR + 1) * tsz);
-  const int64_t region = o;
-  int64_t r = region;
-  s.a = r; r = al(r + (int64_t)TR * NK * tsz);
-  s.cd2 = r; r = al(r + (int64_t)TR * NK * tsz);
-  s.off = r; r = al(r + (int64_t)TR * tsz);
-  s.y = r; r = al(r + (int64_t)TR * TC * tsz);
-  s.w = r; r = al(r + (has_w ? (int64_t)TR * TC * tsz : 0));
-  const int64_t p1 = r - region;
-  const int64_t red = al((int64_t)NQ * 2 * Kr * (TR + 1) * tsz);
-  const int64_t cp = al((int64_t)TC * (2 * Kc + 1) * tsz);
-  s.red = region;
-  s.cp = region;
-  int64_t mx = p1 > red ? p1 : red;
-  mx = mx > cp ? mx : cp;
-  s.total = region + mx;
-  return s;
-}
+template <typename T> struct MinBlocks { static constexpr int v = 2; };
+template <> struct MinBlocks<double> { static constexpr int v = 1; };
 
 template <typename T, int FAM, int NK>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
 k_grad(Params P, long long xb, long long xs, double xalpha) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red_scr[kThreads / 32];
-  const int tid = threadIdx.x;
+  __shared__ double scr[kThreads / 32];
+  constexpr int TC = Tile<T>::TC;
   const Ctrl* C = P.ctrl;
-
   long long blk, s;
   double alpha;
   if (xb >= 0) {
@@ -64,254 +39,31 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
     s = t % P.S;
     alpha = C->nb_shape;
   }
-  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
-  const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
-  const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
   const int ct = blockIdx.y, rs = blockIdx.x, RS = gridDim.x;
-  const int64_t nchunks = (nI + TR - 1) / TR;
-  const int64_t cpr = (nchunks + RS - 1) / RS;
-  const int64_t ch_lo = rs * cpr, ch_hi = ch_lo + cpr < nchunks ? ch_lo + cpr : nchunks;
+  grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
 
-  const GradSmem L = grad_smem(NK, sizeof(T), P.has_w, Kr, Kc);
-  T* rd_s = reinterpret_cast<T*>(smem + L.rd);
-  T* P_s = reinterpret_cast<T*>(smem + L.P);
-  T* a_s = reinterpret_cast<T*>(smem + L.a);
-  T* cd2_s = reinterpret_cast<T*>(smem + L.cd2);
-  T* off_s = reinterpret_cast<T*>(smem + L.off);
-  T* y_s = reinterpret_cast<T*>(smem + L.y);
-  T* w_s = reinterpret_cast<T*>(smem + L.w);
-  T* red_s = reinterpret_cast<T*>(smem + L.red);
-  T* cp_s = reinterpret_cast<T*>(smem + L.cp);
-
-  const T* th_row = tptr<T>(P.th_row);
-  const T* th_col = tptr<T>(P.th_col);
-  const T* xg = tptr<T>(P.x);
-  const T* zg = tptr<T>(P.z);
-  const T* offg = tptr<T>(P.off);
-  const T* wg = tptr<T>(P.w);
-
-  // ---- column features of this thread's column (phase 1) ----
-  const int c = tid % TC, g = tid / TC;
-  const int64_t pos = (int64_t)ct * TC + c;
-  const bool col_ok = pos < nJ;
-  const int64_t j = col_ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
-  T cf[NK];
-  #pragma unroll
-  for (int k = 0; k < NK; ++k) {
-    T v = T(0);
-    if (col_ok) {
-      if (k < Kc) v = th_col[j * Kc + k];
-      else if (k < KA) v = zg[j * q + (k - Kc)];
-    }
-    cf[k] = v;
-  }
-  // ---- row-side design [z_j | v_j] and squares for the tile (phase 2) ----
-  for (int e = tid; e < TC * NK; e += kThreads) {
-    const int cc = e / NK, k = e % NK;
-    const int64_t pp = (int64_t)ct * TC + cc;
-    T v = T(0);
-    if (pp < nJ && k < Kr) {
-      const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
-      v = k < q ? zg[jj * q + k] : th_col[jj * Kc + p + (k - q)];
-    }
-    rd_s[cc * NK + k] = v;
-    rd_s[(TC + cc) * NK + k] = v * v;
-  }
-
-  T gacc[NK], hacc[NK];
-  #pragma unroll
-  for (int k = 0; k < NK; ++k) { gacc[k] = T(0); hacc[k] = T(0); }
-  double nb_num = 0.0, nb_den = 0.0;
-  const T rphi = T(1.0 / P.phi);
-  const T ralpha = T(1.0 / alpha);
-
-  // phase-2 role
-  const int pr = tid % TR, ph = (tid / TR) & 1, pq = tid / (2 * TR);
-  constexpr int TCQ = TC / NQ;
-  const int rkk = 2 * Kr;
-
-  for (int64_t ch = ch_lo; ch < ch_hi; ++ch) {
-    const int64_t rowbase = ch * TR;                       // within block
-    const int rows = (int)((nI - rowbase) < TR ? (nI - rowbase) : TR);
-    __syncthreads();   // previous chunk's red_s reads are done
-    // ---- load row features [x | u | gamma], squares, offset ----
-    for (int e = tid; e < TR * NK; e += kThreads) {
-      const int rr = e / NK, k = e % NK;
-      T v = T(0);
-      if (rr < rows) {
-        const int64_t i = r0 + rowbase + rr;
-        if (k < p) v = xg[i * p + k];
-        else if (k < p + d) v = th_row[i * Kr + q + (k - p)];
-        else if (k < KA) v = th_row[i * Kr + (k - p - d)];
-      }
-      a_s[rr * NK + k] = v;
-      cd2_s[rr * NK + k] = k < Kc ? v * v : T(0);
-    }
-    if (tid < TR) {
-      T v = T(0);
-      if (tid < rows && P.has_off) v = offg[r0 + rowbase + tid];
-      off_s[tid] = v;
-    }
-    // ---- response tile ----
-    if (P.yfmt == GMF_Y_DENSE_I32) {
-      for (int e = tid; e < TR * TC; e += kThreads) {
-        const int rr = e / TC, cc = e % TC;
-        const int64_t pp = (int64_t)ct * TC + cc;
-        T v = T(0), wv = T(0);
-        if (rr < rows && pp < nJ) {
-          const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
-          const int64_t i = r0 + rowbase + rr;
-          v = (T)P.y[i * P.m + jj];
-          if (P.has_w) wv = wg[i * P.m + jj];
-        }
-        y_s[e] = v;
-        if (P.has_w) w_s[e] = wv;
-      }
-    } else {
-      for (int e = tid; e < TR * TC; e += kThreads) y_s[e] = T(0);
-      __syncthreads();
-      const int lane = tid & 31, warp = tid >> 5;
-      for (int rr = warp; rr < rows; rr += kThreads / 32) {
-        const int64_t i = r0 + rowbase + rr;
-        const int64_t a = P.rp[i], b = P.rp[i + 1];
-        for (int64_t k = a + lane; k < b; k += 32) {
-          const int col = P.ci[k];
-          int64_t pp;
-          if (P.col_identity) pp = col;
-          else pp = (P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1;
-          const int64_t cl = pp - (int64_t)ct * TC;
-          if (pp >= 0 && cl >= 0 && cl < TC) y_s[rr * TC + cl] = (T)P.cv[k];
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- phase 1: eta, mu, dotD, ddotD; column side in registers ----
-    T cn = T(0), cd = T(0);
-    #pragma unroll 2
-    for (int rr = g; rr < TR; rr += NG) {
-      const T* a = a_s + rr * NK;
-      T eta = off_s[rr];
-      #pragma unroll
-      for (int k = 0; k < NK; ++k) eta = fma(a[k], cf[k], eta);
-      const T mu = exp_t(eta);
-      const T yv = y_s[rr * TC + c];
-      const T wv = P.has_w ? w_s[rr * TC + c] : T(1);
-      const T r = yv - mu;
-      T dd, hh;
-      if (FAM == 0) {
-        dd = -wv * r * rphi;
-        hh = wv * mu * rphi;
-      } else {
-        const T inv = rcp_t(T(P.phi) * fma(mu, ralpha, T(1)));
-        dd = -wv * r * inv;
-        hh = wv * mu * inv;
-      }
-      const bool ok = col_ok && rr < rows;
-      if (!ok) { dd = T(0); hh = T(0); }
-      const T* a2 = cd2_s + rr * NK;
-      #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        gacc[k] = fma(dd, a[k], gacc[k]);
-        hacc[k] = fma(hh, a2[k], hacc[k]);
-      }
-      P_s[c * (TR + 1) + rr] = dd;
-      P_s[(TC + c) * (TR + 1) + rr] = hh;
-      if (FAM == 1 && ok) {
-        cn = fma(wv * mu, mu, cn);
-        cd = fma(wv, fma(r, r, -mu), cd);
-      }
-    }
-    nb_num += (double)cn;
-    nb_den += (double)cd;
-    __syncthreads();
-
-    // ---- phase 2: row side  P (TR x TC) . rd (TC x Kr) ----
-    T acc[NK];
-    #pragma unroll
-    for (int k = 0; k < NK; ++k) acc[k] = T(0);
-    {
-      const T* Pp = P_s + ph * TC * (TR + 1);
-      const T* rdp = rd_s + ph * TC * NK;
-      #pragma unroll 4
-      for (int cc = pq * TCQ; cc < (pq + 1) * TCQ; ++cc) {
-        const T pv = Pp[cc * (TR + 1) + pr];
-        const T* rd = rdp + cc * NK;
-        #pragma unroll
-        for (int k = 0; k < NK; ++k) acc[k] = fma(pv, rd[k], acc[k]);
-      }
-    }
-    // red_s aliases the phase-1 tile region: every thread finished phase 1
-    // before the barrier above, so it is free now.
-    #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < Kr) red_s[((pq * 2 + ph) * Kr + k) * (TR + 1) + pr] = acc[k];
-    __syncthreads();
-    {
-      T* outp = tptr<T>(P.rowpart) + ((int64_t)ct * P.nstar_max + rowbase) * rkk;
-      for (int o = tid; o < rows * rkk; o += kThreads) {
-        const int rr = o / rkk, hk = o % rkk;
-        const int h = hk / Kr, k = hk % Kr;
-        T sum = T(0);
-        #pragma unroll
-        for (int qq = 0; qq < NQ; ++qq) sum += red_s[((qq * 2 + h) * Kr + k) * (TR + 1) + rr];
-        outp[o] = sum;
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- column partials: fixed-order sum over the NG row groups ----
-  const int ck = 2 * Kc + 1;
-  for (int round = 0; round < NG; ++round) {
-    if (g == round) {
-      #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        if (k < Kc) {
-          if (round == 0) { cp_s[c * ck + k] = gacc[k]; cp_s[c * ck + Kc + k] = hacc[k]; }
-          else { cp_s[c * ck + k] += gacc[k]; cp_s[c * ck + Kc + k] += hacc[k]; }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  const int kk = 2 * Kc;
-  T* colpart = tptr<T>(P.colpart);
-  const int64_t cbase = ((int64_t)ct * RS + rs) * TC * kk;
-  for (int e = tid; e < TC * kk; e += kThreads) colpart[cbase + e] = cp_s[(e / kk) * ck + (e % kk)];
-
-  // NB moment partials (optim.py:225-226)
-  const double bn = block_sum<kThreads>(nb_num, red_scr);
-  const double bd = block_sum<kThreads>(nb_den, red_scr);
-  if (tid == 0) {
-    P.nbpart[2 * ((int64_t)ct * RS + rs)] = bn;
-    P.nbpart[2 * ((int64_t)ct * RS + rs) + 1] = bd;
-  }
-
-  // ---- last CTA of this column tile: rank-level column partial ----
+  const int64_t nJ = P.cbp[s + 1] - P.cbp[s];
+  const int kk = 2 * P.Kc;
+  // last CTA of this column tile: rank-level column partial (parallel)
   if (last_block_ticket(P.tickets + ct, RS)) {
     T* recp = reinterpret_cast<T*>(P.rec + REC_HDR);
-    for (int e = tid; e < TC * kk; e += kThreads) {
-      const int64_t pp = (int64_t)ct * TC + e / kk;
+    for (int e = threadIdx.x; e < TC * P.Kc; e += kThreads) {
+      const int64_t pp = (int64_t)ct * TC + e / P.Kc;
+      const int k = e % P.Kc;
       if (pp >= nJ) continue;
-      T sum = T(0);
-      for (int r2 = 0; r2 < RS; ++r2) {
-        const T* src = colpart + ((int64_t)ct * RS + r2) * TC * kk + e;
-        sum += sizeof(T) == 8 ? (T)__ldcg((const double*)src) : (T)__ldcg((const float*)src);
-      }
-      recp[pp * kk + (e % kk)] = sum;
+      T g, h;
+      colpart_sum<T>(P, pp, k, RS, g, h);
+      recp[pp * kk + k] = g;
+      recp[pp * kk + P.Kc + k] = h;
     }
-    if (tid == 0) P.tickets[ct] = 0u;
+    if (threadIdx.x == 0) P.tickets[ct] = 0u;
   }
-  // ---- last CTA overall: NB sums in fixed CTA order ----
+  // last CTA overall: NB moment sums in fixed CTA order (parallel)
   const unsigned int total = (unsigned int)(RS * gridDim.y);
   if (last_block_ticket(P.tickets + P.CT, total)) {
-    if (tid == 0) {
-      double sn = 0.0, sd = 0.0;
-      for (unsigned int b = 0; b < total; ++b) {
-        sn += __ldcg(P.nbpart + 2 * b);
-        sd += __ldcg(P.nbpart + 2 * b + 1);
-      }
+    const double sn = sum_parts<kThreads>(P.nbpart, total, 2, scr);
+    const double sd = sum_parts<kThreads>(P.nbpart + 1, total, 2, scr);
+    if (threadIdx.x == 0) {
       P.rec[R_NBNUM] = sn;
       P.rec[R_NBDEN] = sd;
       P.tickets[P.CT] = 0u;
@@ -319,47 +71,150 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// persistent fit kernel (single rank)
+// ---------------------------------------------------------------------------
 template <typename T, int FAM, int NK>
-static int launch_one(const Params& P, dim3 grid, size_t smem, cudaStream_t st, long long xb,
-                      long long xs, double xalpha) {
-  k_grad<T, FAM, NK><<<grid, kThreads, smem, st>>>(P, xb, xs, xalpha);
-  GMF_LAUNCH_CHECK("k_grad");
-  return GMF_OK;
-}
+__global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
+k_fit(Params P, long long n_steps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double scr[kThreads / 32];
+  constexpr int TC = Tile<T>::TC;
+  cg::grid_group grid = cg::this_grid();
+  Ctrl C = *P.ctrl;
+  if (C.stopped) return;
+  const int G = gridDim.x;
+  const int ct = blockIdx.x % P.CT, rs = blockIdx.x / P.CT, RS = G / P.CT;
+  const int64_t gstride = (int64_t)G * kThreads;
+  const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int Kr = P.Kr, Kc = P.Kc;
+  long long prev_blk = -1;
 
-template <typename T, int FAM>
-static int launch_nk(const Params& P, int NK, dim3 grid, size_t smem, cudaStream_t st,
-                     long long xb, long long xs, double xa) {
-  switch (NK) {
-    case 8: return launch_one<T, FAM, 8>(P, grid, smem, st, xb, xs, xa);
-    case 12: return launch_one<T, FAM, 12>(P, grid, smem, st, xb, xs, xa);
-    case 16: return launch_one<T, FAM, 16>(P, grid, smem, st, xb, xs, xa);
-    case 24: return launch_one<T, FAM, 24>(P, grid, smem, st, xb, xs, xa);
-    case 32: return launch_one<T, FAM, 32>(P, grid, smem, st, xb, xs, xa);
-    default: set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED;
+  for (long long it = 0; it < n_steps; ++it) {
+    const long long t = C.t;
+    const bool boundary = (t % P.S) == 0;
+    const bool run_grad = t < P.max_steps;
+    const long long blk = run_grad ? (long long)P.bseq[t] : -1;
+    const long long sidx = t % P.S;
+    // ------------------------- phase 1 -------------------------
+    if (blockIdx.x == 0 && prev_blk >= 0) {   // row norms of the block updated last step
+      const double g2 = sum_parts<kThreads>(P.rnpart, G, 2, scr);
+      const double u2 = sum_parts<kThreads>(P.rnpart + 1, G, 2, scr);
+      if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = g2; P.blocksum[2 * prev_blk + 1] = u2; }
+    }
+    if (boundary) obj_partial<T>(P, C.nb_shape, blockIdx.x, G, P.objpart + OBJ_W * blockIdx.x);
+    if (run_grad && rs < RS) grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
+    grid.sync();
+    // ------------------------- phase 2 -------------------------
+    double dev = 0, nb = 0, nv = 0, ng = 0, nu = 0;
+    if (boundary) {
+      dev = sum_parts<kThreads>(P.objpart + 0, G, OBJ_W, scr);
+      nb = sum_parts<kThreads>(P.objpart + 1, G, OBJ_W, scr);
+      nv = sum_parts<kThreads>(P.objpart + 2, G, OBJ_W, scr);
+      ng = sum_parts<kThreads>(P.blocksum + 0, P.R, 2, scr);
+      nu = sum_parts<kThreads>(P.blocksum + 1, P.R, 2, scr);
+    }
+    const Decision D = decide_from(P, C, dev, ng, nu, nb, nv);
+    double nbn = 0.0, nbd = 0.0;
+    if (!D.stop && P.est_alpha) {
+      nbn = sum_parts<kThreads>(P.nbpart, G, 2, scr);
+      nbd = sum_parts<kThreads>(P.nbpart + 1, G, 2, scr);
+    }
+    const bool upd = !D.stop;
+    const double rho = upd ? P.rho_tab[t] : 0.0;
+    const double at = upd ? P.alpt_tab[t] : 0.0;
+    // rows of block I (snapshot before update)
+    double rg = 0.0, ru = 0.0;
+    if (blk >= 0 && (upd || D.snap)) {
+      const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
+      const int64_t nJ = P.cbp[sidx + 1] - P.cbp[sidx];
+      const double s_row = (double)P.m / (double)nJ;
+      for (int64_t e = gtid; e < nI * Kr; e += gstride) {
+        const int64_t il = e / Kr;
+        const int k = (int)(e % Kr);
+        const int64_t i = r0 + il;
+        T* th = tptr<T>(P.th_row) + i * Kr + k;
+        if (D.snap) tptr<T>(P.sn_row)[i * Kr + k] = *th;
+        if (upd) {
+          T gs, hs;
+          rowpart_sum<T>(P, il, k, gs, hs);
+          const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_row) + i * Kr + k,
+                                      tptr<T>(P.hb_row) + i * Kr + k, gs, hs, s_row,
+                                      k < P.q ? P.lam_g : P.lam_u, rho, at);
+          const double sq = (double)nvv * (double)nvv;
+          if (k < P.q) rg += sq; else ru += sq;
+        }
+      }
+    }
+    rg = block_sum<kThreads>(rg, scr);
+    ru = block_sum<kThreads>(ru, scr);
+    if (threadIdx.x == 0) { P.rnpart[2 * blockIdx.x] = rg; P.rnpart[2 * blockIdx.x + 1] = ru; }
+    // columns: snapshot all m, update those of block J
+    if (upd || D.snap) {
+      const double s_col = blk >= 0 ? P.rbscale[blk] : 0.0;
+      for (int64_t e = gtid; e < P.m * Kc; e += gstride) {
+        const int64_t j = e / Kc;
+        const int k = (int)(e % Kc);
+        T* th = tptr<T>(P.th_col) + j * Kc + k;
+        if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
+        if (!upd) continue;
+        int64_t pos = -1;
+        if (P.col_identity) pos = j;
+        else if (P.cbof[j] == sidx) pos = P.cpos[j];
+        if (pos < 0) continue;
+        T gs, hs;
+        colpart_sum<T>(P, pos, k, RS, gs, hs);
+        ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k, tptr<T>(P.hb_col) + j * Kc + k, gs,
+                      hs, s_col, k < P.p ? P.lam_b : P.lam_v, rho, at);
+      }
+    }
+    if (D.snap) snapshot_dirty<T>(P, blk, C.last_snap_t, gtid, gstride);
+    const Ctrl N = advance(P, C, D, nbn, nbd);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (D.boundary) {
+        P.trace_obj[C.trace_len] = D.obj;
+        P.trace_nb[C.trace_len] = C.nb_shape;
+      }
+      if (upd) P.last_mod[blk] = t;
+      *P.ctrl = N;
+    }
+    C = N;
+    prev_blk = upd ? blk : -1;
+    if (D.stop) break;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && prev_blk >= 0) {
+    const double g2 = sum_parts<kThreads>(P.rnpart, G, 2, scr);
+    const double u2 = sum_parts<kThreads>(P.rnpart + 1, G, 2, scr);
+    if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = g2; P.blocksum[2 * prev_blk + 1] = u2; }
   }
 }
 
+// ---------------------------------------------------------------------------
+// host side: dispatch over (dtype, family, feature bucket)
+// ---------------------------------------------------------------------------
+template <typename T, int FAM, int NK>
+struct Inst {
+  static void* grad() { return (void*)k_grad<T, FAM, NK>; }
+  static void* fit() { return (void*)k_fit<T, FAM, NK>; }
+};
+
 template <typename T, int FAM>
-static int prepare_nk(int NK) {
-  cudaError_t e = cudaSuccess;
+static void* pick(int NK, bool fit) {
   switch (NK) {
-    case 8: e = cudaFuncSetAttribute(k_grad<T, FAM, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); break;
-    case 12: e = cudaFuncSetAttribute(k_grad<T, FAM, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); break;
-    case 16: e = cudaFuncSetAttribute(k_grad<T, FAM, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); break;
-    case 24: e = cudaFuncSetAttribute(k_grad<T, FAM, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); break;
-    case 32: e = cudaFuncSetAttribute(k_grad<T, FAM, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); break;
-    default: set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED;
+    case 8: return fit ? Inst<T, FAM, 8>::fit() : Inst<T, FAM, 8>::grad();
+    case 12: return fit ? Inst<T, FAM, 12>::fit() : Inst<T, FAM, 12>::grad();
+    case 16: return fit ? Inst<T, FAM, 16>::fit() : Inst<T, FAM, 16>::grad();
+    case 24: return fit ? Inst<T, FAM, 24>::fit() : Inst<T, FAM, 24>::grad();
+    case 32: return fit ? Inst<T, FAM, 32>::fit() : Inst<T, FAM, 32>::grad();
+    default: return nullptr;
   }
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_grad)");
-  return GMF_OK;
 }
 
-// opt in to >48 KB dynamic shared memory once per handle (outside graph capture)
-int prepare_grad(int dtype, int family, int NK) {
+static void* kernel_for(int dtype, int family, int NK, bool fit) {
   const int fam = family == GMF_NEG_BINOMIAL ? 1 : 0;
-  if (dtype == GMF_F64) return fam ? prepare_nk<double, 1>(NK) : prepare_nk<double, 0>(NK);
-  return fam ? prepare_nk<float, 1>(NK) : prepare_nk<float, 0>(NK);
+  if (dtype == GMF_F64) return fam ? pick<double, 1>(NK, fit) : pick<double, 0>(NK, fit);
+  return fam ? pick<float, 1>(NK, fit) : pick<float, 0>(NK, fit);
 }
 
 int grad_bucket(int KA) {
@@ -371,20 +226,45 @@ int grad_bucket(int KA) {
   return -1;
 }
 
+int tile_cols(int dtype) { return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC; }
+
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc) {
-  return grad_smem(NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
+  return grad_smem(tile_cols(dtype), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
+}
+
+// opt in to >48 KB dynamic shared memory (outside any graph capture) and
+// report how many k_fit CTAs can be co-resident per SM
+int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int* fit_blocks_per_sm) {
+  void* g = kernel_for(dtype, family, NK, false);
+  void* f = kernel_for(dtype, family, NK, true);
+  if (!g || !f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
+  const int smem = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc);
+  GMF_CUDA(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  GMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int nb = 0;
+  GMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem));
+  *fit_blocks_per_sm = nb;
+  return GMF_OK;
 }
 
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha) {
+  void* f = kernel_for(dtype, P.fam, NK, false);
+  if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   dim3 grid(P.RS, P.CT);
   const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc);
-  const int fam = P.fam == GMF_NEG_BINOMIAL ? 1 : 0;
-  if (dtype == GMF_F64)
-    return fam ? launch_nk<double, 1>(P, NK, grid, smem, st, xb, xs, xalpha)
-               : launch_nk<double, 0>(P, NK, grid, smem, st, xb, xs, xalpha);
-  return fam ? launch_nk<float, 1>(P, NK, grid, smem, st, xb, xs, xalpha)
-             : launch_nk<float, 0>(P, NK, grid, smem, st, xb, xs, xalpha);
+  void* args[] = {(void*)&P, (void*)&xb, (void*)&xs, (void*)&xalpha};
+  GMF_CUDA(cudaLaunchKernel(f, grid, dim3(kThreads), args, smem, st));
+  return GMF_OK;
+}
+
+int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st) {
+  void* f = kernel_for(dtype, P.fam, NK, true);
+  if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
+  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc);
+  void* args[] = {(void*)&P, (void*)&n_steps};
+  GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+  return GMF_OK;
 }
 
 }  // namespace gmf

@@ -1,0 +1,384 @@
+// Device bodies shared by the per-step kernels (multi-rank path) and the
+// persistent fit kernel (single-rank path).
+#pragma once
+#include "gmf_engine.cuh"
+
+namespace gmf {
+
+// ---------------------------------------------------------------------------
+// value of Y and eta at a tracked entry (optim.py:274-280)
+// ---------------------------------------------------------------------------
+GMF_D double y_lookup(const Params& P, int64_t i, int64_t j) {
+  if (P.yfmt == GMF_Y_DENSE_I32) return (double)P.y[i * P.m + j];
+  int64_t lo = P.rp[i], hi = P.rp[i + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int cm = P.ci[mid];
+    if (cm == j) return (double)P.cv[mid];
+    if (cm < j) lo = mid + 1; else hi = mid;
+  }
+  return 0.0;
+}
+
+template <typename T>
+GMF_D double eta_at(const Params& P, int64_t i, int64_t j) {
+  const T* tr = tptr<T>(P.th_row) + i * P.Kr;
+  const T* tc = tptr<T>(P.th_col) + j * P.Kc;
+  double eta = 0.0;
+  for (int k = 0; k < P.d; ++k) eta += (double)tr[P.q + k] * (double)tc[P.p + k];
+  const T* x = tptr<T>(P.x) + i * P.p;
+  for (int k = 0; k < P.p; ++k) eta += (double)x[k] * (double)tc[k];
+  const T* z = tptr<T>(P.z) + j * P.q;
+  for (int k = 0; k < P.q; ++k) eta += (double)tr[k] * (double)z[k];
+  if (P.has_off) eta += (double)tptr<T>(P.off)[i];
+  return eta;
+}
+
+// ---------------------------------------------------------------------------
+// K3 body: this CTA's share of the tracked objective of the current state
+// (optim.py:283-290) -> out[0] deviance, out[1] ||B||^2, out[2] ||V||^2.
+// ---------------------------------------------------------------------------
+template <typename T>
+GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double* out) {
+  __shared__ double scr[kThreads / 32];
+  const T* wg = tptr<T>(P.w);
+  double s = 0.0;
+  const int64_t stride = (int64_t)ncta * kThreads;
+  for (int64_t e = (int64_t)cta * kThreads + threadIdx.x; e < P.E; e += stride) {
+    const int64_t i = P.erow[e];
+    const int64_t j = P.ecol[e];
+    const double mu = exp(eta_at<T>(P, i, j));
+    const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
+    const double y = P.ey ? (double)P.ey[e] : y_lookup(P, i, j);
+    s += w * unit_deviance(P.fam, y, mu, alpha);
+  }
+  const T* tc = tptr<T>(P.th_col);
+  double nb = 0.0, nv = 0.0;
+  for (int64_t e = (int64_t)cta * kThreads + threadIdx.x; e < P.m * P.Kc; e += stride) {
+    const double v = (double)tc[e];
+    if ((int)(e % P.Kc) < P.p) nb += v * v; else nv += v * v;
+  }
+  s = block_sum<kThreads>(s, scr);
+  nb = block_sum<kThreads>(nb, scr);
+  nv = block_sum<kThreads>(nv, scr);
+  if (threadIdx.x == 0) { out[0] = s; out[1] = nb; out[2] = nv; }
+}
+
+// ---------------------------------------------------------------------------
+// K1 body: fused minibatch gradient for one CTA tile.
+//
+// The CTA owns TC columns (column tile `ct` of block J) and a contiguous
+// range of TR-row chunks of block I (row split `rs` of RS).  Per entry:
+//   eta = offset_i + [x_i|u_i|gamma_i] . [b_j|v_j|z_j]       (model.py:229-256)
+//   mu  = exp(eta)                                             (_ref.py:21-32)
+//   dotD, ddotD  (Poisson / NB with log link)                  (_core.pyx:79-103)
+// Column side sum_i dotD_ij [x_i, u_i] (ddotD with squares) accumulates in
+// registers (thread == column) across all rows of the CTA; the row side
+// sum_j dotD_ij [z_j, v_j] is a small shared-memory GEMM over the chunk's
+// P tile (gradients.py:102-113).  eta and mu stay in registers.  Outputs:
+// rowpart[ct][row][2Kr], colpart[ct][rs][c][2Kc], nbpart[ct*RS+rs][2].
+// ---------------------------------------------------------------------------
+struct GradSmem {
+  int64_t rd, P, a, cd2, off, rp, y, w, red, cp, total;
+};
+
+GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
+  GradSmem s;
+  int64_t o = 0;
+  auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
+  s.rd = o; o = al(o + (int64_t)2 * TC * NK * tsz);
+  s.P = o; o = al(o + (int64_t)2 * TC * (TR + 1) * tsz);
+  const int64_t region = o;
+  int64_t r = region;
+  s.a = r; r = al(r + (int64_t)TR * NK * tsz);
+  s.cd2 = r; r = al(r + (int64_t)TR * NK * tsz);
+  s.off = r; r = al(r + (int64_t)TR * tsz);
+  s.rp = r; r = al(r + (int64_t)(TR + 1) * 8);
+  s.y = r; r = al(r + (int64_t)TR * TC * tsz);
+  s.w = r; r = al(r + (has_w ? (int64_t)TR * TC * tsz : 0));
+  const int64_t p1 = r - region;
+  const int64_t red = al((int64_t)NQ * 2 * Kr * (TR + 1) * tsz);
+  const int64_t cp = al((int64_t)TC * (2 * Kc + 1) * tsz);
+  s.red = region;
+  s.cp = region;
+  int64_t mx = p1 > red ? p1 : red;
+  mx = mx > cp ? mx : cp;
+  s.total = region + mx;
+  return s;
+}
+
+template <typename T, int FAM, int NK, int TC>
+GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct,
+                    int RS, unsigned char* smem) {
+  constexpr int NG = kThreads / TC;
+  constexpr int TCQ = TC / NQ;
+  __shared__ double red_scr[kThreads / 32];
+  const int tid = threadIdx.x;
+  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
+  const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
+  const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
+  const int64_t nchunks = (nI + TR - 1) / TR;
+  const int64_t cpr = (nchunks + RS - 1) / RS;
+  const int64_t ch_lo = rs * cpr, ch_hi = ch_lo + cpr < nchunks ? ch_lo + cpr : nchunks;
+
+  const GradSmem L = grad_smem(TC, NK, sizeof(T), P.has_w, Kr, Kc);
+  T* rd_s = reinterpret_cast<T*>(smem + L.rd);
+  T* P_s = reinterpret_cast<T*>(smem + L.P);
+  T* a_s = reinterpret_cast<T*>(smem + L.a);
+  T* cd2_s = reinterpret_cast<T*>(smem + L.cd2);
+  T* off_s = reinterpret_cast<T*>(smem + L.off);
+  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
+  T* y_s = reinterpret_cast<T*>(smem + L.y);
+  T* w_s = reinterpret_cast<T*>(smem + L.w);
+  T* red_s = reinterpret_cast<T*>(smem + L.red);
+  T* cp_s = reinterpret_cast<T*>(smem + L.cp);
+
+  const T* th_row = tptr<T>(P.th_row);
+  const T* th_col = tptr<T>(P.th_col);
+  const T* xg = tptr<T>(P.x);
+  const T* zg = tptr<T>(P.z);
+  const T* offg = tptr<T>(P.off);
+  const T* wg = tptr<T>(P.w);
+
+  // ---- this thread's column features [b | v | z] (phase 1) ----
+  const int c = tid % TC, g = tid / TC;
+  const int64_t pos = (int64_t)ct * TC + c;
+  const bool col_ok = pos < nJ;
+  const int64_t j = col_ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
+  T cf[NK];
+  #pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    T v = T(0);
+    if (col_ok) {
+      if (k < Kc) v = th_col[j * Kc + k];
+      else if (k < KA) v = zg[j * q + (k - Kc)];
+    }
+    cf[k] = v;
+  }
+  // ---- row-side design [z_j | v_j] and squares of the tile (phase 2) ----
+  __syncthreads();   // smem reuse across calls (persistent kernel)
+  for (int e = tid; e < TC * NK; e += kThreads) {
+    const int cc = e / NK, k = e % NK;
+    const int64_t pp = (int64_t)ct * TC + cc;
+    T v = T(0);
+    if (pp < nJ && k < Kr) {
+      const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
+      v = k < q ? zg[jj * q + k] : th_col[jj * Kc + p + (k - q)];
+    }
+    rd_s[cc * NK + k] = v;
+    rd_s[(TC + cc) * NK + k] = v * v;
+  }
+
+  T gacc[NK], hacc[NK];
+  #pragma unroll
+  for (int k = 0; k < NK; ++k) { gacc[k] = T(0); hacc[k] = T(0); }
+  double nb_num = 0.0, nb_den = 0.0;
+  const T rphi = T(1.0 / P.phi);
+  const T ralpha = T(1.0 / alpha);
+  const T tphi = T(P.phi);
+
+  const int pr = tid % TR, ph = (tid / TR) & 1, pq = tid / (2 * TR);
+  const int rkk = 2 * Kr;
+
+  for (int64_t ch = ch_lo; ch < ch_hi; ++ch) {
+    const int64_t rowbase = ch * TR;
+    const int rows = (int)((nI - rowbase) < TR ? (nI - rowbase) : TR);
+    const int64_t i0 = r0 + rowbase;
+    __syncthreads();   // previous chunk's red_s reads are done
+    // ---- row features [x | u | gamma], squares, offset ----
+    for (int e = tid; e < TR * NK; e += kThreads) {
+      const int rr = e / NK, k = e % NK;
+      T v = T(0);
+      if (rr < rows) {
+        const int64_t i = i0 + rr;
+        if (k < p) v = xg[i * p + k];
+        else if (k < p + d) v = th_row[i * Kr + q + (k - p)];
+        else if (k < KA) v = th_row[i * Kr + (k - p - d)];
+      }
+      a_s[rr * NK + k] = v;
+      cd2_s[rr * NK + k] = k < Kc ? v * v : T(0);
+    }
+    if (tid < TR) off_s[tid] = (tid < rows && P.has_off) ? offg[i0 + tid] : T(0);
+    // ---- response tile ----
+    if (P.yfmt == GMF_Y_DENSE_I32) {
+      for (int e = tid; e < TR * TC; e += kThreads) {
+        const int rr = e / TC, cc = e % TC;
+        const int64_t pp = (int64_t)ct * TC + cc;
+        T v = T(0), wv = T(0);
+        if (rr < rows && pp < nJ) {
+          const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
+          v = (T)P.y[(i0 + rr) * P.m + jj];
+          if (P.has_w) wv = wg[(i0 + rr) * P.m + jj];
+        }
+        y_s[e] = v;
+        if (P.has_w) w_s[e] = wv;
+      }
+    } else {
+      // CSR: the chunk's nonzeros are one contiguous range; stage the row
+      // pointers, then scatter the range into the dense tile in smem
+      if (tid <= rows) rp_s[tid] = P.rp[i0 + tid];
+      for (int e = tid; e < TR * TC; e += kThreads) y_s[e] = T(0);
+      __syncthreads();
+      const int64_t lo = rp_s[0], hi = rp_s[rows];
+      const int64_t cbase = (int64_t)ct * TC;
+      for (int64_t k = lo + tid; k < hi; k += kThreads) {
+        int a = 0, b = rows;
+        while (b - a > 1) {
+          const int mid = (a + b) >> 1;
+          if (rp_s[mid] <= k) a = mid; else b = mid;
+        }
+        const int col = P.ci[k];
+        int64_t pp;
+        if (P.col_identity) pp = col;
+        else pp = (P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1;
+        const int64_t cl = pp - cbase;
+        if (pp >= 0 && cl >= 0 && cl < TC) y_s[a * TC + cl] = (T)P.cv[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 1: eta, mu, dotD, ddotD; column side in registers ----
+    T cn = T(0), cd = T(0);
+    #pragma unroll 2
+    for (int rr = g; rr < TR; rr += NG) {
+      const T* a = a_s + rr * NK;
+      T eta = off_s[rr];
+      #pragma unroll
+      for (int k = 0; k < NK; ++k) eta = fma(a[k], cf[k], eta);
+      const T mu = exp_t(eta);
+      const T yv = y_s[rr * TC + c];
+      const T wv = P.has_w ? w_s[rr * TC + c] : T(1);
+      const T r = yv - mu;
+      T dd, hh;
+      if (FAM == 0) {
+        dd = -wv * r * rphi;
+        hh = wv * mu * rphi;
+      } else {
+        const T inv = rcp_t(tphi * fma(mu, ralpha, T(1)));
+        dd = -wv * r * inv;
+        hh = wv * mu * inv;
+      }
+      const bool ok = col_ok && rr < rows;
+      if (!ok) { dd = T(0); hh = T(0); }
+      const T* a2 = cd2_s + rr * NK;
+      #pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        gacc[k] = fma(dd, a[k], gacc[k]);
+        hacc[k] = fma(hh, a2[k], hacc[k]);
+      }
+      P_s[c * (TR + 1) + rr] = dd;
+      P_s[(TC + c) * (TR + 1) + rr] = hh;
+      if (FAM == 1 && ok) {
+        cn = fma(wv * mu, mu, cn);
+        cd = fma(wv, fma(r, r, -mu), cd);
+      }
+    }
+    nb_num += (double)cn;
+    nb_den += (double)cd;
+    __syncthreads();
+
+    // ---- phase 2: row side  P (TR x TC) . rd (TC x Kr) ----
+    T acc[NK];
+    #pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = T(0);
+    {
+      const T* Pp = P_s + ph * TC * (TR + 1);
+      const T* rdp = rd_s + ph * TC * NK;
+      #pragma unroll 4
+      for (int cc = pq * TCQ; cc < (pq + 1) * TCQ; ++cc) {
+        const T pv = Pp[cc * (TR + 1) + pr];
+        const T* rd = rdp + cc * NK;
+        #pragma unroll
+        for (int k = 0; k < NK; ++k) acc[k] = fma(pv, rd[k], acc[k]);
+      }
+    }
+    #pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < Kr) red_s[((pq * 2 + ph) * Kr + k) * (TR + 1) + pr] = acc[k];
+    __syncthreads();
+    {
+      T* outp = tptr<T>(P.rowpart) + ((int64_t)ct * P.nstar_max + rowbase) * rkk;
+      for (int o = tid; o < rows * rkk; o += kThreads) {
+        const int rr = o / rkk, hk = o % rkk;
+        const int h = hk / Kr, k = hk % Kr;
+        T sum = T(0);
+        #pragma unroll
+        for (int qq = 0; qq < NQ; ++qq) sum += red_s[((qq * 2 + h) * Kr + k) * (TR + 1) + rr];
+        outp[o] = sum;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- column partials: fixed-order sum over the NG row groups ----
+  const int ck = 2 * Kc + 1;
+  for (int round = 0; round < NG; ++round) {
+    if (g == round) {
+      #pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        if (k < Kc) {
+          if (round == 0) { cp_s[c * ck + k] = gacc[k]; cp_s[c * ck + Kc + k] = hacc[k]; }
+          else { cp_s[c * ck + k] += gacc[k]; cp_s[c * ck + Kc + k] += hacc[k]; }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int kk = 2 * Kc;
+  T* colpart = tptr<T>(P.colpart);
+  const int64_t cbase2 = ((int64_t)ct * RS + rs) * TC * kk;
+  for (int e = tid; e < TC * kk; e += kThreads) colpart[cbase2 + e] = cp_s[(e / kk) * ck + (e % kk)];
+  const double bn = block_sum<kThreads>(nb_num, red_scr);
+  const double bd = block_sum<kThreads>(nb_den, red_scr);
+  if (tid == 0) {
+    P.nbpart[2 * ((int64_t)ct * RS + rs)] = bn;
+    P.nbpart[2 * ((int64_t)ct * RS + rs) + 1] = bd;
+  }
+}
+
+// column-side gradient sums of element (pos, k) of column block J from the
+// per-CTA K1 partials (fixed rs order)
+template <typename T>
+GMF_D void colpart_sum(const Params& P, int64_t pos, int k, int RS, T& gs, T& hs) {
+  const int TC = P.TC, kk = 2 * P.Kc;
+  const int64_t ct = pos / TC, c = pos % TC;
+  const T* base = tptr<T>(P.colpart) + (ct * RS * TC + c) * kk + k;
+  const int64_t stride = (int64_t)TC * kk;
+  T g = T(0), h = T(0);
+  #pragma unroll 8
+  for (int r = 0; r < RS; ++r) {
+    g += ldcg_t<T>(base + r * stride);
+    h += ldcg_t<T>(base + r * stride + P.Kc);
+  }
+  gs = g;
+  hs = h;
+}
+
+// row-side sums of (row il of the block, k) over the CT column tiles
+template <typename T>
+GMF_D void rowpart_sum(const Params& P, int64_t il, int k, T& gs, T& hs) {
+  const T* rp = tptr<T>(P.rowpart);
+  T g = T(0), h = T(0);
+  for (int ct = 0; ct < P.CT; ++ct) {
+    const T* src = rp + ((int64_t)ct * P.nstar_max + il) * (2 * P.Kr);
+    g += ldcg_t<T>(src + k);
+    h += ldcg_t<T>(src + P.Kr + k);
+  }
+  gs = g;
+  hs = h;
+}
+
+// copy the rows of dirty row blocks (other than `skip`) into the snapshot
+template <typename T>
+GMF_D void snapshot_dirty(const Params& P, long long skip, long long since, int64_t first,
+                          int64_t stride) {
+  const T* src = tptr<T>(P.th_row);
+  T* dst = tptr<T>(P.sn_row);
+  for (int64_t r = 0; r < P.R; ++r) {
+    if (r == skip || P.last_mod[r] < since) continue;
+    const int64_t a = P.rbp[r] * P.Kr, b = P.rbp[r + 1] * P.Kr;
+    for (int64_t e = a + first; e < b; e += stride) dst[e] = src[e];
+  }
+}
+
+}  // namespace gmf
