@@ -46,6 +46,7 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=400)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phases", type=int, default=0)
     return ap.parse_args()
 
 
@@ -245,7 +246,7 @@ def main():
     st = gk.FactorizationState(**wl.init_state())
     fam = gk.NegBinomial(st.nb_shape) if sp.family == "neg_binomial" else gk.Poisson()
     W, K, E = args.warmup, args.steps, args.e2e_steps
-    cfg = gk.SgdConfig(max_epochs=W + K + E + 8, mb_rows=sp.mb_rows, mb_cols=sp.m, tol=1e-30,
+    cfg = gk.SgdConfig(max_epochs=W + K + E + args.phases + 8, mb_rows=sp.mb_rows, mb_cols=sp.m, tol=1e-30,
                        seed=0)
     sched = Schedule(sp.n, sp.m, cfg)
     fit = DeviceFit(data, covs, fam, gk.Log(), gk.PenaltyConfig(), cfg, st, schedule=sched,
@@ -292,6 +293,35 @@ def main():
         ms = float(t.item())
     status = fit.status()
     assert status.t == W + K and not status.stopped, (status.t, status.stopped)
+    phases = None
+    if args.phases and world == 1:
+        import ctypes as C
+        nprof = int(fit.lib.gmf_profile_len(fit.h))
+        buf = (C.c_double * nprof)()
+        _lib.check(fit.lib.gmf_profile(fit.h, 1, None, fit.stream()), "gmf_profile")
+        fit.run(args.phases)
+        _lib.check(fit.lib.gmf_profile(fit.h, 0, buf, fit.stream()), "gmf_profile")
+        nst = max(buf[5], 1.0)
+        names = ["objective_partials", "k1_tiles", "barrier1", "phase2_update", "barrier2"]
+        phases = {nm: buf[i] / nst / 1e3 for i, nm in enumerate(names)}
+        for i, nm in ((6, "p2_totals"), (7, "p2_rows"), (8, "p2_cols"), (9, "p2_rest"), (10, "p2_norms")):
+            phases[nm + "_cum"] = buf[i] / nst / 1e3
+        st_ = np.array(buf[16:]).reshape(-1, 8)[:, :5]
+        t0 = st_[:, 0].min()
+        rel = (st_ - t0) / 1e3
+        phases["last_step_per_cta_us"] = {
+            "obj_end(min/mean/max)": [rel[:, 1].min(), rel[:, 1].mean(), rel[:, 1].max()],
+            "k1_end(min/mean/max)": [rel[:, 2].min(), rel[:, 2].mean(), rel[:, 2].max()],
+            "k1_dur(min/mean/max)": [(rel[:, 2] - rel[:, 1]).min(), (rel[:, 2] - rel[:, 1]).mean(),
+                                     (rel[:, 2] - rel[:, 1]).max()],
+            "barrier1_release(min/max)": [rel[:, 3].min(), rel[:, 3].max()],
+            "phase2_end(min/mean/max)": [rel[:, 4].min(), rel[:, 4].mean(), rel[:, 4].max()],
+        }
+        phases["unit"] = "us/step (CTA 0 globaltimer)"
+        print(json.dumps({"phases": phases}), file=sys.stderr, flush=True)
+        K2 = args.phases
+    else:
+        K2 = 0
     sizes = np.array([b.size for b in sched.row_blocks])
     seq = sched.block_seq
     entries = float(sizes[seq[W:W + K]].sum()) * sp.m
@@ -344,7 +374,7 @@ def main():
         h2d = 0
         e0.record()
         for k in range(E):
-            t = W + K + k
+            t = W + K + K2 + k
             b = int(seq[t])
             r0, r1 = int(rbp[b]), int(rbp[b + 1])
             if fit.csr_ptr is not None:
@@ -368,8 +398,8 @@ def main():
             e_ms = float(t_.item())
         st_e = _lib.GmfStatus()
         fit.lib.gmf_status_decode(C.c_void_p(raw.data_ptr()), C.byref(st_e))
-        assert st_e.t == W + K + E, st_e.t
-        e_entries = float(sizes[seq[W + K:W + K + E]].sum()) * sp.m
+        assert st_e.t == W + K + K2 + E, st_e.t
+        e_entries = float(sizes[seq[W + K + K2:W + K + K2 + E]].sum()) * sp.m
         e2e = {"value": e_entries / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": raw.numel(),
                "steps": E, "ms_per_step": e_ms / E,

@@ -202,6 +202,14 @@ int gmf_status_decode(const void* raw, gmf_status* out);
  * launches of the fused gradient kernel K1 alone on row block `row_block`,
  * column block 0, at the current state (no state change). */
 int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_ms, void* stream);
+/* Profiling hook: phase timers of the persistent kernel (globaltimer ns):
+ * out[0..5] = CTA 0's {objective partials, K1 tiles, barrier 1, phase 2,
+ * barrier 2, steps}, out[6..10] phase-2 sub-timers, out[16 + 8 c + i] the
+ * last profiled step's stamps of CTA c (i: start, K1 start, K1 end, after
+ * barrier 1, phase-2 end).  `out` holds gmf_profile_len(h) doubles; reads
+ * (if out) and resets the counters, then enables/disables. */
+int64_t gmf_profile_len(gmf_handle* h);
+int gmf_profile(gmf_handle* h, int enable, double* out, void* stream);
 /* host copies of the first n trace entries (objective, nb shape) */
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);
 

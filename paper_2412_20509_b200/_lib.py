@@ -103,6 +103,8 @@ SIGNATURES = {
     "gmf_status_copy_async": (C.c_int, [_P, _P, _P]),
     "gmf_status_decode": (C.c_int, [_P, C.POINTER(GmfStatus)]),
     "gmf_time_grad": (C.c_int, [_P, _i64, _i32, _pd, _P]),
+    "gmf_profile": (C.c_int, [_P, C.c_int, _pd, _P]),
+    "gmf_profile_len": (_i64, [_P]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),
     "gmf_cross_rows": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _P, _i64, _i32, _i32,

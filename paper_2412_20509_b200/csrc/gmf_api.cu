@@ -13,7 +13,7 @@ int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long x
                 double xalpha);
 int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int* fit_blocks_per_sm);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
-int launch_eval_y(const Params& P, int32_t* out, cudaStream_t st);
+int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int tile_cols(int dtype);
 int grad_bucket(int KA);
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc);
@@ -45,6 +45,7 @@ struct gmf_handle {
   std::map<int64_t, cudaGraphExec_t> graphs;
   int fit_grid = 0;             // co-resident CTAs of the persistent kernel
   int fit_rs = 0;               // its row splits (fit_grid / CT)
+  void* prof_buf = nullptr;
   std::vector<int64_t> rbp_host, cbp_host;
   bool reset_done = false;
 };
@@ -208,7 +209,8 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_alp = take(ms * 8);
   const int64_t o_fp = take(2 * kSMs * 8);
   const int64_t o_ft = take(64);
-  const int64_t o_ey = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 4);
+  const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
+  const int64_t o_cnp = take(cta_max * 2 * 8);
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -223,6 +225,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.rec_stride = rec_bytes;
   P.objpart = (double*)(base + o_objp);
   P.rnpart = (double*)(base + o_rnp);
+  P.cnpart = (double*)(base + o_cnp);
   P.blocksum = (double*)(base + o_bs);
   P.last_mod = (long long*)(base + o_lm);
   P.rho_tab = (double*)(base + o_rho);
@@ -230,12 +233,11 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   h->full_part = (double*)(base + o_fp);
   h->full_ticket = (unsigned int*)(base + o_ft);
   GMF_CUDA(cudaMemset(h->ws, 0, off));
-  P.ey = nullptr;
-  if (bufs->n_eval > 0) {   // Y at the fixed tracked sample, looked up once
-    rc = launch_eval_y(P, (int32_t*)(base + o_ey), 0);
+  P.ep = (const int4*)(base + o_ep);
+  if (bufs->n_eval > 0) {   // tracked sample packed with its Y, once per fit
+    rc = launch_eval_pack(P, (int4*)(base + o_ep), 0);
     if (rc) { gmf_destroy(h); return rc; }
     GMF_CUDA(cudaDeviceSynchronize());
-    P.ey = (const int32_t*)(base + o_ey);
   }
 
   // learning-rate and bias-correction tables, host libm (optim.py:130-148)
@@ -264,6 +266,7 @@ int gmf_destroy(gmf_handle* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->internal) cudaStreamSynchronize(h->internal);
   if (h->ws) cudaFree(h->ws);
+  if (h->prof_buf) cudaFree(h->prof_buf);
   if (h->host_ctrl) cudaFreeHost(h->host_ctrl);
   if (h->internal) cudaStreamDestroy(h->internal);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
@@ -404,6 +407,25 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
 }
 
 int64_t gmf_status_raw_bytes(void) { return (int64_t)sizeof(Ctrl); }
+
+int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 8 * (int64_t)h->fit_grid : 0; }
+
+int gmf_profile(gmf_handle* h, int enable, double* out6, void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  const int64_t NPROF = gmf_profile_len(h);
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h->prof_buf) GMF_CUDA(cudaMalloc(&h->prof_buf, NPROF * sizeof(unsigned long long)));
+  if (out6) {
+    std::vector<unsigned long long> v(NPROF);
+    GMF_CUDA(cudaMemcpyAsync(v.data(), h->prof_buf, NPROF * 8, cudaMemcpyDeviceToHost, st));
+    GMF_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < NPROF; ++i) out6[i] = (double)v[i];
+  }
+  GMF_CUDA(cudaMemsetAsync(h->prof_buf, 0, NPROF * sizeof(unsigned long long), st));
+  h->P.prof = enable ? (unsigned long long*)h->prof_buf : nullptr;
+  return GMF_OK;
+}
 
 int gmf_status_copy_async(gmf_handle* h, void* host_dst, void* stream) {
   if (!h || !host_dst) { set_error("null handle/dst"); return GMF_ERR_STATE; }

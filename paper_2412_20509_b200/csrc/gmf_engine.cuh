@@ -66,7 +66,7 @@ struct Params {
   int64_t max_steps;
   const int64_t* erow;
   const int32_t* ecol;
-  const int32_t* ey;  // Y at the tracked entries (precomputed once)
+  const int4* ep;     // tracked entries packed (row, col, y, 0), built once
   int64_t E;
   // config
   double a1, a2, damp, tol;
@@ -87,12 +87,20 @@ struct Params {
   int64_t rec_stride;  // bytes between gathered records
   double* objpart;     // [n_obj_ctas][OBJ_W]
   double* rnpart;      // [n_row_ctas][2]
+  double* cnpart;      // [fit CTAs][2] column-norm partials (persistent kernel)
   double* blocksum;    // [R][2] (gamma, u) squared norms per row block
   long long* last_mod; // [R]
   int TC, RS, CT;
   int64_t nstar_max, jmax;
   int n_obj_ctas, n_row_ctas, n_col_ctas;
+  unsigned long long* prof;   // optional phase timers of k_fit (ns, CTA 0)
 };
+
+GMF_D unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <typename T>
 GMF_D T* tptr(void* p) { return reinterpret_cast<T*>(p); }
@@ -116,6 +124,32 @@ GMF_D double block_sum_all(double v, double* scr) {
   s = scr[0];
   __syncthreads();
   return s;
+}
+
+// block-wide sums of N values at once, broadcast to every thread; xor
+// butterflies give bitwise-identical lane results (a+b == b+a), then a fixed
+// warp order (scr >= N * warps doubles)
+template <int N>
+GMF_D void block_sum_vec(double (&v)[N], double* scr) {
+  #pragma unroll
+  for (int i = 0; i < N; ++i) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    #pragma unroll
+    for (int i = 0; i < N; ++i) scr[wid * N + i] = v[i];
+  }
+  __syncthreads();
+  #pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scr[w * N + i];
+    v[i] = s;
+  }
+  __syncthreads();
 }
 
 // sum of n strided partials published by other CTAs, identical in every

@@ -74,11 +74,49 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
 // ---------------------------------------------------------------------------
 // persistent fit kernel (single rank)
 // ---------------------------------------------------------------------------
+
+// this CTA's share of the tracked-sample deviance, predictor in fp64 from
+// unrolled feature loads (all gathers of an entry in flight together)
+template <typename T, int NK>
+GMF_D double obj_dev_partial(const Params& P, double alpha, int64_t first, int64_t stride) {
+  const T* tr = tptr<T>(P.th_row);
+  const T* tc = tptr<T>(P.th_col);
+  const T* xg = tptr<T>(P.x);
+  const T* zg = tptr<T>(P.z);
+  const T* wg = tptr<T>(P.w);
+  const int p = P.p, q = P.q, d = P.d, Kr = P.Kr, Kc = P.Kc;
+  double s = 0.0;
+  for (int64_t e = first; e < P.E; e += stride) {
+    const int4 en = P.ep[e];
+    const int64_t i = en.x, j = en.y;
+    double eta = P.has_off ? (double)tptr<T>(P.off)[i] : 0.0;
+    #pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < d) eta += (double)tr[i * Kr + q + k] * (double)tc[j * Kc + p + k];
+    #pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < p) eta += (double)xg[i * p + k] * (double)tc[j * Kc + k];
+    #pragma unroll
+    for (int k = 0; k < NK; ++k)
+      if (k < q) eta += (double)tr[i * Kr + k] * (double)zg[j * q + k];
+    const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
+    s += w * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
+  }
+  return s;
+}
+
+template <typename T>
+GMF_D T warp_sum(T v) {
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <typename T, int FAM, int NK>
 __global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
 k_fit(Params P, long long n_steps) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double scr[kThreads / 32];
+  __shared__ double scr[8 * (kThreads / 32)];
   constexpr int TC = Tile<T>::TC;
   cg::grid_group grid = cg::this_grid();
   Ctrl C = *P.ctrl;
@@ -87,44 +125,86 @@ k_fit(Params P, long long n_steps) {
   const int ct = blockIdx.x % P.CT, rs = blockIdx.x / P.CT, RS = G / P.CT;
   const int64_t gstride = (int64_t)G * kThreads;
   const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  const int Kr = P.Kr, Kc = P.Kc;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = gtid >> 5, nw = gstride >> 5;
+  const int Kr = P.Kr, Kc = P.Kc, kk = 2 * Kc;
   long long prev_blk = -1;
 
+  // column-norm partials of the current state (phase 2 keeps them current)
+  {
+    double v[2] = {0.0, 0.0};
+    const T* tc = tptr<T>(P.th_col);
+    for (int64_t e = gtid; e < P.m * Kc; e += gstride) {
+      const double x = (double)tc[e];
+      v[(int)(e % Kc) < P.p ? 0 : 1] += x * x;
+    }
+    block_sum_vec<2>(v, scr);
+    if (threadIdx.x == 0) { P.cnpart[2 * blockIdx.x] = v[0]; P.cnpart[2 * blockIdx.x + 1] = v[1]; }
+  }
+
+  const bool prof = P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  // per-CTA stamps of the last profiled step (block-uniform condition)
+  const bool profc = P.prof != nullptr;
+  unsigned long long t_a = prof ? gtimer() : 0, t_b;
   for (long long it = 0; it < n_steps; ++it) {
     const long long t = C.t;
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 0] = gtimer(); }
     const bool boundary = (t % P.S) == 0;
     const bool run_grad = t < P.max_steps;
     const long long blk = run_grad ? (long long)P.bseq[t] : -1;
     const long long sidx = t % P.S;
     // ------------------------- phase 1 -------------------------
     if (blockIdx.x == 0 && prev_blk >= 0) {   // row norms of the block updated last step
-      const double g2 = sum_parts<kThreads>(P.rnpart, G, 2, scr);
-      const double u2 = sum_parts<kThreads>(P.rnpart + 1, G, 2, scr);
-      if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = g2; P.blocksum[2 * prev_blk + 1] = u2; }
+      double v[2] = {0.0, 0.0};
+      for (int i = threadIdx.x; i < G; i += kThreads) {
+        v[0] += __ldcg(P.rnpart + 2 * i);
+        v[1] += __ldcg(P.rnpart + 2 * i + 1);
+      }
+      block_sum_vec<2>(v, scr);
+      if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
     }
-    if (boundary) obj_partial<T>(P, C.nb_shape, blockIdx.x, G, P.objpart + OBJ_W * blockIdx.x);
-    if (run_grad && rs < RS) grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
-    grid.sync();
-    // ------------------------- phase 2 -------------------------
-    double dev = 0, nb = 0, nv = 0, ng = 0, nu = 0;
     if (boundary) {
-      dev = sum_parts<kThreads>(P.objpart + 0, G, OBJ_W, scr);
-      nb = sum_parts<kThreads>(P.objpart + 1, G, OBJ_W, scr);
-      nv = sum_parts<kThreads>(P.objpart + 2, G, OBJ_W, scr);
-      ng = sum_parts<kThreads>(P.blocksum + 0, P.R, 2, scr);
-      nu = sum_parts<kThreads>(P.blocksum + 1, P.R, 2, scr);
+      double v[1] = {obj_dev_partial<T, NK>(P, C.nb_shape, gtid, gstride)};
+      block_sum_vec<1>(v, scr);
+      if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
     }
-    const Decision D = decide_from(P, C, dev, ng, nu, nb, nv);
-    double nbn = 0.0, nbd = 0.0;
-    if (!D.stop && P.est_alpha) {
-      nbn = sum_parts<kThreads>(P.nbpart, G, 2, scr);
-      nbd = sum_parts<kThreads>(P.nbpart + 1, G, 2, scr);
+    if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 1] = gtimer(); }
+    if (run_grad && rs < RS) grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
+    if (prof) { t_b = gtimer(); P.prof[1] += t_b - t_a; t_a = t_b; }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 2] = gtimer(); }
+    grid.sync();
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 3] = gtimer(); }
+    if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
+    // ------------------------- phase 2 -------------------------
+    // totals, redundantly in every CTA: deviance, ||B||^2, ||V||^2,
+    // ||Gamma||^2, ||U||^2, NB moment sums (one merged reduction)
+    double v7[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (boundary) {
+      for (int i = threadIdx.x; i < G; i += kThreads) {
+        v7[0] += __ldcg(P.objpart + OBJ_W * i);
+        v7[1] += __ldcg(P.cnpart + 2 * i);
+        v7[2] += __ldcg(P.cnpart + 2 * i + 1);
+      }
+      for (int64_t r = threadIdx.x; r < P.R; r += kThreads) {
+        v7[3] += __ldcg(P.blocksum + 2 * r);
+        v7[4] += __ldcg(P.blocksum + 2 * r + 1);
+      }
     }
+    if (run_grad && P.est_alpha) {
+      for (int i = threadIdx.x; i < G; i += kThreads) {
+        v7[5] += __ldcg(P.nbpart + 2 * i);
+        v7[6] += __ldcg(P.nbpart + 2 * i + 1);
+      }
+    }
+    block_sum_vec<7>(v7, scr);
+    if (prof) { t_b = gtimer(); P.prof[6] += t_b - t_a; }
+    const Decision D = decide_from(P, C, v7[0], v7[3], v7[4], v7[1], v7[2]);
     const bool upd = !D.stop;
     const double rho = upd ? P.rho_tab[t] : 0.0;
     const double at = upd ? P.alpt_tab[t] : 0.0;
+    double nrm[4] = {0.0, 0.0, 0.0, 0.0};   // new ||Gamma_I||, ||U_I||, ||B||, ||V|| partials
     // rows of block I (snapshot before update)
-    double rg = 0.0, ru = 0.0;
     if (blk >= 0 && (upd || D.snap)) {
       const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
       const int64_t nJ = P.cbp[sidx + 1] - P.cbp[sidx];
@@ -141,35 +221,65 @@ k_fit(Params P, long long n_steps) {
           const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_row) + i * Kr + k,
                                       tptr<T>(P.hb_row) + i * Kr + k, gs, hs, s_row,
                                       k < P.q ? P.lam_g : P.lam_u, rho, at);
-          const double sq = (double)nvv * (double)nvv;
-          if (k < P.q) rg += sq; else ru += sq;
+          nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
         }
       }
     }
-    rg = block_sum<kThreads>(rg, scr);
-    ru = block_sum<kThreads>(ru, scr);
-    if (threadIdx.x == 0) { P.rnpart[2 * blockIdx.x] = rg; P.rnpart[2 * blockIdx.x + 1] = ru; }
-    // columns: snapshot all m, update those of block J
-    if (upd || D.snap) {
-      const double s_col = blk >= 0 ? P.rbscale[blk] : 0.0;
+    if (prof) { t_b = gtimer(); P.prof[7] += t_b - t_a; }
+    // columns of block J: one warp per coordinate, lanes split the K1 row
+    // splits, fixed butterfly order; lane 0 snapshots and updates
+    if (upd) {
+      const int64_t j0 = P.cbp[sidx], nJ = P.cbp[sidx + 1] - j0;
+      const double s_col = P.rbscale[blk];
+      const T* cpart = tptr<T>(P.colpart);
+      const int64_t rstride = (int64_t)TC * kk;
+      for (int64_t e = gw; e < nJ * Kc; e += nw) {
+        const int64_t pos = e / Kc;
+        const int k = (int)(e % Kc);
+        const T* base = cpart + ((pos / TC) * RS * TC + (pos % TC)) * kk + k;
+        T g = T(0), h = T(0);
+        for (int r = lane; r < RS; r += 32) {
+          g += ldcg_t<T>(base + r * rstride);
+          h += ldcg_t<T>(base + r * rstride + Kc);
+        }
+        g = warp_sum<T>(g);
+        h = warp_sum<T>(h);
+        if (lane == 0) {
+          const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
+          T* th = tptr<T>(P.th_col) + j * Kc + k;
+          if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
+          const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k,
+                                      tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
+                                      k < P.p ? P.lam_b : P.lam_v, rho, at);
+          nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
+        }
+      }
+    }
+    if (prof) { t_b = gtimer(); P.prof[8] += t_b - t_a; }
+    // columns outside J: snapshot and norms (nothing to do when J = all)
+    if ((upd || D.snap) && !(upd && P.col_identity)) {
+      const T* tc = tptr<T>(P.th_col);
       for (int64_t e = gtid; e < P.m * Kc; e += gstride) {
         const int64_t j = e / Kc;
-        const int k = (int)(e % Kc);
-        T* th = tptr<T>(P.th_col) + j * Kc + k;
-        if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
-        if (!upd) continue;
-        int64_t pos = -1;
-        if (P.col_identity) pos = j;
-        else if (P.cbof[j] == sidx) pos = P.cpos[j];
-        if (pos < 0) continue;
-        T gs, hs;
-        colpart_sum<T>(P, pos, k, RS, gs, hs);
-        ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k, tptr<T>(P.hb_col) + j * Kc + k, gs,
-                      hs, s_col, k < P.p ? P.lam_b : P.lam_v, rho, at);
+        if (upd && P.cbof[j] == sidx) continue;
+        const T x = tc[e];
+        if (D.snap) tptr<T>(P.sn_col)[e] = x;
+        nrm[(int)(e % Kc) < P.p ? 2 : 3] += (double)x * (double)x;
       }
     }
     if (D.snap) snapshot_dirty<T>(P, blk, C.last_snap_t, gtid, gstride);
-    const Ctrl N = advance(P, C, D, nbn, nbd);
+    if (prof) { t_b = gtimer(); P.prof[9] += t_b - t_a; }
+    block_sum_vec<4>(nrm, scr);
+    if (prof) { t_b = gtimer(); P.prof[10] += t_b - t_a; }
+    if (threadIdx.x == 0) {
+      P.rnpart[2 * blockIdx.x] = nrm[0];
+      P.rnpart[2 * blockIdx.x + 1] = nrm[1];
+      if (upd) {
+        P.cnpart[2 * blockIdx.x] = nrm[2];
+        P.cnpart[2 * blockIdx.x + 1] = nrm[3];
+      }
+    }
+    const Ctrl N = advance(P, C, D, v7[5], v7[6]);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       if (D.boundary) {
         P.trace_obj[C.trace_len] = D.obj;
@@ -180,13 +290,20 @@ k_fit(Params P, long long n_steps) {
     }
     C = N;
     prev_blk = upd ? blk : -1;
+    if (prof) { t_b = gtimer(); P.prof[3] += t_b - t_a; t_a = t_b; }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 4] = gtimer(); }
     if (D.stop) break;
     grid.sync();
+    if (prof) { t_b = gtimer(); P.prof[4] += t_b - t_a; t_a = t_b; P.prof[5] += 1; }
   }
   if (blockIdx.x == 0 && prev_blk >= 0) {
-    const double g2 = sum_parts<kThreads>(P.rnpart, G, 2, scr);
-    const double u2 = sum_parts<kThreads>(P.rnpart + 1, G, 2, scr);
-    if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = g2; P.blocksum[2 * prev_blk + 1] = u2; }
+    double v[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < G; i += kThreads) {
+      v[0] += __ldcg(P.rnpart + 2 * i);
+      v[1] += __ldcg(P.rnpart + 2 * i + 1);
+    }
+    block_sum_vec<2>(v, scr);
+    if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
   }
 }
 

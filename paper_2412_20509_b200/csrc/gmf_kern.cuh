@@ -45,12 +45,11 @@ GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double*
   double s = 0.0;
   const int64_t stride = (int64_t)ncta * kThreads;
   for (int64_t e = (int64_t)cta * kThreads + threadIdx.x; e < P.E; e += stride) {
-    const int64_t i = P.erow[e];
-    const int64_t j = P.ecol[e];
+    const int4 en = P.ep[e];
+    const int64_t i = en.x, j = en.y;
     const double mu = exp(eta_at<T>(P, i, j));
     const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-    const double y = P.ey ? (double)P.ey[e] : y_lookup(P, i, j);
-    s += w * unit_deviance(P.fam, y, mu, alpha);
+    s += w * unit_deviance(P.fam, (double)en.z, mu, alpha);
   }
   const T* tc = tptr<T>(P.th_col);
   double nb = 0.0, nv = 0.0;
@@ -79,7 +78,7 @@ GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double*
 // rowpart[ct][row][2Kr], colpart[ct][rs][c][2Kc], nbpart[ct*RS+rs][2].
 // ---------------------------------------------------------------------------
 struct GradSmem {
-  int64_t rd, P, a, cd2, off, rp, y, w, red, cp, total;
+  int64_t rd, P, a, cd2, off, rm, rp, y, w, red, cp, total;
 };
 
 GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
@@ -93,6 +92,7 @@ GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
   s.a = r; r = al(r + (int64_t)TR * NK * tsz);
   s.cd2 = r; r = al(r + (int64_t)TR * NK * tsz);
   s.off = r; r = al(r + (int64_t)TR * tsz);
+  s.rm = r; r = al(r + (int64_t)TR * tsz);
   s.rp = r; r = al(r + (int64_t)(TR + 1) * 8);
   s.y = r; r = al(r + (int64_t)TR * TC * tsz);
   s.w = r; r = al(r + (has_w ? (int64_t)TR * TC * tsz : 0));
@@ -107,6 +107,62 @@ GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
   return s;
 }
 
+// exp of a predictor that the caller pre-scaled by log2(e) (fp32: MUFU ex2)
+GMF_D float exp_pre(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+GMF_D double exp_pre(double x) { return exp(x); }
+template <typename T> struct Pre { static constexpr double s = 1.4426950408889634; };
+template <> struct Pre<double> { static constexpr double s = 1.0; };
+
+// phase 1 of one chunk: eta, mu, dotD, ddotD per entry; column side into
+// registers; P tile into shared memory.  Branch-free: invalid rows/columns
+// carry weight 0, which zeroes dotD, ddotD and the NB moment terms.
+template <typename T, int FAM, int NK, int TC, bool HW>
+GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
+                  const T* __restrict__ off_s, const T* __restrict__ rm_s,
+                  const T* __restrict__ y_s, const T* __restrict__ w_s, T* __restrict__ P_s,
+                  const T (&cf)[NK], T (&gacc)[NK], T (&hacc)[NK], T cm, int c, int g, int rows,
+                  T rphi, T tphi, T ralpha, T& cn, T& cd) {
+  constexpr int NG = kThreads / TC;
+  #pragma unroll 2
+  for (int rr = g; rr < rows; rr += NG) {
+    const T* a = a_s + rr * NK;
+    T e0 = off_s[rr], e1 = T(0);
+    #pragma unroll
+    for (int k = 0; k < NK; k += 2) {
+      e0 = fma(a[k], cf[k], e0);
+      e1 = fma(a[k + 1], cf[k + 1], e1);
+    }
+    const T mu = exp_pre(e0 + e1);
+    const T yv = y_s[rr * TC + c];
+    const T wv = HW ? w_s[rr * TC + c] : rm_s[rr] * cm;
+    const T r = yv - mu;
+    T dd, hh;
+    if (FAM == 0) {
+      const T ws = wv * rphi;
+      dd = -ws * r;
+      hh = ws * mu;
+    } else {
+      const T inv = wv * rcp_t(tphi * fma(mu, ralpha, T(1)));
+      dd = -r * inv;
+      hh = mu * inv;
+      cn = fma(wv * mu, mu, cn);
+      cd = fma(wv, fma(r, r, -mu), cd);
+    }
+    const T* a2 = cd2_s + rr * NK;
+    #pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      gacc[k] = fma(dd, a[k], gacc[k]);
+      hacc[k] = fma(hh, a2[k], hacc[k]);
+    }
+    P_s[c * (TR + 1) + rr] = dd;
+    P_s[(TC + c) * (TR + 1) + rr] = hh;
+  }
+}
+
 template <typename T, int FAM, int NK, int TC>
 GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct,
                     int RS, unsigned char* smem) {
@@ -117,9 +173,8 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
   const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
   const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
-  const int64_t nchunks = (nI + TR - 1) / TR;
-  const int64_t cpr = (nchunks + RS - 1) / RS;
-  const int64_t ch_lo = rs * cpr, ch_hi = ch_lo + cpr < nchunks ? ch_lo + cpr : nchunks;
+  // this row split's contiguous rows of block I, balanced to within one row
+  const int64_t rlo = nI * rs / RS, rhi = nI * (rs + 1) / RS;
 
   const GradSmem L = grad_smem(TC, NK, sizeof(T), P.has_w, Kr, Kc);
   T* rd_s = reinterpret_cast<T*>(smem + L.rd);
@@ -127,6 +182,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   T* a_s = reinterpret_cast<T*>(smem + L.a);
   T* cd2_s = reinterpret_cast<T*>(smem + L.cd2);
   T* off_s = reinterpret_cast<T*>(smem + L.off);
+  T* rm_s = reinterpret_cast<T*>(smem + L.rm);
   int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
   T* y_s = reinterpret_cast<T*>(smem + L.y);
   T* w_s = reinterpret_cast<T*>(smem + L.w);
@@ -139,8 +195,9 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const T* zg = tptr<T>(P.z);
   const T* offg = tptr<T>(P.off);
   const T* wg = tptr<T>(P.w);
+  const T pre = T(Pre<T>::s);
 
-  // ---- this thread's column features [b | v | z] (phase 1) ----
+  // ---- this thread's column features [b | v | z] (phase 1), pre-scaled ----
   const int c = tid % TC, g = tid / TC;
   const int64_t pos = (int64_t)ct * TC + c;
   const bool col_ok = pos < nJ;
@@ -153,8 +210,9 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       if (k < Kc) v = th_col[j * Kc + k];
       else if (k < KA) v = zg[j * q + (k - Kc)];
     }
-    cf[k] = v;
+    cf[k] = v * pre;
   }
+  const T cm = col_ok ? T(1) : T(0);
   // ---- row-side design [z_j | v_j] and squares of the tile (phase 2) ----
   __syncthreads();   // smem reuse across calls (persistent kernel)
   for (int e = tid; e < TC * NK; e += kThreads) {
@@ -180,12 +238,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const int pr = tid % TR, ph = (tid / TR) & 1, pq = tid / (2 * TR);
   const int rkk = 2 * Kr;
 
-  for (int64_t ch = ch_lo; ch < ch_hi; ++ch) {
-    const int64_t rowbase = ch * TR;
-    const int rows = (int)((nI - rowbase) < TR ? (nI - rowbase) : TR);
+  for (int64_t rowbase = rlo; rowbase < rhi; rowbase += TR) {
+    const int rows = (int)((rhi - rowbase) < TR ? (rhi - rowbase) : TR);
     const int64_t i0 = r0 + rowbase;
     __syncthreads();   // previous chunk's red_s reads are done
-    // ---- row features [x | u | gamma], squares, offset ----
+    // ---- row features [x | u | gamma], squares, offset, row mask ----
     for (int e = tid; e < TR * NK; e += kThreads) {
       const int rr = e / NK, k = e % NK;
       T v = T(0);
@@ -198,8 +255,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       a_s[rr * NK + k] = v;
       cd2_s[rr * NK + k] = k < Kc ? v * v : T(0);
     }
-    if (tid < TR) off_s[tid] = (tid < rows && P.has_off) ? offg[i0 + tid] : T(0);
-    // ---- response tile ----
+    if (tid < TR) {
+      off_s[tid] = (tid < rows && P.has_off) ? offg[i0 + tid] * pre : T(0);
+      rm_s[tid] = tid < rows ? T(1) : T(0);
+    }
+    // ---- response tile (and weights, zero outside the block) ----
     if (P.yfmt == GMF_Y_DENSE_I32) {
       for (int e = tid; e < TR * TC; e += kThreads) {
         const int rr = e / TC, cc = e % TC;
@@ -222,57 +282,32 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       const int64_t lo = rp_s[0], hi = rp_s[rows];
       const int64_t cbase = (int64_t)ct * TC;
       for (int64_t k = lo + tid; k < hi; k += kThreads) {
-        int a = 0, b = rows;
-        while (b - a > 1) {
-          const int mid = (a + b) >> 1;
-          if (rp_s[mid] <= k) a = mid; else b = mid;
-        }
         const int col = P.ci[k];
+        const int val = P.cv[k];
         int64_t pp;
         if (P.col_identity) pp = col;
         else pp = (P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1;
         const int64_t cl = pp - cbase;
-        if (pp >= 0 && cl >= 0 && cl < TC) y_s[a * TC + cl] = (T)P.cv[k];
+        if (pp >= 0 && cl >= 0 && cl < TC) {
+          int a = 0, b = rows;
+          while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (rp_s[mid] <= k) a = mid; else b = mid;
+          }
+          y_s[a * TC + cl] = (T)val;
+        }
       }
     }
     __syncthreads();
 
-    // ---- phase 1: eta, mu, dotD, ddotD; column side in registers ----
+    // ---- phase 1 ----
     T cn = T(0), cd = T(0);
-    #pragma unroll 2
-    for (int rr = g; rr < TR; rr += NG) {
-      const T* a = a_s + rr * NK;
-      T eta = off_s[rr];
-      #pragma unroll
-      for (int k = 0; k < NK; ++k) eta = fma(a[k], cf[k], eta);
-      const T mu = exp_t(eta);
-      const T yv = y_s[rr * TC + c];
-      const T wv = P.has_w ? w_s[rr * TC + c] : T(1);
-      const T r = yv - mu;
-      T dd, hh;
-      if (FAM == 0) {
-        dd = -wv * r * rphi;
-        hh = wv * mu * rphi;
-      } else {
-        const T inv = rcp_t(tphi * fma(mu, ralpha, T(1)));
-        dd = -wv * r * inv;
-        hh = wv * mu * inv;
-      }
-      const bool ok = col_ok && rr < rows;
-      if (!ok) { dd = T(0); hh = T(0); }
-      const T* a2 = cd2_s + rr * NK;
-      #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        gacc[k] = fma(dd, a[k], gacc[k]);
-        hacc[k] = fma(hh, a2[k], hacc[k]);
-      }
-      P_s[c * (TR + 1) + rr] = dd;
-      P_s[(TC + c) * (TR + 1) + rr] = hh;
-      if (FAM == 1 && ok) {
-        cn = fma(wv * mu, mu, cn);
-        cd = fma(wv, fma(r, r, -mu), cd);
-      }
-    }
+    if (P.has_w)
+      phase1<T, FAM, NK, TC, true>(a_s, cd2_s, off_s, rm_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
+                                   g, rows, rphi, tphi, ralpha, cn, cd);
+    else
+      phase1<T, FAM, NK, TC, false>(a_s, cd2_s, off_s, rm_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
+                                    g, rows, rphi, tphi, ralpha, cn, cd);
     nb_num += (double)cn;
     nb_den += (double)cd;
     __syncthreads();
@@ -357,13 +392,20 @@ GMF_D void colpart_sum(const Params& P, int64_t pos, int k, int RS, T& gs, T& hs
 // row-side sums of (row il of the block, k) over the CT column tiles
 template <typename T>
 GMF_D void rowpart_sum(const Params& P, int64_t il, int k, T& gs, T& hs) {
+  // all CT loads issued before the (fixed-order) adds
+  constexpr int MAXCT = 16;
   const T* rp = tptr<T>(P.rowpart);
-  T g = T(0), h = T(0);
-  for (int ct = 0; ct < P.CT; ++ct) {
-    const T* src = rp + ((int64_t)ct * P.nstar_max + il) * (2 * P.Kr);
-    g += ldcg_t<T>(src + k);
-    h += ldcg_t<T>(src + P.Kr + k);
+  const int64_t cstride = P.nstar_max * (2 * P.Kr);
+  const T* src = rp + il * (2 * P.Kr) + k;
+  T gv[MAXCT], hv[MAXCT];
+  #pragma unroll
+  for (int ct = 0; ct < MAXCT; ++ct) {
+    gv[ct] = ct < P.CT ? ldcg_t<T>(src + ct * cstride) : T(0);
+    hv[ct] = ct < P.CT ? ldcg_t<T>(src + ct * cstride + P.Kr) : T(0);
   }
+  T g = T(0), h = T(0);
+  #pragma unroll
+  for (int ct = 0; ct < MAXCT; ++ct) { g += gv[ct]; h += hv[ct]; }
   gs = g;
   hs = h;
 }
@@ -372,12 +414,22 @@ GMF_D void rowpart_sum(const Params& P, int64_t il, int k, T& gs, T& hs) {
 template <typename T>
 GMF_D void snapshot_dirty(const Params& P, long long skip, long long since, int64_t first,
                           int64_t stride) {
+  // dirty flags are staged through shared memory 1024 blocks at a time so
+  // the scan costs one load round trip, not one per block
+  __shared__ unsigned char dirty[1024];
   const T* src = tptr<T>(P.th_row);
   T* dst = tptr<T>(P.sn_row);
-  for (int64_t r = 0; r < P.R; ++r) {
-    if (r == skip || P.last_mod[r] < since) continue;
-    const int64_t a = P.rbp[r] * P.Kr, b = P.rbp[r + 1] * P.Kr;
-    for (int64_t e = a + first; e < b; e += stride) dst[e] = src[e];
+  for (int64_t r0 = 0; r0 < P.R; r0 += 1024) {
+    const int64_t nr = P.R - r0 < 1024 ? P.R - r0 : 1024;
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < nr; r += blockDim.x)
+      dirty[r] = (r0 + r != skip && __ldcg(P.last_mod + r0 + r) >= since) ? 1 : 0;
+    __syncthreads();
+    for (int64_t r = 0; r < nr; ++r) {
+      if (!dirty[r]) continue;
+      const int64_t a = P.rbp[r0 + r] * P.Kr, b = P.rbp[r0 + r + 1] * P.Kr;
+      for (int64_t e = a + first; e < b; e += stride) dst[e] = src[e];
+    }
   }
 }
 

@@ -159,11 +159,13 @@ __global__ void __launch_bounds__(kThreads) k_blocknorm(Params P) {
   if (threadIdx.x == 0) { P.blocksum[2 * r] = ng; P.blocksum[2 * r + 1] = nu; }
 }
 
-// Y at the tracked entries, looked up once per fit (the sample is fixed)
-__global__ void __launch_bounds__(kThreads) k_eval_y(Params P, int32_t* out) {
+// tracked entries packed (row, col, Y, 0), built once per fit (the sample is fixed)
+__global__ void __launch_bounds__(kThreads) k_eval_pack(Params P, int4* out) {
   for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < P.E;
-       e += (int64_t)gridDim.x * kThreads)
-    out[e] = (int32_t)y_lookup(P, P.erow[e], P.ecol[e]);
+       e += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = P.erow[e], j = P.ecol[e];
+    out[e] = make_int4((int)i, (int)j, (int)y_lookup(P, i, j), 0);
+  }
 }
 
 // standalone gradient outputs (gradients.py:109-112) from the K1 partials
@@ -268,12 +270,12 @@ int launch_blocknorm(const Params& P, int dtype, cudaStream_t st) {
   return GMF_OK;
 }
 
-int launch_eval_y(const Params& P, int32_t* out, cudaStream_t st) {
+int launch_eval_pack(const Params& P, int4* out, cudaStream_t st) {
   if (P.E <= 0) return GMF_OK;
   int64_t b = (P.E + kThreads - 1) / kThreads;
   if (b > 4 * kSMs) b = 4 * kSMs;
-  k_eval_y<<<(unsigned)b, kThreads, 0, st>>>(P, out);
-  GMF_LAUNCH_CHECK("k_eval_y");
+  k_eval_pack<<<(unsigned)b, kThreads, 0, st>>>(P, out);
+  GMF_LAUNCH_CHECK("k_eval_pack");
   return GMF_OK;
 }
 
