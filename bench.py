@@ -293,6 +293,12 @@ def main():
         ms = float(t.item())
     status = fit.status()
     assert status.t == W + K and not status.stopped, (status.t, status.stopped)
+    import ctypes as C
+    geo = (C.c_int64 * 8)()
+    _lib.check(fit.lib.gmf_geometry(fit.h, geo), "gmf_geometry")
+    geometry = dict(zip(["fit_ctas", "fit_row_splits", "col_tiles", "tile_cols",
+                         "step_row_splits", "feature_bucket", "k1_smem_bytes", "max_block_rows"],
+                        [int(v) for v in geo]))
     phases = None
     if args.phases and world == 1:
         import ctypes as C
@@ -423,7 +429,8 @@ def main():
                        "y_format": sp.y_format,
                        "l2": "inputs (CSR %.0f MB + factors) exceed the 126 MB L2; each step draws "
                              "a random row block" % (wl.meta.get("nnz", 0) * 8 / 1e6),
-                       "parallelism": f"rows of each block split x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": f"rows of each block split x{world}" if world > 1 else "1 GPU",
+                       "geometry": geometry},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 3 * K, "clocks": clocks,
         }

@@ -193,6 +193,10 @@ int gmf_record_copy(gmf_handle* h, void* dst, void* stream);
 int gmf_run(gmf_handle* h, int64_t n_steps, void* stream);
 
 int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream);   /* syncs stream */
+/* Divergence snapshot bookkeeping (copy-on-write): ver[r] (R entries, host)
+ * and the current snapshot period; the snapshot's rows of block r are
+ * snap_row if ver[r] == period, else the live theta_row. */
+int gmf_snapshot_blocks(gmf_handle* h, int64_t* ver, int64_t* period, void* stream);
 /* Asynchronous D2H of the raw status word (gmf_status_raw_bytes() bytes) into
  * host memory (pinned for true asynchrony); decode later on the host. */
 int64_t gmf_status_raw_bytes(void);
@@ -209,6 +213,9 @@ int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_m
  * barrier 1, phase-2 end).  `out` holds gmf_profile_len(h) doubles; reads
  * (if out) and resets the counters, then enables/disables. */
 int64_t gmf_profile_len(gmf_handle* h);
+/* launch geometry: {persistent CTAs, its row splits, column tiles, tile
+ * width, per-step-kernel row splits, feature bucket, K1 smem bytes, max |I|} */
+int gmf_geometry(gmf_handle* h, int64_t* out8);
 int gmf_profile(gmf_handle* h, int enable, double* out, void* stream);
 /* host copies of the first n trace entries (objective, nb shape) */
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);

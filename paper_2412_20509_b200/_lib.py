@@ -100,11 +100,13 @@ SIGNATURES = {
     "gmf_status_read": (C.c_int, [_P, C.POINTER(GmfStatus), _P]),
     "gmf_trace_read": (C.c_int, [_P, _pd, _pd, _i64, _P]),
     "gmf_status_raw_bytes": (_i64, []),
+    "gmf_snapshot_blocks": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P]),
     "gmf_status_copy_async": (C.c_int, [_P, _P, _P]),
     "gmf_status_decode": (C.c_int, [_P, C.POINTER(GmfStatus)]),
     "gmf_time_grad": (C.c_int, [_P, _i64, _i32, _pd, _P]),
     "gmf_profile": (C.c_int, [_P, C.c_int, _pd, _P]),
     "gmf_profile_len": (_i64, [_P]),
+    "gmf_geometry": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),
     "gmf_cross_rows": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _P, _i64, _i32, _i32,

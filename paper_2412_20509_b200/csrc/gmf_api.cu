@@ -227,7 +227,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.rnpart = (double*)(base + o_rnp);
   P.cnpart = (double*)(base + o_cnp);
   P.blocksum = (double*)(base + o_bs);
-  P.last_mod = (long long*)(base + o_lm);
+  P.snap_ver = (long long*)(base + o_lm);
   P.rho_tab = (double*)(base + o_rho);
   P.alpt_tab = (double*)(base + o_alp);
   h->full_part = (double*)(base + o_fp);
@@ -283,13 +283,12 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
   const Params& P = h->P;
   Ctrl c;
   memset(&c, 0, sizeof(c));
-  c.last_snap_t = -1;
   c.nb_shape = nb_shape;
   c.phi = h->cfg.phi;
   GMF_CUDA(cudaStreamSynchronize(st));
   *h->host_ctrl = c;
   GMF_CUDA(cudaMemcpyAsync(P.ctrl, h->host_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-  GMF_CUDA(cudaMemsetAsync(P.last_mod, 0xFF, P.R * 8, st));
+  GMF_CUDA(cudaMemsetAsync(P.snap_ver, 0, P.R * 8, st));
   GMF_CUDA(cudaMemsetAsync(P.tickets, 0, (2 * P.CT + 4) * 4, st));
   const int64_t rb = P.n * P.Kr * h->tsz, cb = P.m * P.Kc * h->tsz;
   if (rb) {
@@ -408,7 +407,31 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
 
 int64_t gmf_status_raw_bytes(void) { return (int64_t)sizeof(Ctrl); }
 
+int gmf_snapshot_blocks(gmf_handle* h, int64_t* ver, int64_t* period, void* stream) {
+  if (!h || !ver || !period) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  GMF_CUDA(cudaMemcpyAsync(ver, h->P.snap_ver, h->P.R * 8, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaMemcpyAsync(h->host_ctrl, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  *period = h->host_ctrl->snap_period;
+  return GMF_OK;
+}
+
 int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 8 * (int64_t)h->fit_grid : 0; }
+
+int gmf_geometry(gmf_handle* h, int64_t* out8) {
+  if (!h || !out8) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  out8[0] = h->fit_grid;
+  out8[1] = h->fit_rs;
+  out8[2] = h->P.CT;
+  out8[3] = h->P.TC;
+  out8[4] = h->P.RS;
+  out8[5] = h->NK;
+  out8[6] = grad_smem_bytes(h->desc.dtype, h->NK, h->P.has_w, h->P.Kr, h->P.Kc);
+  out8[7] = h->P.nstar_max;
+  return GMF_OK;
+}
 
 int gmf_profile(gmf_handle* h, int enable, double* out6, void* stream) {
   if (!h) { set_error("null handle"); return GMF_ERR_STATE; }

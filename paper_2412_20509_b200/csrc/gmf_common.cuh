@@ -96,6 +96,14 @@ GMF_D T mean_of_eta_t(int lcode, T eta) {
 // xlogy(y, y/mu) with 0 log 0 = 0 (scipy.special.xlogy)
 GMF_HD double xlogy_ratio(double y, double mu) { return y == 0.0 ? 0.0 : y * log(y / mu); }
 
+// fp32 unit deviance for the fp32 path's tracked objective (Poisson / NB);
+// callers accumulate in fp64
+GMF_D float unit_deviance_f(int fcode, float y, float mu, float alpha) {
+  const float xl = y == 0.f ? 0.f : y * __logf(y / mu);
+  if (fcode == GMF_POISSON) return 2.f * (xl - (y - mu));
+  return 2.f * (xl - (y + alpha) * log1pf((y - mu) / (mu + alpha)));
+}
+
 GMF_HD double unit_deviance(int fcode, double y, double mu, double alpha) {
   switch (fcode) {
     case GMF_POISSON: return 2.0 * (xlogy_ratio(y, mu) - (y - mu));

@@ -25,7 +25,7 @@ enum { R_DEV = 0, R_NGAM = 1, R_NU = 2, R_NB = 3, R_NV = 4, R_NBNUM = 5, R_NBDEN
 struct Ctrl {
   long long t;                  // steps applied
   long long trace_len;          // objective_trace entries
-  long long last_snap_t;        // step index of the last snapshot (-1: none)
+  long long snap_period;        // number of snapshot points passed (copy-on-write epoch)
   long long snapshot_trace_len;
   double nb_shape;
   double phi;
@@ -89,7 +89,11 @@ struct Params {
   double* rnpart;      // [n_row_ctas][2]
   double* cnpart;      // [fit CTAs][2] column-norm partials (persistent kernel)
   double* blocksum;    // [R][2] (gamma, u) squared norms per row block
-  long long* last_mod; // [R]
+  // Divergence snapshots are copy-on-write: snap_ver[r] is the snapshot
+  // period in which block r's pre-snapshot rows were saved to sn_row.  The
+  // snapshot of period k is sn_row for blocks with snap_ver == k and the
+  // live theta_row for the others (untouched since the snapshot point).
+  long long* snap_ver; // [R]
   int TC, RS, CT;
   int64_t nstar_max, jmax;
   int n_obj_ctas, n_row_ctas, n_col_ctas;
@@ -113,6 +117,33 @@ template <>
 GMF_D float ldcg_t<float>(const float* p) { return __ldcg(p); }
 template <>
 GMF_D double ldcg_t<double>(const double* p) { return __ldcg(p); }
+
+// N-wide gathers with branch-free bounds: out-of-range lanes read a clamped
+// valid address and are zeroed by a select, so the compiler issues every
+// load before the first use (one round trip instead of N)
+template <int N, typename T>
+GMF_D void gather_vec(const T* base, int count, T (&out)[N]) {
+  if (count <= 0) {
+    #pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = T(0);
+    return;
+  }
+  #pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int kk = k < count ? k : 0;
+    const T v = base[kk];
+    out[k] = k < count ? v : T(0);
+  }
+}
+template <int N, typename T>
+GMF_D void gather_vec_cg(const T* base, int64_t stride, int count, T (&out)[N]) {
+  #pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int kk = k < count ? k : 0;
+    const T v = ldcg_t<T>(base + kk * stride);
+    out[k] = k < count ? v : T(0);
+  }
+}
 
 // block-wide sum with the result broadcast to every thread (fixed order)
 template <int NT>
@@ -207,7 +238,7 @@ GMF_D Ctrl advance(const Params& P, const Ctrl& C, const Decision& D, double nb_
     N.diverged_init = D.div_init;
   }
   if (D.snap) {
-    N.last_snap_t = C.t;
+    N.snap_period = C.snap_period + 1;
     N.snapshot_trace_len = N.trace_len;
   }
   if (!D.stop) {

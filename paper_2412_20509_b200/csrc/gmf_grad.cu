@@ -85,22 +85,40 @@ GMF_D double obj_dev_partial(const Params& P, double alpha, int64_t first, int64
   const T* zg = tptr<T>(P.z);
   const T* wg = tptr<T>(P.w);
   const int p = P.p, q = P.q, d = P.d, Kr = P.Kr, Kc = P.Kc;
+  const T* offg = tptr<T>(P.off);
   double s = 0.0;
+  // every gather of an entry in flight before any math (branch-free bounds)
+  constexpr int W = 4;   // covariate widths p, q handled 4 at a time
   for (int64_t e = first; e < P.E; e += stride) {
     const int4 en = P.ep[e];
     const int64_t i = en.x, j = en.y;
-    double eta = P.has_off ? (double)tptr<T>(P.off)[i] : 0.0;
+    T uu[NK], vv[NK];
+    gather_vec<NK>(tr + i * Kr + q, d, uu);
+    gather_vec<NK>(tc + j * Kc + p, d, vv);
+    const T of = P.has_off ? offg[i] : T(0);
+    const T wv = P.has_w ? wg[i * P.m + j] : T(1);
+    double eta = (double)of;
+    for (int k0 = 0; k0 < p; k0 += W) {
+      T xb[W], bb[W];
+      gather_vec<W>(xg + i * p + k0, p - k0, xb);
+      gather_vec<W>(tc + j * Kc + k0, p - k0, bb);
+      #pragma unroll
+      for (int k = 0; k < W; ++k) eta += (double)xb[k] * (double)bb[k];
+    }
+    for (int k0 = 0; k0 < q; k0 += W) {
+      T gg[W], zz[W];
+      gather_vec<W>(tr + i * Kr + k0, q - k0, gg);
+      gather_vec<W>(zg + j * q + k0, q - k0, zz);
+      #pragma unroll
+      for (int k = 0; k < W; ++k) eta += (double)gg[k] * (double)zz[k];
+    }
     #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < d) eta += (double)tr[i * Kr + q + k] * (double)tc[j * Kc + p + k];
-    #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < p) eta += (double)xg[i * p + k] * (double)tc[j * Kc + k];
-    #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < q) eta += (double)tr[i * Kr + k] * (double)zg[j * q + k];
-    const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-    s += w * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
+    for (int k = 0; k < NK; ++k) eta += (double)uu[k] * (double)vv[k];
+    if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
+      s += (double)wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta),
+                                                (float)alpha);
+    else
+      s += (double)wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
   }
   return s;
 }
@@ -164,7 +182,15 @@ k_fit(Params P, long long n_steps) {
       if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
     }
     if (boundary) {
-      double v[1] = {obj_dev_partial<T, NK>(P, C.nb_shape, gtid, gstride)};
+      // contiguous, equal entry ranges per CTA keep the objective balanced
+      const int64_t per = (P.E + G - 1) / G;
+      const int64_t lo = per * blockIdx.x, hi = lo + per < P.E ? lo + per : P.E;
+      double v[1] = {0.0};
+      {
+        Params Q = P;
+        Q.E = hi;
+        v[0] = obj_dev_partial<T, NK>(Q, C.nb_shape, lo + threadIdx.x, kThreads);
+      }
       block_sum_vec<1>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
     }
@@ -173,6 +199,21 @@ k_fit(Params P, long long n_steps) {
     if (run_grad && rs < RS) grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
     if (prof) { t_b = gtimer(); P.prof[1] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 2] = gtimer(); }
+    // Phase-2 inputs that phase 1 does not write are read before the barrier
+    // so their latency hides behind it: this thread's first two row
+    // coordinates (theta, EMA state) and the block's snapshot version.
+    const long long sv = blk >= 0 ? __ldcg(P.snap_ver + blk) : 0;
+    const int64_t rI0 = blk >= 0 ? P.rbp[blk] : 0;
+    const int64_t nIK = blk >= 0 ? (P.rbp[blk + 1] - rI0) * Kr : 0;
+    T pth[2], pgb[2], phb[2];
+    #pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t e = gtid + u * gstride;
+      const int64_t o = (rI0 * Kr) + (e < nIK ? e : 0);
+      pth[u] = ldcg_t<T>(tptr<T>(P.th_row) + o);
+      pgb[u] = ldcg_t<T>(tptr<T>(P.gb_row) + o);
+      phb[u] = ldcg_t<T>(tptr<T>(P.hb_row) + o);
+    }
     grid.sync();
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
@@ -203,48 +244,78 @@ k_fit(Params P, long long n_steps) {
     const bool upd = !D.stop;
     const double rho = upd ? P.rho_tab[t] : 0.0;
     const double at = upd ? P.alpt_tab[t] : 0.0;
+    // copy-on-write snapshot of block I (first update after a snapshot point)
+    const long long per_now = C.snap_period + (D.snap ? 1 : 0);
+    const bool cow = upd && sv != per_now;
     double nrm[4] = {0.0, 0.0, 0.0, 0.0};   // new ||Gamma_I||, ||U_I||, ||B||, ||V|| partials
-    // rows of block I (snapshot before update)
-    if (blk >= 0 && (upd || D.snap)) {
-      const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
+    // rows of block I
+    if (upd) {
       const int64_t nJ = P.cbp[sidx + 1] - P.cbp[sidx];
       const double s_row = (double)P.m / (double)nJ;
-      for (int64_t e = gtid; e < nI * Kr; e += gstride) {
+      for (int64_t e = gtid, u = 0; e < nIK; e += gstride, ++u) {
         const int64_t il = e / Kr;
         const int k = (int)(e % Kr);
-        const int64_t i = r0 + il;
-        T* th = tptr<T>(P.th_row) + i * Kr + k;
-        if (D.snap) tptr<T>(P.sn_row)[i * Kr + k] = *th;
-        if (upd) {
-          T gs, hs;
-          rowpart_sum<T>(P, il, k, gs, hs);
-          const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_row) + i * Kr + k,
-                                      tptr<T>(P.hb_row) + i * Kr + k, gs, hs, s_row,
-                                      k < P.q ? P.lam_g : P.lam_u, rho, at);
-          nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
-        }
+        const int64_t o = rI0 * Kr + e;
+        T gs, hs;
+        rowpart_sum<T>(P, il, k, gs, hs);
+        const T old = u < 2 ? pth[u] : ldcg_t<T>(tptr<T>(P.th_row) + o);
+        const T ogb = u < 2 ? pgb[u] : ldcg_t<T>(tptr<T>(P.gb_row) + o);
+        const T ohb = u < 2 ? phb[u] : ldcg_t<T>(tptr<T>(P.hb_row) + o);
+        if (cow) tptr<T>(P.sn_row)[o] = old;
+        const double lam = k < P.q ? P.lam_g : P.lam_u;
+        const T G_ = T(s_row) * gs + T(lam) * old;
+        const T H_ = T(s_row) * hs + T(lam);
+        const T gn = (T(1) - T(P.a1)) * ogb + T(P.a1) * G_;
+        const T hn = (T(1) - T(P.a2)) * ohb + T(P.a2) * H_;
+        const T nvv = old + T(rho) * (-T(at) * gn / (hn + T(P.damp)));
+        tptr<T>(P.gb_row)[o] = gn;
+        tptr<T>(P.hb_row)[o] = hn;
+        tptr<T>(P.th_row)[o] = nvv;
+        nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
       }
     }
     if (prof) { t_b = gtimer(); P.prof[7] += t_b - t_a; }
-    // columns of block J: one warp per coordinate, lanes split the K1 row
-    // splits, fixed butterfly order; lane 0 snapshots and updates
+    // columns of block J: a group of 8 lanes per coordinate splits the K1 row
+    // splits (all loads in flight), fixed xor-butterfly order inside the
+    // group; the group's first lane snapshots and updates
     if (upd) {
       const int64_t j0 = P.cbp[sidx], nJ = P.cbp[sidx + 1] - j0;
       const double s_col = P.rbscale[blk];
       const T* cpart = tptr<T>(P.colpart);
       const int64_t rstride = (int64_t)TC * kk;
-      for (int64_t e = gw; e < nJ * Kc; e += nw) {
-        const int64_t pos = e / Kc;
-        const int k = (int)(e % Kc);
+      const int sub = lane & 7;
+      const int64_t gg = gtid >> 3, ng = gstride >> 3;
+      const int64_t ne = nJ * Kc;
+      const int64_t rounds = (ne + ng - 1) / ng;   // uniform trip count (shuffles)
+      for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int64_t e = gg + rd * ng;
+        const bool live = e < ne;
+        const int64_t ee = live ? e : 0;
+        const int64_t pos = ee / Kc;
+        const int k = (int)(ee % Kc);
         const T* base = cpart + ((pos / TC) * RS * TC + (pos % TC)) * kk + k;
+        constexpr int MAXU = 16;   // 128 row splits per pass
         T g = T(0), h = T(0);
-        for (int r = lane; r < RS; r += 32) {
-          g += ldcg_t<T>(base + r * rstride);
-          h += ldcg_t<T>(base + r * rstride + Kc);
+        for (int r0 = 0; r0 < RS; r0 += 8 * MAXU) {
+          T gv[MAXU], hv[MAXU];
+          #pragma unroll
+          for (int u = 0; u < MAXU; ++u) {   // clamped addresses: all loads in flight
+            const int r = r0 + sub + 8 * u;
+            const int rc = r < RS ? r : 0;
+            const T gx = ldcg_t<T>(base + rc * rstride);
+            const T hx = ldcg_t<T>(base + rc * rstride + Kc);
+            gv[u] = r < RS ? gx : T(0);
+            hv[u] = r < RS ? hx : T(0);
+          }
+          #pragma unroll
+          for (int u = 0; u < MAXU; ++u) { g += gv[u]; h += hv[u]; }
         }
-        g = warp_sum<T>(g);
-        h = warp_sum<T>(h);
-        if (lane == 0) {
+        #pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+          h += __shfl_xor_sync(0xffffffffu, h, o);
+        }
+        if (live && sub == 0) {
           const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
           T* th = tptr<T>(P.th_col) + j * Kc + k;
           if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
@@ -267,7 +338,6 @@ k_fit(Params P, long long n_steps) {
         nrm[(int)(e % Kc) < P.p ? 2 : 3] += (double)x * (double)x;
       }
     }
-    if (D.snap) snapshot_dirty<T>(P, blk, C.last_snap_t, gtid, gstride);
     if (prof) { t_b = gtimer(); P.prof[9] += t_b - t_a; }
     block_sum_vec<4>(nrm, scr);
     if (prof) { t_b = gtimer(); P.prof[10] += t_b - t_a; }
@@ -285,7 +355,7 @@ k_fit(Params P, long long n_steps) {
         P.trace_obj[C.trace_len] = D.obj;
         P.trace_nb[C.trace_len] = C.nb_shape;
       }
-      if (upd) P.last_mod[blk] = t;
+      if (cow) P.snap_ver[blk] = per_now;
       *P.ctrl = N;
     }
     C = N;

@@ -64,21 +64,44 @@ GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double*
 }
 
 // ---------------------------------------------------------------------------
+// cp.async (LDGSTS) helpers: 4/8-byte copies with zero fill
+// ---------------------------------------------------------------------------
+template <int BYTES>
+GMF_D void cp_async(void* sdst, const void* gsrc, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  const int n = valid ? BYTES : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(s), "l"(gsrc), "n"(BYTES),
+               "r"(n)
+               : "memory");
+}
+GMF_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+GMF_D void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // K1 body: fused minibatch gradient for one CTA tile.
 //
-// The CTA owns TC columns (column tile `ct` of block J) and a contiguous
-// range of TR-row chunks of block I (row split `rs` of RS).  Per entry:
+// The CTA owns TC columns (column tile `ct` of block J) and a contiguous,
+// balanced row range of block I (row split `rs` of RS), walked in TR-row
+// chunks.  Per entry:
 //   eta = offset_i + [x_i|u_i|gamma_i] . [b_j|v_j|z_j]       (model.py:229-256)
 //   mu  = exp(eta)                                             (_ref.py:21-32)
 //   dotD, ddotD  (Poisson / NB with log link)                  (_core.pyx:79-103)
 // Column side sum_i dotD_ij [x_i, u_i] (ddotD with squares) accumulates in
 // registers (thread == column) across all rows of the CTA; the row side
-// sum_j dotD_ij [z_j, v_j] is a small shared-memory GEMM over the chunk's
-// P tile (gradients.py:102-113).  eta and mu stay in registers.  Outputs:
-// rowpart[ct][row][2Kr], colpart[ct][rs][c][2Kc], nbpart[ct*RS+rs][2].
+// sum_j dotD_ij [z_j, v_j] is a small shared-memory GEMM over the chunk's P
+// tile (gradients.py:102-113).  eta and mu stay in registers.
+//
+// Software pipeline: the next chunk's row features, offsets and Y (the
+// chunk's CSR nonzeros are one contiguous range; dense rows are contiguous)
+// are copied into the other staging buffer with cp.async while the current
+// chunk computes, so global latency overlaps the FMA work.
+// Outputs: rowpart[ct][row][2Kr], colpart[ct][rs][c][2Kc], nbpart[ct*RS+rs][2].
 // ---------------------------------------------------------------------------
+constexpr int kStageCap = 2048;   // CSR nonzeros staged per chunk (else direct path)
+constexpr int kRpMax = 192;       // CSR row pointers staged per CTA row range
+
 struct GradSmem {
-  int64_t rd, P, a, cd2, off, rm, rp, y, w, red, cp, total;
+  int64_t rd, P, red, rp, ytile, stage[2], a[2], cd2[2], off[2], wt[2], total, stage_bytes;
 };
 
 GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
@@ -87,23 +110,23 @@ GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
   auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
   s.rd = o; o = al(o + (int64_t)2 * TC * NK * tsz);
   s.P = o; o = al(o + (int64_t)2 * TC * (TR + 1) * tsz);
-  const int64_t region = o;
-  int64_t r = region;
-  s.a = r; r = al(r + (int64_t)TR * NK * tsz);
-  s.cd2 = r; r = al(r + (int64_t)TR * NK * tsz);
-  s.off = r; r = al(r + (int64_t)TR * tsz);
-  s.rm = r; r = al(r + (int64_t)TR * tsz);
-  s.rp = r; r = al(r + (int64_t)(TR + 1) * 8);
-  s.y = r; r = al(r + (int64_t)TR * TC * tsz);
-  s.w = r; r = al(r + (has_w ? (int64_t)TR * TC * tsz : 0));
-  const int64_t p1 = r - region;
-  const int64_t red = al((int64_t)NQ * 2 * Kr * (TR + 1) * tsz);
-  const int64_t cp = al((int64_t)TC * (2 * Kc + 1) * tsz);
-  s.red = region;
-  s.cp = region;
-  int64_t mx = p1 > red ? p1 : red;
-  mx = mx > cp ? mx : cp;
-  s.total = region + mx;
+  const int64_t red = (int64_t)NQ * 2 * Kr * (TR + 1) * tsz;
+  const int64_t cp = (int64_t)TC * (2 * Kc + 1) * tsz;
+  s.red = o; o = al(o + red);   // (column partials reuse the P region at the end)
+  (void)cp;
+  s.rp = o; o = al(o + (int64_t)(kRpMax + 1) * 8);
+  s.ytile = o; o = al(o + (int64_t)TR * TC * 4);
+  // a stage holds either the dense int32 Y tile or the CSR (col, val) range
+  const int64_t dense = (int64_t)TR * TC * 4, csr = (int64_t)kStageCap * 8;
+  s.stage_bytes = dense > csr ? dense : csr;
+  for (int b = 0; b < 2; ++b) {
+    s.stage[b] = o; o = al(o + s.stage_bytes);
+    s.a[b] = o; o = al(o + (int64_t)TR * NK * tsz);
+    s.cd2[b] = o; o = al(o + (int64_t)TR * NK * tsz);
+    s.off[b] = o; o = al(o + (int64_t)TR * tsz);
+    s.wt[b] = o; o = al(o + (has_w ? (int64_t)TR * TC * tsz : 0));
+  }
+  s.total = o;
   return s;
 }
 
@@ -117,15 +140,22 @@ GMF_D double exp_pre(double x) { return exp(x); }
 template <typename T> struct Pre { static constexpr double s = 1.4426950408889634; };
 template <> struct Pre<double> { static constexpr double s = 1.0; };
 
+GMF_D float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+GMF_D double rcp_fast(double x) { return 1.0 / x; }
+
 // phase 1 of one chunk: eta, mu, dotD, ddotD per entry; column side into
 // registers; P tile into shared memory.  Branch-free: invalid rows/columns
 // carry weight 0, which zeroes dotD, ddotD and the NB moment terms.
 template <typename T, int FAM, int NK, int TC, bool HW>
 GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
-                  const T* __restrict__ off_s, const T* __restrict__ rm_s,
-                  const T* __restrict__ y_s, const T* __restrict__ w_s, T* __restrict__ P_s,
-                  const T (&cf)[NK], T (&gacc)[NK], T (&hacc)[NK], T cm, int c, int g, int rows,
-                  T rphi, T tphi, T ralpha, T& cn, T& cd) {
+                  const T* __restrict__ off_s, const int32_t* __restrict__ y_s,
+                  const T* __restrict__ w_s, T* __restrict__ P_s, const T (&cf)[NK],
+                  T (&gacc)[NK], T (&hacc)[NK], T cm, int c, int g, int rows, T rphi, T tphi,
+                  T ralpha, T& cn, T& cd) {
   constexpr int NG = kThreads / TC;
   #pragma unroll 2
   for (int rr = g; rr < rows; rr += NG) {
@@ -137,8 +167,8 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
       e1 = fma(a[k + 1], cf[k + 1], e1);
     }
     const T mu = exp_pre(e0 + e1);
-    const T yv = y_s[rr * TC + c];
-    const T wv = HW ? w_s[rr * TC + c] : rm_s[rr] * cm;
+    const T yv = (T)y_s[rr * TC + c];
+    const T wv = HW ? w_s[rr * TC + c] : cm;
     const T r = yv - mu;
     T dd, hh;
     if (FAM == 0) {
@@ -146,7 +176,7 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
       dd = -ws * r;
       hh = ws * mu;
     } else {
-      const T inv = wv * rcp_t(tphi * fma(mu, ralpha, T(1)));
+      const T inv = wv * rcp_fast(tphi * fma(mu, ralpha, T(1)));
       dd = -r * inv;
       hh = mu * inv;
       cn = fma(wv * mu, mu, cn);
@@ -169,25 +199,25 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   constexpr int NG = kThreads / TC;
   constexpr int TCQ = TC / NQ;
   __shared__ double red_scr[kThreads / 32];
+  __shared__ int stage_n[2];   // staged CSR nonzeros per buffer, -1 = overflow
   const int tid = threadIdx.x;
   const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
   const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
   const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
   // this row split's contiguous rows of block I, balanced to within one row
   const int64_t rlo = nI * rs / RS, rhi = nI * (rs + 1) / RS;
+  const int64_t nrows = rhi - rlo;
+  const bool csr = P.yfmt != GMF_Y_DENSE_I32;
+  const bool rp_staged = csr && nrows <= kRpMax;
+  const int64_t cbase = (int64_t)ct * TC;
 
   const GradSmem L = grad_smem(TC, NK, sizeof(T), P.has_w, Kr, Kc);
   T* rd_s = reinterpret_cast<T*>(smem + L.rd);
   T* P_s = reinterpret_cast<T*>(smem + L.P);
-  T* a_s = reinterpret_cast<T*>(smem + L.a);
-  T* cd2_s = reinterpret_cast<T*>(smem + L.cd2);
-  T* off_s = reinterpret_cast<T*>(smem + L.off);
-  T* rm_s = reinterpret_cast<T*>(smem + L.rm);
-  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
-  T* y_s = reinterpret_cast<T*>(smem + L.y);
-  T* w_s = reinterpret_cast<T*>(smem + L.w);
   T* red_s = reinterpret_cast<T*>(smem + L.red);
-  T* cp_s = reinterpret_cast<T*>(smem + L.cp);
+  T* cp_s = reinterpret_cast<T*>(smem + L.P);
+  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
+  int32_t* ytile = reinterpret_cast<int32_t*>(smem + L.ytile);
 
   const T* th_row = tptr<T>(P.th_row);
   const T* th_col = tptr<T>(P.th_col);
@@ -199,7 +229,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
 
   // ---- this thread's column features [b | v | z] (phase 1), pre-scaled ----
   const int c = tid % TC, g = tid / TC;
-  const int64_t pos = (int64_t)ct * TC + c;
+  const int64_t pos = cbase + c;
   const bool col_ok = pos < nJ;
   const int64_t j = col_ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
   T cf[NK];
@@ -213,11 +243,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     cf[k] = v * pre;
   }
   const T cm = col_ok ? T(1) : T(0);
-  // ---- row-side design [z_j | v_j] and squares of the tile (phase 2) ----
   __syncthreads();   // smem reuse across calls (persistent kernel)
+  // ---- row-side design [z_j | v_j] and squares of the tile (phase 2) ----
   for (int e = tid; e < TC * NK; e += kThreads) {
     const int cc = e / NK, k = e % NK;
-    const int64_t pp = (int64_t)ct * TC + cc;
+    const int64_t pp = cbase + cc;
     T v = T(0);
     if (pp < nJ && k < Kr) {
       const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
@@ -226,6 +256,73 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     rd_s[cc * NK + k] = v;
     rd_s[(TC + cc) * NK + k] = v * v;
   }
+  if (rp_staged)
+    for (int64_t e = tid; e <= nrows; e += kThreads) rp_s[e] = P.rp[r0 + rlo + e];
+  if (csr)
+    for (int e = tid; e < TR * TC; e += kThreads) ytile[e] = 0;
+  __syncthreads();
+
+  // ---- asynchronous staging of one chunk into buffer b ----
+  auto issue = [&](int b, int64_t rowbase) {
+    const int rows = (int)((rhi - rowbase) < TR ? (rhi - rowbase) : TR);
+    const int64_t i0 = r0 + rowbase;
+    T* a_b = reinterpret_cast<T*>(smem + L.a[b]);
+    T* off_b = reinterpret_cast<T*>(smem + L.off[b]);
+    for (int e = tid; e < TR * NK; e += kThreads) {
+      const int rr = e / NK, k = e % NK;
+      const T* src = xg;
+      bool ok = false;
+      if (rr < rows) {
+        const int64_t i = i0 + rr;
+        if (k < p) { src = xg + i * p + k; ok = true; }
+        else if (k < p + d) { src = th_row + i * Kr + q + (k - p); ok = true; }
+        else if (k < KA) { src = th_row + i * Kr + (k - p - d); ok = true; }
+      }
+      cp_async<sizeof(T)>(a_b + e, src, ok);
+    }
+    if (tid < TR) {
+      const bool ok = tid < rows && P.has_off;
+      cp_async<sizeof(T)>(off_b + tid, ok ? offg + i0 + tid : offg, ok);
+    }
+    if (P.has_w) {
+      T* w_b = reinterpret_cast<T*>(smem + L.wt[b]);
+      for (int e = tid; e < TR * TC; e += kThreads) {
+        const int rr = e / TC, cc = e % TC;
+        const int64_t pp = cbase + cc;
+        const bool ok = rr < rows && pp < nJ;
+        const int64_t jj = ok ? (P.col_identity ? pp : (int64_t)P.cidx[j0 + pp]) : 0;
+        cp_async<sizeof(T)>(w_b + e, ok ? wg + (i0 + rr) * P.m + jj : wg, ok);
+      }
+    }
+    unsigned char* st = smem + L.stage[b];
+    if (!csr) {
+      int32_t* y_b = reinterpret_cast<int32_t*>(st);
+      for (int e = tid; e < TR * TC; e += kThreads) {
+        const int rr = e / TC, cc = e % TC;
+        const int64_t pp = cbase + cc;
+        const bool ok = rr < rows && pp < nJ;
+        const int64_t jj = ok ? (P.col_identity ? pp : (int64_t)P.cidx[j0 + pp]) : 0;
+        cp_async<4>(y_b + e, ok ? P.y + (i0 + rr) * P.m + jj : P.y, ok);
+      }
+    } else if (rp_staged) {
+      const int64_t lo = rp_s[rowbase - rlo], hi = rp_s[rowbase - rlo + rows];
+      const int64_t nnz = hi - lo;
+      if (nnz <= kStageCap) {
+        int32_t* col_b = reinterpret_cast<int32_t*>(st);
+        int32_t* val_b = col_b + kStageCap;
+        for (int64_t e = tid; e < nnz; e += kThreads) {
+          cp_async<4>(col_b + e, P.ci + lo + e, true);
+          cp_async<4>(val_b + e, P.cv + lo + e, true);
+        }
+        if (tid == 0) stage_n[b] = (int)nnz;
+      } else if (tid == 0) {
+        stage_n[b] = -1;
+      }
+    } else if (tid == 0) {
+      stage_n[b] = -1;
+    }
+    cp_async_commit();
+  };
 
   T gacc[NK], hacc[NK];
   #pragma unroll
@@ -234,85 +331,83 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const T rphi = T(1.0 / P.phi);
   const T ralpha = T(1.0 / alpha);
   const T tphi = T(P.phi);
-
   const int pr = tid % TR, ph = (tid / TR) & 1, pq = tid / (2 * TR);
   const int rkk = 2 * Kr;
+  // incremental (row, component) walk of the row-partial output loop
+  const int o_rr0 = tid / rkk, o_hk0 = tid % rkk, o_dq = kThreads / rkk, o_dr = kThreads % rkk;
 
-  for (int64_t rowbase = rlo; rowbase < rhi; rowbase += TR) {
+  if (nrows > 0) issue(0, rlo);
+  int b = 0;
+  for (int64_t rowbase = rlo; rowbase < rhi; rowbase += TR, b ^= 1) {
     const int rows = (int)((rhi - rowbase) < TR ? (rhi - rowbase) : TR);
     const int64_t i0 = r0 + rowbase;
-    __syncthreads();   // previous chunk's red_s reads are done
-    // ---- row features [x | u | gamma], squares, offset, row mask ----
+    T* a_s = reinterpret_cast<T*>(smem + L.a[b]);
+    T* cd2_s = reinterpret_cast<T*>(smem + L.cd2[b]);
+    T* off_s = reinterpret_cast<T*>(smem + L.off[b]);
+    T* w_s = reinterpret_cast<T*>(smem + L.wt[b]);
+    unsigned char* st = smem + L.stage[b];
+    cp_async_wait0();
+    __syncthreads();   // chunk b landed; previous chunk fully consumed
+    // ---- post-process the staged chunk ----
     for (int e = tid; e < TR * NK; e += kThreads) {
-      const int rr = e / NK, k = e % NK;
-      T v = T(0);
-      if (rr < rows) {
-        const int64_t i = i0 + rr;
-        if (k < p) v = xg[i * p + k];
-        else if (k < p + d) v = th_row[i * Kr + q + (k - p)];
-        else if (k < KA) v = th_row[i * Kr + (k - p - d)];
-      }
-      a_s[rr * NK + k] = v;
-      cd2_s[rr * NK + k] = k < Kc ? v * v : T(0);
+      const T v = a_s[e];
+      cd2_s[e] = (e % NK) < Kc ? v * v : T(0);
     }
-    if (tid < TR) {
-      off_s[tid] = (tid < rows && P.has_off) ? offg[i0 + tid] * pre : T(0);
-      rm_s[tid] = tid < rows ? T(1) : T(0);
-    }
-    // ---- response tile (and weights, zero outside the block) ----
-    if (P.yfmt == GMF_Y_DENSE_I32) {
-      for (int e = tid; e < TR * TC; e += kThreads) {
-        const int rr = e / TC, cc = e % TC;
-        const int64_t pp = (int64_t)ct * TC + cc;
-        T v = T(0), wv = T(0);
-        if (rr < rows && pp < nJ) {
-          const int64_t jj = P.col_identity ? pp : (int64_t)P.cidx[j0 + pp];
-          v = (T)P.y[(i0 + rr) * P.m + jj];
-          if (P.has_w) wv = wg[(i0 + rr) * P.m + jj];
-        }
-        y_s[e] = v;
-        if (P.has_w) w_s[e] = wv;
-      }
+    if (tid < TR) off_s[tid] *= pre;
+    const int32_t* y_s;
+    if (!csr) {
+      y_s = reinterpret_cast<const int32_t*>(st);
     } else {
-      // CSR: the chunk's nonzeros are one contiguous range; stage the row
-      // pointers, then scatter the range into the dense tile in smem
-      if (tid <= rows) rp_s[tid] = P.rp[i0 + tid];
-      for (int e = tid; e < TR * TC; e += kThreads) y_s[e] = T(0);
-      __syncthreads();
-      const int64_t lo = rp_s[0], hi = rp_s[rows];
-      const int64_t cbase = (int64_t)ct * TC;
-      for (int64_t k = lo + tid; k < hi; k += kThreads) {
-        const int col = P.ci[k];
-        const int val = P.cv[k];
-        int64_t pp;
-        if (P.col_identity) pp = col;
-        else pp = (P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1;
-        const int64_t cl = pp - cbase;
-        if (pp >= 0 && cl >= 0 && cl < TC) {
-          int a = 0, b = rows;
-          while (b - a > 1) {
-            const int mid = (a + b) >> 1;
-            if (rp_s[mid] <= k) a = mid; else b = mid;
+      y_s = ytile;
+      const int n_st = stage_n[b];
+      if (n_st >= 0) {
+        // warp per row: the row index is known, no search per nonzero
+        const int32_t* col_b = reinterpret_cast<const int32_t*>(st);
+        const int32_t* val_b = col_b + kStageCap;
+        const int64_t* rpc = rp_s + (rowbase - rlo);
+        const int lo = (int)rpc[0];
+        const int lane = tid & 31;
+        for (int rr = tid >> 5; rr < rows; rr += kThreads / 32) {
+          const int a = (int)rpc[rr] - lo, bnd = (int)rpc[rr + 1] - lo;
+          for (int e = a + lane; e < bnd; e += 32) {
+            const int col = col_b[e];
+            const int pp = P.col_identity ? col : ((P.cbof[col] == s) ? P.cpos[col] : -1);
+            const int cl = pp - (int)cbase;
+            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = val_b[e];
           }
-          y_s[a * TC + cl] = (T)val;
+        }
+      } else {   // row range too long or chunk too dense: direct loads
+        for (int rr = tid >> 5; rr < rows; rr += kThreads / 32) {
+          const int64_t i = i0 + rr;
+          for (int64_t k = P.rp[i] + (tid & 31); k < P.rp[i + 1]; k += 32) {
+            const int col = P.ci[k];
+            const int64_t pp = P.col_identity ? col : ((P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1);
+            const int64_t cl = pp - cbase;
+            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = P.cv[k];
+          }
         }
       }
     }
     __syncthreads();
+    // ---- next chunk's loads fly while this one computes ----
+    if (rowbase + TR < rhi) issue(b ^ 1, rowbase + TR);
 
     // ---- phase 1 ----
     T cn = T(0), cd = T(0);
     if (P.has_w)
-      phase1<T, FAM, NK, TC, true>(a_s, cd2_s, off_s, rm_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
-                                   g, rows, rphi, tphi, ralpha, cn, cd);
+      phase1<T, FAM, NK, TC, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c, g,
+                                   rows, rphi, tphi, ralpha, cn, cd);
     else
-      phase1<T, FAM, NK, TC, false>(a_s, cd2_s, off_s, rm_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
-                                    g, rows, rphi, tphi, ralpha, cn, cd);
+      phase1<T, FAM, NK, TC, false>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c, g,
+                                    rows, rphi, tphi, ralpha, cn, cd);
     nb_num += (double)cn;
     nb_den += (double)cd;
     __syncthreads();
+    if (csr) {   // clear the Y tile for the next scatter (phase 2 does not read it)
+      for (int e = tid; e < rows * TC; e += kThreads) ytile[e] = 0;
+    }
 
-    // ---- phase 2: row side  P (TR x TC) . rd (TC x Kr) ----
+    // ---- phase 2: row side  P (rows x TC) . rd (TC x Kr) ----
     T acc[NK];
     #pragma unroll
     for (int k = 0; k < NK; ++k) acc[k] = T(0);
@@ -332,17 +427,22 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       if (k < Kr) red_s[((pq * 2 + ph) * Kr + k) * (TR + 1) + pr] = acc[k];
     __syncthreads();
     {
+      // o = rr * rkk + hk walked incrementally (no runtime division per element)
       T* outp = tptr<T>(P.rowpart) + ((int64_t)ct * P.nstar_max + rowbase) * rkk;
+      int rr = o_rr0, hk = o_hk0;
       for (int o = tid; o < rows * rkk; o += kThreads) {
-        const int rr = o / rkk, hk = o % rkk;
-        const int h = hk / Kr, k = hk % Kr;
+        const int h = hk >= Kr ? 1 : 0, k = hk - h * Kr;
         T sum = T(0);
         #pragma unroll
         for (int qq = 0; qq < NQ; ++qq) sum += red_s[((qq * 2 + h) * Kr + k) * (TR + 1) + rr];
         outp[o] = sum;
+        rr += o_dq;
+        hk += o_dr;
+        if (hk >= rkk) { hk -= rkk; ++rr; }
       }
     }
   }
+  cp_async_wait0();
   __syncthreads();
 
   // ---- column partials: fixed-order sum over the NG row groups ----
@@ -362,7 +462,16 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const int kk = 2 * Kc;
   T* colpart = tptr<T>(P.colpart);
   const int64_t cbase2 = ((int64_t)ct * RS + rs) * TC * kk;
-  for (int e = tid; e < TC * kk; e += kThreads) colpart[cbase2 + e] = cp_s[(e / kk) * ck + (e % kk)];
+  {
+    int cc = tid / kk, kx = tid % kk;
+    const int dq = kThreads / kk, dr = kThreads % kk;
+    for (int e = tid; e < TC * kk; e += kThreads) {
+      colpart[cbase2 + e] = cp_s[cc * ck + kx];
+      cc += dq;
+      kx += dr;
+      if (kx >= kk) { kx -= kk; ++cc; }
+    }
+  }
   const double bn = block_sum<kThreads>(nb_num, red_scr);
   const double bd = block_sum<kThreads>(nb_den, red_scr);
   if (tid == 0) {
@@ -392,45 +501,21 @@ GMF_D void colpart_sum(const Params& P, int64_t pos, int k, int RS, T& gs, T& hs
 // row-side sums of (row il of the block, k) over the CT column tiles
 template <typename T>
 GMF_D void rowpart_sum(const Params& P, int64_t il, int k, T& gs, T& hs) {
-  // all CT loads issued before the (fixed-order) adds
-  constexpr int MAXCT = 16;
+  // the column tiles' loads issued together, 4 per pass, fixed-order adds
+  constexpr int W = 4;
   const T* rp = tptr<T>(P.rowpart);
   const int64_t cstride = P.nstar_max * (2 * P.Kr);
   const T* src = rp + il * (2 * P.Kr) + k;
-  T gv[MAXCT], hv[MAXCT];
-  #pragma unroll
-  for (int ct = 0; ct < MAXCT; ++ct) {
-    gv[ct] = ct < P.CT ? ldcg_t<T>(src + ct * cstride) : T(0);
-    hv[ct] = ct < P.CT ? ldcg_t<T>(src + ct * cstride + P.Kr) : T(0);
-  }
   T g = T(0), h = T(0);
-  #pragma unroll
-  for (int ct = 0; ct < MAXCT; ++ct) { g += gv[ct]; h += hv[ct]; }
+  for (int c0 = 0; c0 < P.CT; c0 += W) {
+    T gv[W], hv[W];
+    gather_vec_cg<W>(src + c0 * cstride, cstride, P.CT - c0, gv);
+    gather_vec_cg<W>(src + c0 * cstride + P.Kr, cstride, P.CT - c0, hv);
+    #pragma unroll
+    for (int ct = 0; ct < W; ++ct) { g += gv[ct]; h += hv[ct]; }
+  }
   gs = g;
   hs = h;
-}
-
-// copy the rows of dirty row blocks (other than `skip`) into the snapshot
-template <typename T>
-GMF_D void snapshot_dirty(const Params& P, long long skip, long long since, int64_t first,
-                          int64_t stride) {
-  // dirty flags are staged through shared memory 1024 blocks at a time so
-  // the scan costs one load round trip, not one per block
-  __shared__ unsigned char dirty[1024];
-  const T* src = tptr<T>(P.th_row);
-  T* dst = tptr<T>(P.sn_row);
-  for (int64_t r0 = 0; r0 < P.R; r0 += 1024) {
-    const int64_t nr = P.R - r0 < 1024 ? P.R - r0 : 1024;
-    __syncthreads();
-    for (int64_t r = threadIdx.x; r < nr; r += blockDim.x)
-      dirty[r] = (r0 + r != skip && __ldcg(P.last_mod + r0 + r) >= since) ? 1 : 0;
-    __syncthreads();
-    for (int64_t r = 0; r < nr; ++r) {
-      if (!dirty[r]) continue;
-      const int64_t a = P.rbp[r0 + r] * P.Kr, b = P.rbp[r0 + r + 1] * P.Kr;
-      for (int64_t e = a + first; e < b; e += stride) dst[e] = src[e];
-    }
-  }
 }
 
 }  // namespace gmf

@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
   const double at = upd ? P.alpt_tab[t] : 0.0;
   const int Kr = P.Kr, Kc = P.Kc;
   const int bx = blockIdx.x;
+  // copy-on-write snapshot: save block I's rows on its first update after a
+  // snapshot point (snap_ver is written only by the committing last CTA)
+  const long long per_now = C.snap_period + (D.snap ? 1 : 0);
+  const bool cow = upd && P.snap_ver[blk >= 0 ? blk : 0] != per_now;
 
   if (bx < P.n_row_ctas) {
     double rg = 0.0, ru = 0.0;
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
         const int k = (int)(e % Kr);
         const int64_t i = r0 + il;
         T* th = tptr<T>(P.th_row) + i * Kr + k;
-        if (D.snap) tptr<T>(P.sn_row)[i * Kr + k] = *th;
+        if (cow) tptr<T>(P.sn_row)[i * Kr + k] = *th;
         const int64_t nJ = P.cbp[sidx + 1] - P.cbp[sidx];
         T gs, hs;
         rowpart_sum<T>(P, il, k, gs, hs);
@@ -113,11 +117,6 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
                       P.rbscale[blk], k < P.p ? P.lam_b : P.lam_v, rho, at);
       }
     }
-  } else if (D.snap) {
-    const int sc = bx - P.n_row_ctas - P.n_col_ctas;
-    const int nsc = gridDim.x - P.n_row_ctas - P.n_col_ctas;
-    snapshot_dirty<T>(P, blk, C.last_snap_t, (int64_t)sc * kThreads + threadIdx.x,
-                      (int64_t)nsc * kThreads);
   }
 
   // ---------------- commit (last CTA) ----------------
@@ -136,7 +135,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
   if (upd) {
     P.blocksum[2 * blk] = g2;
     P.blocksum[2 * blk + 1] = u2;
-    P.last_mod[blk] = t;
+    if (cow) P.snap_ver[blk] = per_now;
   }
   *P.ctrl = advance(P, C, D, nbn, nbd);
   *tk = 0u;
@@ -254,7 +253,7 @@ int launch_obj(const Params& P, int dtype, cudaStream_t st) {
 }
 
 int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t st) {
-  const int grid = P.n_row_ctas + P.n_col_ctas + kSnapCtas;
+  const int grid = P.n_row_ctas + P.n_col_ctas;
   const unsigned char* g = reinterpret_cast<const unsigned char*>(gathered);
   if (dtype == GMF_F64) k_apply<double><<<grid, kThreads, 0, st>>>(P, g);
   else k_apply<float><<<grid, kThreads, 0, st>>>(P, g);

@@ -314,9 +314,25 @@ class DeviceFit:
                    "gmf_objective_full")
         return float(out.item())
 
+    def snapshot_rows(self):
+        """Local rows of the divergence snapshot (copy-on-write reconstruction:
+        blocks saved during the current snapshot period come from snap_row,
+        the others are unchanged since the snapshot point)."""
+        R = len(self.schedule.row_blocks)
+        ver = (C.c_int64 * R)()
+        period = C.c_int64()
+        _lib.check(self.lib.gmf_snapshot_blocks(self.h, ver, C.byref(period), self.stream()),
+                   "gmf_snapshot_blocks")
+        rows = self.theta_row.clone()
+        rbp = self.rbp.cpu().numpy()
+        for r in range(R):
+            if ver[r] == period.value and rbp[r + 1] > rbp[r]:
+                rows[rbp[r]:rbp[r + 1]] = self.snap_row[rbp[r]:rbp[r + 1]]
+        return rows
+
     def download_state(self, snapshot=False, phi=None, nb_shape=None) -> FactorizationState:
         """Host FactorizationState in the original row order (single rank)."""
-        tr = (self.snap_row if snapshot else self.theta_row).double().cpu().numpy()
+        tr = (self.snapshot_rows() if snapshot else self.theta_row).double().cpu().numpy()
         tc = (self.snap_col if snapshot else self.theta_col).double().cpu().numpy()
         rows = np.empty((self.n, tr.shape[1]))
         rows[self.order] = tr

@@ -223,7 +223,8 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
         def host_state(snapshot, nb):
             if world == 1:
                 return fit.download_state(snapshot=snapshot, nb_shape=nb)
-            tr = _gather_rows(fit, fit.snap_row if snapshot else fit.theta_row, process_group, exchange)
+            tr = _gather_rows(fit, fit.snapshot_rows() if snapshot else fit.theta_row, process_group,
+                              exchange)
             tc = (fit.snap_col if snapshot else fit.theta_col).double().cpu().numpy()
             p, q = covs.p, covs.q
             return FactorizationState(tc[:, :p].copy(), tr[:, :q].copy(), tr[:, q:].copy(),
