@@ -249,7 +249,9 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
                                                   dtype=dtype, device=fit.device.index)
             dev_sum = None
         if dev_sum is None:
-            final_obj = _full_objective(final, data, covs, fam, lnk, penalty, offset, dtype,
+            # the live family: NB shape as fitted (optim.py:293-298, 401)
+            live = type(fam)(final.nb_shape) if fam.kind == "neg_binomial" else fam
+            final_obj = _full_objective(final, data, covs, live, lnk, penalty, offset, dtype,
                                         fit.device.index)
         else:
             final_obj = dev_sum / (2.0 * final.phi) + penalty_value(final, penalty)
