@@ -63,6 +63,10 @@ enum gmf_link {
 };
 
 enum gmf_yfmt { GMF_Y_DENSE_I32 = 0, GMF_Y_CSR_I32 = 1 };
+/* K1 (fused minibatch gradient) implementation: AUTO = tensor cores
+ * (tcgen05, bf16-split operands) when eligible -- fp32, no prior weights,
+ * q+d <= 16, p+d <= 16 -- else CUDA cores; TENSOR fails if ineligible. */
+enum gmf_k1_impl { GMF_K1_AUTO = 0, GMF_K1_CUDA_CORES = 1, GMF_K1_TENSOR = 2 };
 
 /* ---------------------------------------------------------------- level 1 */
 
@@ -113,6 +117,8 @@ typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py
   int64_t max_epochs;
   int32_t est_alpha;             /* NB shape estimated (optim.py:156-168) */
   int32_t snapshot_stride;       /* 4 (optim.py:309) */
+  int32_t k1_impl;               /* enum gmf_k1_impl (no reference counterpart) */
+  int32_t reserved;
 } gmf_config;
 
 typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
@@ -216,6 +222,10 @@ int64_t gmf_profile_len(gmf_handle* h);
 /* launch geometry: {persistent CTAs, its row splits, column tiles, tile
  * width, per-step-kernel row splits, feature bucket, K1 smem bytes, max |I|} */
 int gmf_geometry(gmf_handle* h, int64_t* out8);
+/* K1 implementation the handle runs (GMF_K1_CUDA_CORES or GMF_K1_TENSOR) */
+int gmf_k1_impl(gmf_handle* h);
+/* number of kernels this handle has launched so far (graph nodes counted) */
+int64_t gmf_launch_count(gmf_handle* h);
 int gmf_profile(gmf_handle* h, int enable, double* out, void* stream);
 /* host copies of the first n trace entries (objective, nb shape) */
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);

@@ -23,6 +23,8 @@ GMF_ERR_STATE = -5
 
 F32, F64 = 0, 1
 Y_DENSE_I32, Y_CSR_I32 = 0, 1
+K1_IMPL_CODES = {"auto": 0, "cuda_cores": 1, "tensor": 2}
+K1_IMPL_NAMES = {v: k for k, v in K1_IMPL_CODES.items()}
 FAMILY_CODES = {"gaussian": 0, "gamma": 1, "inverse_gaussian": 2, "poisson": 3,
                 "bernoulli": 4, "neg_binomial": 5}
 LINK_CODES = {"identity": 0, "log": 1, "logit": 2, "inverse": 3, "inverse_squared": 4}
@@ -55,7 +57,7 @@ class GmfConfig(C.Structure):
                 ("lam_u", C.c_double), ("lam_v", C.c_double), ("nb_floor", C.c_double),
                 ("nb_ceiling", C.c_double), ("phi", C.c_double), ("eval_scale", C.c_double),
                 ("max_epochs", C.c_int64), ("est_alpha", C.c_int32),
-                ("snapshot_stride", C.c_int32)]
+                ("snapshot_stride", C.c_int32), ("k1_impl", C.c_int32), ("reserved", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -107,6 +109,8 @@ SIGNATURES = {
     "gmf_profile": (C.c_int, [_P, C.c_int, _pd, _P]),
     "gmf_profile_len": (_i64, [_P]),
     "gmf_geometry": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "gmf_k1_impl": (C.c_int, [_P]),
+    "gmf_launch_count": (_i64, [_P]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),
     "gmf_cross_rows": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _P, _i64, _i32, _i32,

@@ -7,16 +7,20 @@
 #include <vector>
 
 #include "gmf_engine.cuh"
+#include <cstdio>
+#include <cstdlib>
 
 namespace gmf {
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha);
-int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int* fit_blocks_per_sm);
+int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
+                 int* fit_blocks_per_sm);
+int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int tile_cols(int dtype);
 int grad_bucket(int KA);
-int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc);
+int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm);
 int launch_obj(const Params& P, int dtype, cudaStream_t st);
 int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t st);
 int launch_blocknorm(const Params& P, int dtype, cudaStream_t st);
@@ -48,6 +52,9 @@ struct gmf_handle {
   void* prof_buf = nullptr;
   std::vector<int64_t> rbp_host, cbp_host;
   bool reset_done = false;
+  int64_t launches = 0;         // kernels this handle launched (gmf_launch_count)
+  bool residency_checked = false;
+  unsigned int* host_abort = nullptr;   // pinned: abort flag of the software grid barrier
 };
 
 namespace {
@@ -74,6 +81,30 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
   if (c->smooth_a1 <= 0 || c->smooth_a1 > 1 || c->smooth_a2 <= 0 || c->smooth_a2 > 1) { set_error("smoothing out of (0,1]"); return GMF_ERR_CONFIG; }
   if (c->tol <= 0 || c->damping < 0 || c->phi <= 0) { set_error("need tol > 0, damping >= 0, phi > 0"); return GMF_ERR_CONFIG; }
   if (c->snapshot_stride < 1) { set_error("snapshot_stride < 1"); return GMF_ERR_CONFIG; }
+  if (c->k1_impl < GMF_K1_AUTO || c->k1_impl > GMF_K1_TENSOR) { set_error("unknown k1_impl %d", c->k1_impl); return GMF_ERR_CONFIG; }
+  return GMF_OK;
+}
+
+// zero-step launch of the tensor-core fit kernel: its first grid barrier has
+// a short timeout; if some CTA is not resident the kernel aborts and the
+// grid shrinks to one CTA per SM (always resident)
+int residency_probe(gmf_handle* h, cudaStream_t st) {
+  Params P = h->P;
+  P.RS = h->fit_rs;
+  int rc = launch_fit(P, h->desc.dtype, h->NK, h->fit_grid, 0, st);
+  if (rc) return rc;
+  h->launches += 1;
+  GMF_CUDA(cudaMemcpyAsync(h->host_abort, P.gbar + 2, 4, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  if (*h->host_abort) {
+    int n_sm = kSMs;
+    GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->desc.device));
+    h->fit_grid = (n_sm / P.CT) * P.CT;
+    h->fit_rs = h->fit_grid / P.CT;
+    if (getenv("GMF_VERBOSE"))
+      fprintf(stderr, "[gmf] fit kernel CTAs not co-resident; %d CTAs (one per SM)\n", h->fit_grid);
+  }
+  h->residency_checked = true;
   return GMF_OK;
 }
 
@@ -150,6 +181,15 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.nbfloor = cfg->nb_floor; P.nbceil = cfg->nb_ceiling; P.escale = cfg->eval_scale; P.phi = cfg->phi;
   P.est_alpha = cfg->est_alpha && desc->family == GMF_NEG_BINOMIAL;
   P.snap_stride = cfg->snapshot_stride; P.world = desc->world_size;
+  // K1 implementation: tensor cores when eligible unless CUDA cores requested
+  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA);
+  if (cfg->k1_impl == GMF_K1_TENSOR && !tc_ok) {
+    set_error("k1_impl=tensor needs fp32, no prior weights, q+d <= 16, p+d <= 16 (got Kr=%d Kc=%d)",
+              Kr, Kc);
+    delete h;
+    return GMF_ERR_UNSUPPORTED;
+  }
+  P.tcm = tc_ok && cfg->k1_impl != GMF_K1_CUDA_CORES;
 
   const int TC = tile_cols(desc->dtype);
   P.TC = TC;
@@ -170,7 +210,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
 
   // persistent kernel geometry: every co-resident CTA, a multiple of CT
   int fit_bps = 0;
-  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, &fit_bps);
+  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, &fit_bps);
   if (rc) { delete h; return rc; }
   int n_sm = kSMs;
   GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
@@ -211,6 +251,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ft = take(64);
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
+  const int64_t o_gbar = take(16);
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -226,6 +267,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.objpart = (double*)(base + o_objp);
   P.rnpart = (double*)(base + o_rnp);
   P.cnpart = (double*)(base + o_cnp);
+  P.gbar = (unsigned int*)(base + o_gbar);
   P.blocksum = (double*)(base + o_bs);
   P.snap_ver = (long long*)(base + o_lm);
   P.rho_tab = (double*)(base + o_rho);
@@ -253,6 +295,8 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   GMF_CUDA(cudaMemcpy((void*)P.alpt_tab, alp.data(), ms * 8, cudaMemcpyHostToDevice));
 
   GMF_CUDA(cudaMallocHost(&h->host_ctrl, sizeof(Ctrl)));
+  GMF_CUDA(cudaMallocHost(&h->host_abort, 16));
+  *h->host_abort = 0;
   GMF_CUDA(cudaStreamCreateWithFlags(&h->internal, cudaStreamNonBlocking));
   GMF_CUDA(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
   GMF_CUDA(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
@@ -268,6 +312,7 @@ int gmf_destroy(gmf_handle* h) {
   if (h->ws) cudaFree(h->ws);
   if (h->prof_buf) cudaFree(h->prof_buf);
   if (h->host_ctrl) cudaFreeHost(h->host_ctrl);
+  if (h->host_abort) cudaFreeHost(h->host_abort);
   if (h->internal) cudaStreamDestroy(h->internal);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_b) cudaEventDestroy(h->ev_b);
@@ -301,7 +346,14 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
   }
   int rc = launch_blocknorm(P, h->desc.dtype, st);
   if (rc) return rc;
+  h->launches += 1;
   GMF_CUDA(cudaStreamSynchronize(st));
+  if (P.tcm && h->fit_grid > 0 && !h->residency_checked) {
+    // the tensor-core fit kernel synchronises with a software grid barrier:
+    // probe once that all its CTAs are co-resident, else one CTA per SM
+    rc = residency_probe(h, st);
+    if (rc) return rc;
+  }
   h->reset_done = true;
   return GMF_OK;
 }
@@ -320,6 +372,7 @@ int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, doub
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_grad(P, h->desc.dtype, h->NK, st, row_block, col_block, nb_shape);
   if (rc) return rc;
+  h->launches += 2;
   const int64_t nI = h->rbp_host[row_block + 1] - h->rbp_host[row_block];
   const int64_t nJ = h->cbp_host[col_block + 1] - h->cbp_host[col_block];
   return launch_gradout(P, h->desc.dtype, row_block, col_block, nI, nJ, g_row, h_row, g_col,
@@ -331,12 +384,14 @@ int gmf_step_local(gmf_handle* h, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_obj(h->P, h->desc.dtype, st);
   if (rc) return rc;
+  h->launches += 2;
   return launch_grad(h->P, h->desc.dtype, h->NK, st, -1, -1, 0.0);
 }
 
 int gmf_step_apply(gmf_handle* h, const void* gathered, void* stream) {
   if (!h || !h->reset_done) { set_error("gmf_step_apply before gmf_reset"); return GMF_ERR_STATE; }
   if (h->desc.world_size > 1 && !gathered) { set_error("world_size > 1 needs gathered records"); return GMF_ERR_CONFIG; }
+  h->launches += 1;
   return launch_apply(h->P, h->desc.dtype, gathered, (cudaStream_t)stream);
 }
 
@@ -360,6 +415,7 @@ int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
     // one cooperative launch runs all n_steps (grid-wide barriers between phases)
     Params P = h->P;
     P.RS = h->fit_rs;
+    h->launches += 1;
     return launch_fit(P, h->desc.dtype, h->NK, h->fit_grid, n_steps, user);
   }
   // fallback for devices without cooperative launch: per-step kernels in CUDA graphs
@@ -389,6 +445,7 @@ int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
       it = h->graphs.emplace(c, ex).first;
     }
     GMF_CUDA(cudaGraphLaunch(it->second, h->internal));
+    h->launches += 3 * c;
     left -= c;
   }
   GMF_CUDA(cudaEventRecord(h->ev_b, h->internal));
@@ -401,7 +458,12 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
   GMF_CUDA(cudaSetDevice(h->desc.device));
   cudaStream_t st = (cudaStream_t)stream;
   GMF_CUDA(cudaMemcpyAsync(h->host_ctrl, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  if (h->P.tcm) GMF_CUDA(cudaMemcpyAsync(h->host_abort, h->P.gbar + 2, 4, cudaMemcpyDeviceToHost, st));
   GMF_CUDA(cudaStreamSynchronize(st));
+  if (h->P.tcm && *h->host_abort) {
+    set_error("persistent fit kernel aborted: a grid barrier timed out (CTAs lost co-residency)");
+    return GMF_ERR_STATE;
+  }
   return gmf_status_decode(h->host_ctrl, out);
 }
 
@@ -428,7 +490,7 @@ int gmf_geometry(gmf_handle* h, int64_t* out8) {
   out8[3] = h->P.TC;
   out8[4] = h->P.RS;
   out8[5] = h->NK;
-  out8[6] = grad_smem_bytes(h->desc.dtype, h->NK, h->P.has_w, h->P.Kr, h->P.Kc);
+  out8[6] = grad_smem_bytes(h->desc.dtype, h->NK, h->P.has_w, h->P.Kr, h->P.Kc, h->P.tcm);
   out8[7] = h->P.nstar_max;
   return GMF_OK;
 }
@@ -488,6 +550,7 @@ int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_m
   GMF_CUDA(cudaEventCreate(&b));
   rc = launch_grad(h->P, h->desc.dtype, h->NK, st, row_block, 0, alpha);   // warm
   if (rc) return rc;
+  h->launches += 1 + iters;
   GMF_CUDA(cudaEventRecord(a, st));
   for (int i = 0; i < iters && rc == GMF_OK; ++i)
     rc = launch_grad(h->P, h->desc.dtype, h->NK, st, row_block, 0, alpha);
@@ -517,8 +580,13 @@ int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
   gmf_status s;
   int rc = gmf_status_read(h, &s, stream);
   if (rc) return rc;
+  h->launches += 1;
   return launch_objfull(h->P, h->desc.dtype, s.nb_shape, h->full_part, h->full_ticket, dev_sum,
                         (cudaStream_t)stream);
 }
+
+int gmf_k1_impl(gmf_handle* h) { return h ? (h->P.tcm ? GMF_K1_TENSOR : GMF_K1_CUDA_CORES) : -1; }
+
+int64_t gmf_launch_count(gmf_handle* h) { return h ? h->launches : -1; }
 
 }  // extern "C"

@@ -73,6 +73,7 @@ struct Params {
   double lam_b, lam_g, lam_u, lam_v;
   double nbfloor, nbceil, escale, phi;
   int est_alpha, snap_stride, world;
+  int tcm;             // K1 on the tensor cores (gmf_tc.cuh)
   const double* rho_tab;     // learning_rate(t)        (optim.py:130-134)
   const double* alpt_tab;    // bias_correction(t + 1)  (optim.py:142-148)
   // workspace
@@ -83,6 +84,7 @@ struct Params {
   void* colpart;       // [CT][RS][TC][2 Kc]            T
   double* nbpart;      // [CT * RS][2]
   unsigned int* tickets;   // [CT] col tiles, [CT] grad-global, [CT+1] obj, [CT+2] apply
+  unsigned int* gbar;      // software grid barrier of the tensor-core fit kernel: count, generation, abort
   double* rec;         // rank record: REC_HDR doubles + [jmax][2 Kc] T
   int64_t rec_stride;  // bytes between gathered records
   double* objpart;     // [n_obj_ctas][OBJ_W]

@@ -11,8 +11,10 @@
 //               microseconds long and strictly sequential through V, so
 //               removing per-kernel launch/drain gaps is the first-order win.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
-#include "gmf_kern.cuh"
+#include "gmf_tc.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -21,11 +23,13 @@ namespace gmf {
 template <typename T> struct MinBlocks { static constexpr int v = 2; };
 template <> struct MinBlocks<double> { static constexpr int v = 1; };
 
-template <typename T, int FAM, int NK>
+template <typename T, int FAM, int NK, bool TCM>
 __global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
 k_grad(Params P, long long xb, long long xs, double xalpha) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double scr[kThreads / 32];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t s_bar[2];
   constexpr int TC = Tile<T>::TC;
   const Ctrl* C = P.ctrl;
   long long blk, s;
@@ -40,7 +44,14 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
     alpha = C->nb_shape;
   }
   const int ct = blockIdx.y, rs = blockIdx.x, RS = gridDim.x;
-  grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
+  if constexpr (TCM) {
+    tc::Ctx tcx;
+    tc::ctx_open(tcx, &s_tmem, s_bar);
+    tc::grad_cta<FAM, NK>(P, blk, s, alpha, rs, ct, RS, smem, tcx);
+    tc::ctx_close(tcx);
+  } else {
+    grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
+  }
 
   const int64_t nJ = P.cbp[s + 1] - P.cbp[s];
   const int kk = 2 * P.Kc;
@@ -123,6 +134,47 @@ GMF_D double obj_dev_partial(const Params& P, double alpha, int64_t first, int64
   return s;
 }
 
+// Grid-wide barrier of the tensor-core persistent kernel.  The occupancy
+// calculator (and so cudaLaunchCooperativeKernel) caps kernels that allocate
+// tensor memory at one CTA per SM, so that kernel is launched normally with
+// every CTA co-resident (two per SM: 256 TMEM columns each) and synchronises
+// through this counter/generation barrier.  A residency probe at launch
+// (short timeout) and a long timeout on every barrier turn a lost CTA into an
+// abort flag instead of a hang; the host falls back to one CTA per SM.
+GMF_D unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long timeout_ns) {
+  __shared__ int ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int res = 1;
+    const unsigned int gen = ld_acquire_u32(gb + 1);
+    __threadfence();
+    if (atomicAdd(gb, 1u) == G - 1) {
+      atomicExch(gb, 0u);
+      __threadfence();
+      atomicAdd(gb + 1, 1u);
+    } else {
+      const unsigned long long t0 = gtimer();
+      while (ld_acquire_u32(gb + 1) == gen) {
+        if (ld_acquire_u32(gb + 2)) { res = 0; break; }
+        if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); res = 0; break; }
+      }
+    }
+    __threadfence();
+    ok = res;
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+constexpr unsigned long long kProbeTimeoutNs = 50ull * 1000 * 1000;        // residency probe
+constexpr unsigned long long kBarrierTimeoutNs = 10ull * 1000 * 1000 * 1000;  // hang guard
+
 template <typename T>
 GMF_D T warp_sum(T v) {
   #pragma unroll
@@ -130,16 +182,34 @@ GMF_D T warp_sum(T v) {
   return v;
 }
 
-template <typename T, int FAM, int NK>
+template <typename T, int FAM, int NK, bool TCM>
 __global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
 k_fit(Params P, long long n_steps) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double scr[8 * (kThreads / 32)];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t s_bar[2];
   constexpr int TC = Tile<T>::TC;
-  cg::grid_group grid = cg::this_grid();
   Ctrl C = *P.ctrl;
   if (C.stopped) return;
+  tc::Ctx tcx;
   const int G = gridDim.x;
+  auto gsync = [&](unsigned long long timeout) -> bool {
+    if constexpr (TCM) {
+      return soft_grid_sync(P.gbar, (unsigned int)G, timeout);
+    } else {
+      (void)timeout;
+      cg::this_grid().sync();
+      return true;
+    }
+  };
+  if constexpr (TCM) {
+    tc::ctx_open(tcx, &s_tmem, s_bar);
+    if (!gsync(kProbeTimeoutNs)) {   // not every CTA resident: abort, host falls back
+      tc::ctx_close(tcx);
+      return;
+    }
+  }
   const int ct = blockIdx.x % P.CT, rs = blockIdx.x / P.CT, RS = G / P.CT;
   const int64_t gstride = (int64_t)G * kThreads;
   const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -196,7 +266,10 @@ k_fit(Params P, long long n_steps) {
     }
     if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 1] = gtimer(); }
-    if (run_grad && rs < RS) grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
+    if (run_grad && rs < RS) {
+      if constexpr (TCM) tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx);
+      else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
+    }
     if (prof) { t_b = gtimer(); P.prof[1] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 2] = gtimer(); }
     // Phase-2 inputs that phase 1 does not write are read before the barrier
@@ -214,7 +287,7 @@ k_fit(Params P, long long n_steps) {
       pgb[u] = ldcg_t<T>(tptr<T>(P.gb_row) + o);
       phb[u] = ldcg_t<T>(tptr<T>(P.hb_row) + o);
     }
-    grid.sync();
+    if (!gsync(kBarrierTimeoutNs)) break;
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
     // ------------------------- phase 2 -------------------------
@@ -363,7 +436,7 @@ k_fit(Params P, long long n_steps) {
     if (prof) { t_b = gtimer(); P.prof[3] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 4] = gtimer(); }
     if (D.stop) break;
-    grid.sync();
+    if (!gsync(kBarrierTimeoutNs)) break;
     if (prof) { t_b = gtimer(); P.prof[4] += t_b - t_a; t_a = t_b; P.prof[5] += 1; }
   }
   if (blockIdx.x == 0 && prev_blk >= 0) {
@@ -375,33 +448,40 @@ k_fit(Params P, long long n_steps) {
     block_sum_vec<2>(v, scr);
     if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
   }
+  if constexpr (TCM) tc::ctx_close(tcx);
 }
 
 // ---------------------------------------------------------------------------
 // host side: dispatch over (dtype, family, feature bucket)
 // ---------------------------------------------------------------------------
-template <typename T, int FAM, int NK>
+template <typename T, int FAM, int NK, bool TCM>
 struct Inst {
-  static void* grad() { return (void*)k_grad<T, FAM, NK>; }
-  static void* fit() { return (void*)k_fit<T, FAM, NK>; }
+  static void* grad() { return (void*)k_grad<T, FAM, NK, TCM>; }
+  static void* fit() { return (void*)k_fit<T, FAM, NK, TCM>; }
 };
 
-template <typename T, int FAM>
+template <typename T, int FAM, bool TCM>
 static void* pick(int NK, bool fit) {
   switch (NK) {
-    case 8: return fit ? Inst<T, FAM, 8>::fit() : Inst<T, FAM, 8>::grad();
-    case 12: return fit ? Inst<T, FAM, 12>::fit() : Inst<T, FAM, 12>::grad();
-    case 16: return fit ? Inst<T, FAM, 16>::fit() : Inst<T, FAM, 16>::grad();
-    case 24: return fit ? Inst<T, FAM, 24>::fit() : Inst<T, FAM, 24>::grad();
-    case 32: return fit ? Inst<T, FAM, 32>::fit() : Inst<T, FAM, 32>::grad();
+    case 8: return fit ? Inst<T, FAM, 8, TCM>::fit() : Inst<T, FAM, 8, TCM>::grad();
+    case 12: return fit ? Inst<T, FAM, 12, TCM>::fit() : Inst<T, FAM, 12, TCM>::grad();
+    case 16: return fit ? Inst<T, FAM, 16, TCM>::fit() : Inst<T, FAM, 16, TCM>::grad();
+    case 24: return fit ? Inst<T, FAM, 24, TCM>::fit() : Inst<T, FAM, 24, TCM>::grad();
+    case 32: return fit ? Inst<T, FAM, 32, TCM>::fit() : Inst<T, FAM, 32, TCM>::grad();
     default: return nullptr;
   }
 }
 
-static void* kernel_for(int dtype, int family, int NK, bool fit) {
+// tcm: K1 on the tensor cores (fp32 only; gmf_tc.cuh)
+static void* kernel_for(int dtype, int family, int NK, bool fit, int tcm) {
   const int fam = family == GMF_NEG_BINOMIAL ? 1 : 0;
-  if (dtype == GMF_F64) return fam ? pick<double, 1>(NK, fit) : pick<double, 0>(NK, fit);
-  return fam ? pick<float, 1>(NK, fit) : pick<float, 0>(NK, fit);
+  if (dtype == GMF_F64) return fam ? pick<double, 1, false>(NK, fit) : pick<double, 0, false>(NK, fit);
+  if (tcm) return fam ? pick<float, 1, true>(NK, fit) : pick<float, 0, true>(NK, fit);
+  return fam ? pick<float, 1, false>(NK, fit) : pick<float, 0, false>(NK, fit);
+}
+
+int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA) {
+  return dtype == GMF_F32 && !has_w && Kr <= 16 && Kc <= 16 && KA <= 32;
 }
 
 int grad_bucket(int KA) {
@@ -415,42 +495,77 @@ int grad_bucket(int KA) {
 
 int tile_cols(int dtype) { return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC; }
 
-int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc) {
+int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm) {
+  if (tcm) return tc::smem_layout(NK).total;
   return grad_smem(tile_cols(dtype), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
 }
 
 // opt in to >48 KB dynamic shared memory (outside any graph capture) and
 // report how many k_fit CTAs can be co-resident per SM
-int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int* fit_blocks_per_sm) {
-  void* g = kernel_for(dtype, family, NK, false);
-  void* f = kernel_for(dtype, family, NK, true);
+int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
+                 int* fit_blocks_per_sm) {
+  void* g = kernel_for(dtype, family, NK, false, tcm);
+  void* f = kernel_for(dtype, family, NK, true, tcm);
   if (!g || !f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const int smem = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc);
+  const int smem = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc, tcm);
   GMF_CUDA(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   GMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nb = 0;
   GMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem));
+  if (tcm) {
+    // The occupancy calculator caps kernels that allocate tensor memory at one
+    // CTA per SM; each K1 CTA takes 256 of the 512 TMEM columns, so the SM
+    // holds as many as registers and shared memory allow, up to two.
+    cudaFuncAttributes a;
+    GMF_CUDA(cudaFuncGetAttributes(&a, f));
+    int dev = 0, smem_sm = 0, regs_sm = 0;
+    GMF_CUDA(cudaGetDevice(&dev));
+    GMF_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    GMF_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+    const int by_smem = smem_sm / (int)(smem + a.sharedSizeBytes + 1024);
+    const int by_regs = regs_sm / (((a.numRegs + 7) / 8) * 8 * kThreads);
+    int v = by_smem < by_regs ? by_smem : by_regs;
+    if (v > (int)(512 / tc::kCols)) v = (int)(512 / tc::kCols);
+    if (v > nb) nb = v;
+  }
   *fit_blocks_per_sm = nb;
+  if (getenv("GMF_VERBOSE")) {
+    for (void* k : {g, f}) {
+      cudaFuncAttributes a;
+      cudaFuncGetAttributes(&a, k);
+      int n1 = 0, n2 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k, kThreads, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k, kThreads, 0);
+      fprintf(stderr, "[gmf] %s kernel: regs %d static smem %zu dyn smem %d (max %d) local %zu maxthreads %d -> %d CTAs/SM (%d without dyn smem)\n",
+              k == f ? "fit" : "grad", a.numRegs, a.sharedSizeBytes, smem, a.maxDynamicSharedSizeBytes,
+              a.localSizeBytes, a.maxThreadsPerBlock, n1, n2);
+    }
+  }
   return GMF_OK;
 }
 
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha) {
-  void* f = kernel_for(dtype, P.fam, NK, false);
+  void* f = kernel_for(dtype, P.fam, NK, false, P.tcm);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   dim3 grid(P.RS, P.CT);
-  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc);
+  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm);
   void* args[] = {(void*)&P, (void*)&xb, (void*)&xs, (void*)&xalpha};
   GMF_CUDA(cudaLaunchKernel(f, grid, dim3(kThreads), args, smem, st));
   return GMF_OK;
 }
 
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st) {
-  void* f = kernel_for(dtype, P.fam, NK, true);
+  void* f = kernel_for(dtype, P.fam, NK, true, P.tcm);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc);
+  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm);
   void* args[] = {(void*)&P, (void*)&n_steps};
-  GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+  if (P.tcm) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
+    GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 4 * sizeof(unsigned int), st));
+    GMF_CUDA(cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+  } else {
+    GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+  }
   return GMF_OK;
 }
 

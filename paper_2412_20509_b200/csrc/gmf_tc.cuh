@@ -1,0 +1,586 @@
+// K1 on the 5th-generation tensor cores (fp32 path): tcgen05.mma with
+// operands in shared memory, accumulators in TMEM.
+//
+// Same contract as grad_cta (gmf_kern.cuh): one CTA owns column tile `ct`
+// (128 columns of block J) and a balanced contiguous row range of block I,
+// and writes rowpart / colpart / nbpart identically.  Per 32-row chunk:
+//
+//   GEMM1  eta[128 x 128]   = A1 . B1^T      rows x columns, K = p+q+d
+//          (A1 = [x|u|gamma] of the 32 rows, replicated into the four TMEM
+//          lane quarters so all 8 warps read eta; B1 = [b|v|z] * log2 e)
+//   elementwise (CUDA cores, thread = row, 16 columns):
+//          mu = 2^eta, dotD / ddotD (NB or Poisson, log link), NB moments,
+//          written as the stacked bf16 tile P = [dd_hi; hh_hi; dd_lo; hh_lo]
+//   GEMM2  D2[128 x 64]    = P . R          row side, K = tile columns
+//          (R = [Rd_hi | Rd_lo | Rd2_hi | Rd2_lo], Rd = [z_j | v_j])
+//   GEMM3  D3[128 x 64]   += P^T . B3        column side, K = chunk rows
+//          (P read MN-major, B3 = [Ac_hi | Ac_lo | Ac2_hi | Ac2_lo], Ac = [x|u])
+//
+// fp32 accuracy from bf16 operands: every operand is split x = hi + lo
+// (hi = bf16(x), lo = bf16(x - hi)); GEMM1 sums hi.hi + hi.lo + lo.hi,
+// GEMM2/3 all four products, accumulation in fp32 (TMEM).  Relative error
+// per product ~2^-17, inside the fp32 north-star tolerance (1e-4).
+//
+// Shared-memory operands use the canonical no-swizzle core-matrix layout
+// (8 rows x 16 bytes): K-major tiles for every operand, and the same P tile
+// read MN-major by GEMM3 (verified layouts: tools/umma_test.cu).
+// TMEM: 256 columns per CTA (two CTAs per SM): eta [0,128), D2 [128,192),
+// D3 [192,256).  One thread issues the MMAs; completion is tracked with
+// tcgen05.commit -> mbarrier.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "gmf_kern.cuh"
+
+namespace gmf {
+namespace tc {
+
+constexpr int TCC = 128;              // tile columns (GEMM1 N, GEMM3 M)
+constexpr int TRC = 32;               // rows per chunk (x4 replicas = UMMA M 128)
+constexpr int YP = 132;               // Y tile pitch (int32): conflict-free 16-byte row reads
+constexpr uint32_t kCols = 256;       // TMEM columns per CTA
+constexpr uint32_t T_ETA = 0, T_D2 = 128, T_D3 = 192;
+constexpr uint32_t SBO_P = 2048;      // P / R: 16 column cores x 128 B
+constexpr uint32_t SBO_B3 = 512;      // B3: 4 row cores x 128 B
+
+struct Smem {
+  int64_t P, R, B1h, B1l, A1h, A1l, B3, Y, stage, araw, off, rp, total;
+  int nka;
+};
+
+GMF_HD Smem smem_layout(int NK) {
+  Smem s;
+  int64_t o = 0;
+  auto al = [](int64_t v) { return (v + 127) & ~int64_t(127); };
+  s.nka = NK <= 16 ? 16 : 32;
+  s.P = o; o = al(o + 128 * TCC * 2);
+  s.R = o; o = al(o + 64 * TCC * 2);
+  s.B1h = o; o = al(o + TCC * s.nka * 2);
+  s.B1l = o; o = al(o + TCC * s.nka * 2);
+  s.A1h = o; o = al(o + 128 * s.nka * 2);
+  s.A1l = o; o = al(o + 128 * s.nka * 2);
+  s.B3 = o; o = al(o + 64 * TRC * 2);
+  s.Y = o; o = al(o + TRC * YP * 4);
+  s.stage = o; o = al(o + (int64_t)kStageCap * 8);   // == TRC * TCC * 4 (dense)
+  s.araw = o; o = al(o + TRC * NK * 4);
+  s.off = o; o = al(o + TRC * 4);
+  s.rp = o; o = al(o + (kRpMax + 1) * 8);
+  s.total = o;
+  return s;
+}
+
+// byte offset of bf16 element (mn, k) in a K-major no-swizzle tile:
+// core matrices of 8 (mn) rows x 8 k-elements, next k core +128 B,
+// next 8-row group +sbo
+GMF_HD uint32_t kofs(int mn, int k, uint32_t sbo) {
+  return (uint32_t)(mn >> 3) * sbo + (uint32_t)(k >> 3) * 128u + (uint32_t)(mn & 7) * 16u +
+         (uint32_t)(k & 7) * 2u;
+}
+
+GMF_D uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// shared-memory matrix descriptor (no swizzle, Blackwell version bit)
+GMF_D uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, M x N, operand majors
+constexpr uint32_t idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+GMF_D void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+
+GMF_D void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_addr(bar))
+               : "memory");
+}
+
+GMF_D void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+
+GMF_D void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+GMF_D void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+GMF_D void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+GMF_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+GMF_D void tmem_alloc(uint32_t* dst) {   // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(dst)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+GMF_D void tmem_dealloc(uint32_t base) {   // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kCols)
+               : "memory");
+}
+
+// 32 lanes x 16 consecutive TMEM columns -> 16 registers per thread; the
+// wait carries the registers so no use is scheduled before the data lands
+GMF_D void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+
+// per-CTA tensor state, persistent across calls (mbarrier phases)
+struct Ctx {
+  uint32_t tmem;
+  uint64_t* bar;   // [0] GEMM1 done, [1] GEMM2+3 done
+  uint32_t n1, n23;
+};
+
+// CTA prologue / epilogue (all threads)
+GMF_D void ctx_open(Ctx& X, uint32_t* s_tmem, uint64_t* s_bar) {
+  if (threadIdx.x < 32) tmem_alloc(s_tmem);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0]);
+    mbar_init(&s_bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  X.tmem = *s_tmem;
+  X.bar = s_bar;
+  X.n1 = 0;
+  X.n23 = 0;
+}
+GMF_D void ctx_close(const Ctx& X) {
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (threadIdx.x < 32) tmem_dealloc(X.tmem);
+}
+
+GMF_D void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// 16 consecutive fp32 values -> bf16 hi at stacked row m_hi and lo at m_lo
+// of the P tile, columns c0..c0+15 (two 16-byte core rows each)
+GMF_D void put_split16(const float (&x)[16], unsigned char* Pb, int m_hi, int m_lo, int c0) {
+  uint32_t hi[8], lo[8];
+  #pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float a = x[2 * u], b = x[2 * u + 1];
+    uint32_t h, l;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    const float ra = a - __uint_as_float(h << 16);
+    const float rb = b - __uint_as_float(h & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(rb), "f"(ra));
+    hi[u] = h;
+    lo[u] = l;
+  }
+  *reinterpret_cast<uint4*>(Pb + kofs(m_hi, c0, SBO_P)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(Pb + kofs(m_hi, c0 + 8, SBO_P)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+  *reinterpret_cast<uint4*>(Pb + kofs(m_lo, c0, SBO_P)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  *reinterpret_cast<uint4*>(Pb + kofs(m_lo, c0 + 8, SBO_P)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+}
+
+template <int FAM, int NK>
+GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct, int RS,
+                    unsigned char* smem, Ctx& X) {
+  using T = float;
+  __shared__ double red_scr[kThreads / 32];
+  __shared__ int stage_n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int qd = warp & 3, hf = warp >> 2;
+  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
+  const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
+  const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
+  const int64_t rlo = nI * rs / RS, rhi = nI * (rs + 1) / RS;
+  const int64_t nrows = rhi - rlo;
+  const bool csr = P.yfmt != GMF_Y_DENSE_I32;
+  const bool rp_staged = csr && nrows <= kRpMax;
+  const int64_t cbase = (int64_t)ct * TCC;
+  const int64_t ncv64 = nJ - cbase;
+  const int ncv = ncv64 < 0 ? 0 : (ncv64 > TCC ? TCC : (int)ncv64);   // valid tile columns
+  const Smem L = smem_layout(NK);
+  const int nka = L.nka;
+  const uint32_t sbo1 = (uint32_t)(nka / 8) * 128u;
+  const uint32_t sb = smem_addr(smem);
+
+  unsigned char* Pb = smem + L.P;
+  unsigned char* Rb = smem + L.R;
+  unsigned char* B1h = smem + L.B1h;
+  unsigned char* B1l = smem + L.B1l;
+  unsigned char* A1h = smem + L.A1h;
+  unsigned char* A1l = smem + L.A1l;
+  unsigned char* B3b = smem + L.B3;
+  int32_t* Y = reinterpret_cast<int32_t*>(smem + L.Y);
+  unsigned char* st = smem + L.stage;
+  T* araw = reinterpret_cast<T*>(smem + L.araw);
+  T* off_s = reinterpret_cast<T*>(smem + L.off);
+  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
+
+  const T* th_row = tptr<T>(P.th_row);
+  const T* th_col = tptr<T>(P.th_col);
+  const T* xg = tptr<T>(P.x);
+  const T* zg = tptr<T>(P.z);
+  const T* offg = tptr<T>(P.off);
+  const T pre = 1.4426950408889634f;
+  T* colpart = tptr<T>(P.colpart);
+  const int64_t cpb = ((int64_t)ct * RS + rs) * TCC * (2 * Kc);
+
+  __syncthreads();   // shared memory reuse across calls (persistent kernel)
+  if (nrows <= 0) {   // nothing to do: zero column partials and NB sums
+    for (int e = tid; e < TCC * 2 * Kc; e += kThreads) colpart[cpb + e] = T(0);
+    if (tid == 0) {
+      P.nbpart[2 * ((int64_t)ct * RS + rs)] = 0.0;
+      P.nbpart[2 * ((int64_t)ct * RS + rs) + 1] = 0.0;
+    }
+    return;
+  }
+
+  // ---- column operands of the tile (once per call) ----
+  // B1 = [b | v | z] * log2(e), split hi/lo; K-major (N = columns)
+  for (int e = tid; e < TCC * nka; e += kThreads) {
+    const int c = e / nka, k = e % nka;
+    T v = T(0);
+    if (c < ncv && k < KA) {
+      const int64_t pos = cbase + c;
+      const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
+      v = (k < Kc ? th_col[j * Kc + k] : zg[j * q + (k - Kc)]) * pre;
+    }
+    __nv_bfloat16 h, l;
+    split_bf16(v, h, l);
+    const uint32_t o = kofs(c, k, sbo1);
+    *reinterpret_cast<__nv_bfloat16*>(B1h + o) = h;
+    *reinterpret_cast<__nv_bfloat16*>(B1l + o) = l;
+  }
+  // R = [Rd_hi | Rd_lo | Rd2_hi | Rd2_lo], Rd = [z_j | v_j]; K-major (N = 64 features)
+  for (int e = tid; e < TCC * 16; e += kThreads) {
+    const int c = e >> 4, k = e & 15;
+    T v = T(0);
+    if (c < ncv && k < Kr) {
+      const int64_t pos = cbase + c;
+      const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
+      v = k < q ? zg[j * q + k] : th_col[j * Kc + p + (k - q)];
+    }
+    __nv_bfloat16 h, l, h2, l2;
+    split_bf16(v, h, l);
+    split_bf16(v * v, h2, l2);
+    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(k, c, SBO_P)) = h;
+    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(16 + k, c, SBO_P)) = l;
+    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(32 + k, c, SBO_P)) = h2;
+    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(48 + k, c, SBO_P)) = l2;
+  }
+  if (rp_staged)
+    for (int64_t e = tid; e <= nrows; e += kThreads) rp_s[e] = P.rp[r0 + rlo + e];
+  for (int e = tid; e < TRC * YP; e += kThreads) Y[e] = 0;
+  __syncthreads();
+
+  // ---- asynchronous staging of one chunk (row features, offsets, Y) ----
+  auto issue = [&](int64_t rowbase) {
+    const int rows = (int)((rhi - rowbase) < TRC ? (rhi - rowbase) : TRC);
+    const int64_t i0 = r0 + rowbase;
+    for (int e = tid; e < TRC * NK; e += kThreads) {
+      const int rr = e / NK, k = e % NK;
+      const T* src = xg;
+      bool ok = false;
+      if (rr < rows) {
+        const int64_t i = i0 + rr;
+        if (k < p) { src = xg + i * p + k; ok = true; }
+        else if (k < p + d) { src = th_row + i * Kr + q + (k - p); ok = true; }
+        else if (k < KA) { src = th_row + i * Kr + (k - p - d); ok = true; }
+      }
+      cp_async<4>(araw + e, src, ok);
+    }
+    if (tid < TRC) {
+      const bool ok = tid < rows && P.has_off;
+      cp_async<4>(off_s + tid, ok ? offg + i0 + tid : offg, ok);
+    }
+    if (!csr) {
+      int32_t* y_b = reinterpret_cast<int32_t*>(st);
+      for (int e = tid; e < TRC * TCC; e += kThreads) {
+        const int rr = e / TCC, cc = e % TCC;
+        const bool ok = rr < rows && cc < ncv;
+        const int64_t pos = cbase + cc;
+        const int64_t jj = ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
+        cp_async<4>(y_b + e, ok ? P.y + (i0 + rr) * P.m + jj : P.y, ok);
+      }
+    } else if (rp_staged) {
+      const int64_t lo = rp_s[rowbase - rlo], hi = rp_s[rowbase - rlo + rows];
+      const int64_t nnz = hi - lo;
+      if (nnz <= kStageCap) {
+        int32_t* col_b = reinterpret_cast<int32_t*>(st);
+        int32_t* val_b = col_b + kStageCap;
+        for (int64_t e = tid; e < nnz; e += kThreads) {
+          cp_async<4>(col_b + e, P.ci + lo + e, true);
+          cp_async<4>(val_b + e, P.cv + lo + e, true);
+        }
+        if (tid == 0) stage_n = (int)nnz;
+      } else if (tid == 0) {
+        stage_n = -1;
+      }
+    } else if (tid == 0) {
+      stage_n = -1;
+    }
+    cp_async_commit();
+  };
+
+  const T rphi = T(1.0 / P.phi);
+  const T ralpha = T(1.0 / alpha);
+  const T tphi = T(P.phi);
+  const T tra = tphi * ralpha;
+  const uint32_t tm = X.tmem;
+  constexpr uint32_t ID1 = idesc(128, 128, 0, 0);
+  constexpr uint32_t ID2 = idesc(128, 64, 0, 0);
+  constexpr uint32_t ID3 = idesc(128, 32, 1, 0);
+  const int c0 = 32 * qd + 16 * hf;                 // this thread's first tile column
+  const int vcols = ncv - c0 < 0 ? 0 : (ncv - c0 > 16 ? 16 : ncv - c0);
+  const uint32_t lane_base = (uint32_t)(32 * qd) << 16;
+  double nb_num = 0.0, nb_den = 0.0;
+  T* rowpart = tptr<T>(P.rowpart);
+  const int rkk = 2 * Kr;
+
+  // row side of the previous chunk: wait GEMM2/3, read D2 (warps 0-3:
+  // quarter 0 = dd_hi rows, 1 = hh_hi, 2 = dd_lo, 3 = hh_lo), combine the
+  // hi and lo halves through shared memory, write rowpart
+  auto readout_d2 = [&](int64_t rowbase, int rows) {
+    mbar_wait(&X.bar[1], X.n23 & 1u);
+    ++X.n23;
+    fence_after();
+    float* scr = reinterpret_cast<float*>(st);   // [2][32][17]
+    float v[16];
+    if (hf == 0) {
+      uint32_t a[16], b[16];
+      const uint32_t col = tm + lane_base + T_D2 + ((qd & 1) ? 32u : 0u);
+      tmem_ld16(col, a);
+      tmem_ld16(col + 16, b);
+      #pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
+      if (qd >= 2) {
+        #pragma unroll
+        for (int k = 0; k < 16; ++k) scr[((qd - 2) * 32 + lane) * 17 + k] = v[k];
+      }
+    }
+    fence_before();
+    __syncthreads();
+    if (hf == 0 && qd < 2 && lane < rows) {
+      T* outp = rowpart + ((int64_t)ct * P.nstar_max + rowbase + lane) * rkk + (qd == 0 ? 0 : Kr);
+      #pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < Kr) outp[k] = v[k] + scr[(qd * 32 + lane) * 17 + k];
+    }
+  };
+
+  issue(rlo);
+  int64_t prev_rowbase = -1;
+  int prev_rows = 0;
+  bool first3 = true;
+  for (int64_t rowbase = rlo; rowbase < rhi; rowbase += TRC) {
+    const int rows = (int)((rhi - rowbase) < TRC ? (rhi - rowbase) : TRC);
+    const int64_t i0 = r0 + rowbase;
+    cp_async_wait0();
+    __syncthreads();   // chunk staged; previous elementwise done with Y
+    // ---- Y tile ----
+    if (!csr) {
+      const int32_t* y_b = reinterpret_cast<const int32_t*>(st);
+      for (int e = tid; e < TRC * TCC; e += kThreads) Y[(e / TCC) * YP + (e % TCC)] = y_b[e];
+    } else {
+      const int n_st = stage_n;
+      if (n_st >= 0) {
+        const int32_t* col_b = reinterpret_cast<const int32_t*>(st);
+        const int32_t* val_b = col_b + kStageCap;
+        const int64_t* rpc = rp_s + (rowbase - rlo);
+        const int lo = (int)rpc[0];
+        for (int rr = warp; rr < rows; rr += kThreads / 32) {
+          const int a = (int)rpc[rr] - lo, bnd = (int)rpc[rr + 1] - lo;
+          for (int e = a + lane; e < bnd; e += 32) {
+            const int col = col_b[e];
+            const int pp = P.col_identity ? col : ((P.cbof[col] == s) ? P.cpos[col] : -1);
+            const int cl = pp - (int)cbase;
+            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = val_b[e];
+          }
+        }
+      } else {
+        for (int rr = warp; rr < rows; rr += kThreads / 32) {
+          const int64_t i = i0 + rr;
+          for (int64_t k = P.rp[i] + lane; k < P.rp[i + 1]; k += 32) {
+            const int col = P.ci[k];
+            const int64_t pp = P.col_identity ? col : ((P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1);
+            const int64_t cl = pp - cbase;
+            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = P.cv[k];
+          }
+        }
+      }
+    }
+    // ---- A1: [x | u | gamma] of the chunk rows, hi/lo, four replicas ----
+    for (int e = tid; e < TRC * nka; e += kThreads) {
+      const int rr = e / nka, k = e % nka;
+      const T v = (rr < rows && k < KA) ? araw[rr * NK + k] : T(0);
+      __nv_bfloat16 h, l;
+      split_bf16(v, h, l);
+      #pragma unroll
+      for (int rep = 0; rep < 4; ++rep) {
+        const uint32_t o = kofs(32 * rep + rr, k, sbo1);
+        *reinterpret_cast<__nv_bfloat16*>(A1h + o) = h;
+        *reinterpret_cast<__nv_bfloat16*>(A1l + o) = l;
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    // ---- GEMM1: eta = A1 . B1^T (hi.hi + hi.lo + lo.hi) ----
+    if (tid == 0) {
+      fence_after();
+      for (int kt = 0; kt < nka / 16; ++kt) {
+        const uint32_t ko = (uint32_t)kt * 256u;
+        const uint64_t ah = sdesc(sb + (uint32_t)L.A1h + ko, 128, sbo1);
+        const uint64_t al = sdesc(sb + (uint32_t)L.A1l + ko, 128, sbo1);
+        const uint64_t bh = sdesc(sb + (uint32_t)L.B1h + ko, 128, sbo1);
+        const uint64_t bl = sdesc(sb + (uint32_t)L.B1l + ko, 128, sbo1);
+        umma(tm + T_ETA, ah, bh, ID1, kt > 0 ? 1u : 0u);
+        umma(tm + T_ETA, ah, bl, ID1, 1u);
+        umma(tm + T_ETA, al, bh, ID1, 1u);
+      }
+      umma_commit(&X.bar[0]);
+    }
+    // ---- previous chunk's row side (frees P, D2 and B3) ----
+    if (prev_rowbase >= 0) readout_d2(prev_rowbase, prev_rows);
+    // ---- B3: [Ac_hi | Ac_lo | Ac2_hi | Ac2_lo] x chunk rows, K-major ----
+    for (int e = tid; e < TRC * 16; e += kThreads) {
+      const int rr = e >> 4, k = e & 15;
+      const T v = (rr < rows && k < Kc) ? araw[rr * NK + k] : T(0);
+      __nv_bfloat16 h, l, h2, l2;
+      split_bf16(v, h, l);
+      split_bf16(v * v, h2, l2);
+      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(k, rr, SBO_B3)) = h;
+      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(16 + k, rr, SBO_B3)) = l;
+      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(32 + k, rr, SBO_B3)) = h2;
+      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(48 + k, rr, SBO_B3)) = l2;
+    }
+    const T offr = (lane < rows && P.has_off) ? off_s[lane] * pre : T(0);
+    __syncthreads();   // staging buffers consumed
+    if (rowbase + TRC < rhi) issue(rowbase + TRC);
+
+    // ---- elementwise: thread = chunk row `lane`, columns c0..c0+15 ----
+    mbar_wait(&X.bar[0], X.n1 & 1u);
+    ++X.n1;
+    fence_after();
+    uint32_t ev[16];
+    tmem_ld16(tm + lane_base + T_ETA + (uint32_t)c0, ev);
+    int4* yrow = reinterpret_cast<int4*>(Y + lane * YP + c0);
+    int yv[16];
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int4 t4 = yrow[u];
+      yv[4 * u] = t4.x; yv[4 * u + 1] = t4.y; yv[4 * u + 2] = t4.z; yv[4 * u + 3] = t4.w;
+    }
+    const bool row_ok = lane < rows;
+    float dd[16], hh[16];
+    float cn = 0.f, cdn = 0.f;
+    #pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float w = (row_ok && i < vcols) ? 1.f : 0.f;
+      const float mu = exp_pre(__uint_as_float(ev[i]) + offr);
+      const float r = (float)yv[i] - mu;
+      if (FAM == 0) {
+        const float ws = w * rphi;
+        dd[i] = -ws * r;
+        hh[i] = ws * mu;
+      } else {
+        const float inv = w * rcp_fast(fmaf(mu, tra, tphi));
+        dd[i] = -r * inv;
+        hh[i] = mu * inv;
+        cn = fmaf(w * mu, mu, cn);
+        cdn = fmaf(w, fmaf(r, r, -mu), cdn);
+      }
+    }
+    nb_num += (double)cn;
+    nb_den += (double)cdn;
+    put_split16(dd, Pb, lane, 64 + lane, c0);
+    put_split16(hh, Pb, 32 + lane, 96 + lane, c0);
+    if (csr) {
+      const int4 z4 = make_int4(0, 0, 0, 0);
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) yrow[u] = z4;
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    // ---- GEMM2 (row side) and GEMM3 (column side) ----
+    if (tid == 0) {
+      fence_after();
+      #pragma unroll
+      for (int kt = 0; kt < TCC / 16; ++kt) {
+        const uint32_t ko = (uint32_t)kt * 256u;
+        umma(tm + T_D2, sdesc(sb + (uint32_t)L.P + ko, 128, SBO_P),
+             sdesc(sb + (uint32_t)L.R + ko, 128, SBO_P), ID2, kt > 0 ? 1u : 0u);
+      }
+      // P^T (MN-major: column chunks +128 B, 8-row K groups +2048 B) . B3
+      const uint32_t ao[4] = {0u, 4096u, 16384u, 20480u};   // stacked rows 0,16 (hi) 64,80 (lo)
+      const uint32_t bo[4] = {0u, 256u, 0u, 256u};          // chunk rows 0, 16
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t acc = (first3 && u == 0) ? 0u : 1u;
+        umma(tm + T_D3, sdesc(sb + (uint32_t)L.P + ao[u], 2048, 128),
+             sdesc(sb + (uint32_t)L.B3 + bo[u], 128, SBO_B3), ID3, acc);
+        umma(tm + T_D3 + 32, sdesc(sb + (uint32_t)L.P + ao[u] + 8192u, 2048, 128),
+             sdesc(sb + (uint32_t)L.B3 + 4 * SBO_B3 + bo[u], 128, SBO_B3), ID3, acc);
+      }
+      umma_commit(&X.bar[1]);
+    }
+    first3 = false;
+    prev_rowbase = rowbase;   // block-relative row index of the chunk
+    prev_rows = rows;
+  }
+  cp_async_wait0();
+  // ---- drain: last chunk's row side, then the column side ----
+  readout_d2(prev_rowbase, prev_rows);
+  {
+    fence_after();
+    uint32_t a[16], b[16];
+    const uint32_t col = tm + lane_base + T_D3 + 32u * (uint32_t)hf;
+    tmem_ld16(col, a);
+    tmem_ld16(col + 16, b);
+    const int c = 32 * qd + lane;
+    T* outp = colpart + cpb + (int64_t)c * (2 * Kc) + (hf ? Kc : 0);
+    #pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < Kc) outp[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
+  }
+  fence_before();
+  const double bn = block_sum<kThreads>(nb_num, red_scr);
+  const double bd = block_sum<kThreads>(nb_den, red_scr);
+  if (tid == 0) {
+    P.nbpart[2 * ((int64_t)ct * RS + rs)] = bn;
+    P.nbpart[2 * ((int64_t)ct * RS + rs) + 1] = bd;
+  }
+}
+
+}  // namespace tc
+}  // namespace gmf

@@ -137,7 +137,7 @@ class DeviceFit:
 
     def __init__(self, data, covs, fam, lnk, penalty, cfg, state: FactorizationState, *,
                  schedule: Schedule, offset=None, dtype="f64", device=None, world=1, rank=0,
-                 est_alpha=False):
+                 est_alpha=False, k1_impl="auto"):
         import torch
         _lib.require_cuda()
         lib = _lib.lib()
@@ -150,6 +150,8 @@ class DeviceFit:
                                         "(fully observed responses only)")
         if dtype not in ("f32", "f64"):
             raise ConfigError(f"dtype must be 'f32' or 'f64', got {dtype!r}")
+        if k1_impl not in _lib.K1_IMPL_CODES:
+            raise ConfigError(f"k1_impl must be one of {sorted(_lib.K1_IMPL_CODES)}, got {k1_impl!r}")
         self.torch = torch
         dev_index = torch.cuda.current_device() if device is None else int(
             str(device).split(":")[-1] if isinstance(device, str) else device)
@@ -236,7 +238,8 @@ class DeviceFit:
             lam_b=penalty.lam_b, lam_gamma=penalty.lam_gamma, lam_u=penalty.lam_u,
             lam_v=penalty.lam_v, nb_floor=1e-4, nb_ceiling=1e8, phi=float(state.phi),
             eval_scale=float(schedule.eval_scale), max_epochs=cfg.max_epochs,
-            est_alpha=int(bool(est_alpha)), snapshot_stride=4)
+            est_alpha=int(bool(est_alpha)), snapshot_stride=4,
+            k1_impl=_lib.K1_IMPL_CODES[k1_impl], reserved=0)
         P = _lib.ptr
         self.bufs = _lib.GmfBuffers(
             y_dense=P(self.y_dense), csr_ptr=P(self.csr_ptr), csr_col=P(self.csr_col),
@@ -258,6 +261,11 @@ class DeviceFit:
         self.h = h
         self.lib = lib
         self.rec_bytes = int(lib.gmf_record_bytes(h))
+        self.k1_impl = _lib.K1_IMPL_NAMES[int(lib.gmf_k1_impl(h))]
+
+    def launch_count(self):
+        """Kernels this handle has launched so far (C-ABI gmf_launch_count)."""
+        return int(self.lib.gmf_launch_count(self.h))
 
     # ------------------------------------------------------------------
     def stream(self):

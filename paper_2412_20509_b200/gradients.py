@@ -56,7 +56,8 @@ def _complement(idx, size):
 
 
 def minibatch_gradients(state, data, covs, fam, lnk, penalty, mb, y_block=None, *,
-                        offset=None, dtype="f64", device=None, return_nb_sums=False):
+                        offset=None, dtype="f64", device=None, return_nb_sums=False,
+                        k1_impl="auto"):
     """Unbiased block estimates of the full gradients (gradients.py:116-132),
     computed by the fused K1 kernel through gmf_minibatch_grad."""
     from .engine import DeviceFit, Schedule
@@ -72,7 +73,7 @@ def minibatch_gradients(state, data, covs, fam, lnk, penalty, mb, y_block=None, 
     cols = [J] + ([_complement(J, m)] if J.size < m else [])
     sched = Schedule(n, m, SgdConfig(max_epochs=1), row_blocks=rows, col_blocks=cols, n_steps=0)
     fit = DeviceFit(data, covs, fam, lnk, penalty, SgdConfig(max_epochs=1), state,
-                    schedule=sched, offset=offset, dtype=dtype, device=device)
+                    schedule=sched, offset=offset, dtype=dtype, device=device, k1_impl=k1_impl)
     try:
         alpha = getattr(fam, "nb_shape", 1.0)
         g_row, h_row, g_col, h_col, nb = fit.minibatch_grad(0, 0, alpha)

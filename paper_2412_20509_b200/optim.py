@@ -183,14 +183,16 @@ def _gather_rows(fit: DeviceFit, tensor, group, mode):
 
 def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, rank=None,
              identify_mode="B1", dispersion="auto", callback=None, offset=None, dtype="f64",
-             device=None, process_group=None, exchange="device"):
+             device=None, process_group=None, exchange="device", k1_impl="auto"):
     """Block-wise adaptive stochastic quasi-Newton descent on the GPU.
 
     Drop-in for gmfkit.fit_asgd (optim.py:383-489); returns ``(state,
     FitReport)`` with the state projected onto the identifiability constraints
     (``identify_mode=None`` skips it).  Extensions: ``offset`` (per-row term
     in eta), ``dtype`` ('f64' | 'f32'), ``device``, and ``process_group``
-    (rows of every block split across the group's ranks, one GPU each).
+    (rows of every block split across the group's ranks, one GPU each), and
+    ``k1_impl`` ('auto' | 'tensor' | 'cuda_cores'): the fused-gradient kernel
+    (tensor cores for fp32 when eligible).
     """
     started = time.perf_counter()
     if init_state is None:
@@ -211,7 +213,7 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
     sched = Schedule(n, m, cfg, mask=mask)
     fit = DeviceFit(data, covs, fam, lnk, penalty, cfg, init_state, schedule=sched,
                     offset=offset, dtype=dtype, device=device, world=world, rank=my_rank,
-                    est_alpha=est_alpha)
+                    est_alpha=est_alpha, k1_impl=k1_impl)
     try:
         fit.reset()
         _drive(fit, callback, process_group, exchange)

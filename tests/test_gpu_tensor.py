@@ -1,0 +1,152 @@
+"""Tensor-core K1 (tcgen05, bf16-split operands, fp32 accumulation in TMEM)
+against the CPU oracle and against the CUDA-core K1.
+
+Shapes cover the tensor path's edges: partial 128-column tiles, row ranges
+that are not multiples of the 32-row chunk, column blocks that are not the
+identity (mb_cols < m), offsets, Poisson and NB, K = p+q+d above 16 (two
+GEMM1 k-steps) and the largest row/column feature widths (q+d = p+d = 16).
+Tolerance: the north star's fp32 gradient bound, 1e-4 normwise."""
+import numpy as np
+import pytest
+
+from conftest import normwise
+from oracle import asgd_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+gk = pytest.importorskip("paper_2412_20509_b200")
+
+TOL = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _problem(seed, n, m, d, p, q, family, offset):
+    rng = np.random.default_rng(seed)
+    x = np.hstack([np.ones((n, 1)), rng.normal(size=(n, p - 1))]) if p else np.zeros((n, 0))
+    z = np.hstack([np.ones((m, 1)), rng.normal(size=(m, q - 1))]) if q else np.zeros((m, 0))
+    b = rng.normal(0.5, 0.3, size=(m, p))
+    gamma = rng.normal(0, 0.2, size=(n, q))
+    u = rng.normal(0, 0.4, size=(n, d))
+    v = rng.normal(0, 0.4, size=(m, d))
+    off = rng.normal(0, 0.5, size=n) if offset else None
+    eta = x @ b.T + gamma @ z.T + u @ v.T + (off[:, None] if offset else 0.0)
+    mu = np.exp(np.clip(eta, -10, 6))
+    if family == "nb":
+        lam = rng.gamma(2.0, mu / 2.0)
+        y = rng.poisson(lam)
+    else:
+        y = rng.poisson(mu)
+    noisy = lambda a: a + rng.normal(0, 0.05, size=a.shape)
+    st = gk.FactorizationState(noisy(b), noisy(gamma), noisy(u), noisy(v), 1.0, 2.0)
+    return y.astype(float), x, z, off, st
+
+
+CASES = [
+    # (n, m, d, p, q, family, offset, mb_rows, mb_cols)
+    (300, 200, 5, 1, 1, "poisson", False, 137, 200),     # partial 2nd tile, ragged chunks
+    (517, 300, 10, 1, 0, "nb", True, 517, 300),          # c4-like features, offset, all rows
+    (400, 260, 12, 4, 4, "nb", False, 150, 130),         # KA = 20: two GEMM1 k-steps; column blocks
+    (150, 128, 15, 1, 1, "nb", True, 97, 128),           # Kr = Kc = 16 (widest), one full tile
+    (64, 40, 3, 2, 0, "poisson", True, 33, 17),          # tiny: one partial tile, mostly-empty chunks
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}m{c[1]}d{c[2]}p{c[3]}q{c[4]}{c[5]}")
+@pytest.mark.parametrize("impl", ["tensor", "cuda_cores"])
+def test_k1_block_gradient_matches_oracle(case, impl):
+    n, m, d, p, q, family, offset, mbr, mbc = case
+    y, x, z, off, st = _problem(7, n, m, d, p, q, family, offset)
+    rng = np.random.default_rng(11)
+    I = np.sort(rng.choice(n, size=mbr, replace=False))
+    J = np.sort(rng.choice(m, size=mbc, replace=False))
+    data = gk.ResponseMatrix(y)
+    covs = gk.CovariateSet(x=x if p else None, z=z if q else None, n=n, m=m)
+    lam = (0.3, 0.2, 1.0, 0.7)
+    pen = gk.PenaltyConfig(lam=1.0, blocks=lam)
+    fam = gk.NegBinomial(2.0) if family == "nb" else gk.Poisson()
+    gp, nbs = gk.minibatch_gradients(st, data, covs, fam, gk.Log(), pen, gk.Minibatch(I, J),
+                                     offset=off, dtype="f32", k1_impl=impl, return_nb_sums=True)
+    pb = orc.OProblem(y, x, z, offset=off)
+    ost = orc.OState(st.b, st.gamma, st.u, st.v, 1.0, 2.0)
+    fcode = orc.NEG_BINOMIAL if family == "nb" else orc.POISSON
+    ref = orc.minibatch_gradients(ost, pb, I, J, fcode, orc.LOG, lam)
+    errs = {k: normwise(mine, r) for k, mine, r in (
+        ("g_row", gp.g_rowside, ref.g_row), ("h_row", gp.h_rowside, ref.h_row),
+        ("g_col", gp.g_colside, ref.g_col), ("h_col", gp.h_colside, ref.h_col))}
+    assert max(errs.values()) < TOL, errs
+    if family == "nb":
+        _, w, mu, _, _ = orc.block_derivs(ost, pb, I, J, fcode, orc.LOG)
+        num, den = orc.nb_moment_sums(y[I][:, J], mu, w)
+        assert abs(nbs[0] - num) < TOL * abs(num) and abs(nbs[1] - den) < TOL * (abs(num) + abs(den))
+
+
+@pytest.mark.parametrize("case", CASES[:3], ids=lambda c: f"n{c[0]}m{c[1]}")
+def test_k1_tensor_close_to_cuda_cores(case):
+    n, m, d, p, q, family, offset, mbr, mbc = case
+    y, x, z, off, st = _problem(3, n, m, d, p, q, family, offset)
+    I = np.arange(0, n, 2)
+    J = np.arange(m)
+    data = gk.ResponseMatrix(y)
+    covs = gk.CovariateSet(x=x if p else None, z=z if q else None, n=n, m=m)
+    fam = gk.NegBinomial(2.0) if family == "nb" else gk.Poisson()
+    out = {}
+    for impl in ("tensor", "cuda_cores"):
+        out[impl] = gk.minibatch_gradients(st, data, covs, fam, gk.Log(), gk.PenaltyConfig(),
+                                           gk.Minibatch(I, J), offset=off, dtype="f32", k1_impl=impl)
+    a, b = out["tensor"], out["cuda_cores"]
+    for f in ("g_rowside", "h_rowside", "g_colside", "h_colside"):
+        assert normwise(getattr(a, f), getattr(b, f)) < TOL, f
+
+
+def test_k1_tensor_csr_equals_dense_bitwise():
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    y, x, z, off, st = _problem(5, 300, 200, 10, 1, 0, "nb", True)
+    I, J = np.arange(7, 250), np.arange(200)
+    covs = gk.CovariateSet(x=x, n=300, m=200)
+    outs = []
+    for data in (gk.ResponseMatrix(y), gk.ResponseMatrix(csr=dense_to_csr(y), shape=y.shape)):
+        outs.append(gk.minibatch_gradients(st, data, covs, gk.NegBinomial(2.0), gk.Log(),
+                                           gk.PenaltyConfig(), gk.Minibatch(I, J), offset=off,
+                                           dtype="f32", k1_impl="tensor"))
+    for f in ("g_rowside", "h_rowside", "g_colside", "h_colside"):
+        assert np.array_equal(getattr(outs[0], f), getattr(outs[1], f)), f
+
+
+def test_k1_tensor_rejects_ineligible_problems():
+    from paper_2412_20509_b200 import _lib
+    y, x, z, off, st = _problem(1, 50, 30, 3, 1, 0, "nb", False)
+    covs = gk.CovariateSet(x=x, n=50, m=30)
+    mb = gk.Minibatch(np.arange(50), np.arange(30))
+    with pytest.raises(_lib.UnsupportedError):      # fp64 runs on the CUDA cores only
+        gk.minibatch_gradients(st, gk.ResponseMatrix(y), covs, gk.NegBinomial(2.0), gk.Log(),
+                               gk.PenaltyConfig(), mb, dtype="f64", k1_impl="tensor")
+    with pytest.raises(_lib.UnsupportedError):      # prior weights
+        gk.minibatch_gradients(st, gk.ResponseMatrix(y, weights=np.ones_like(y)), covs,
+                               gk.NegBinomial(2.0), gk.Log(), gk.PenaltyConfig(), mb,
+                               dtype="f32", k1_impl="tensor")
+
+
+@pytest.mark.parametrize("impl", ["tensor", "cuda_cores"])
+def test_fit_fp32_trajectory_per_impl(impl):
+    from conftest import golden
+    g = golden("nb_cov_s3")
+    data = gk.ResponseMatrix(g["y"].astype(float))
+    covs = gk.CovariateSet(x=g["x"], z=g["z"])
+    st = gk.FactorizationState(g["init_b"], g["init_gamma"], g["init_u"], g["init_v"], 1.0,
+                               float(g["init_nb"]))
+    me, mr, mc, seed, cap = (int(v) for v in g["cfg"])
+    k0, k1, tau, a1, a2, damp, tol = (float(v) for v in g["cfg_f"])
+    cfg = gk.SgdConfig(max_epochs=me, rate_k0=k0, rate_k1=k1, rate_tau=tau, mb_rows=mr,
+                       mb_cols=mc, smooth_a1=a1, smooth_a2=a2, damping=damp, tol=tol, seed=seed,
+                       max_eval_entries=cap)
+    pen = gk.PenaltyConfig(lam=1.0, blocks=tuple(float(v) for v in g["lam"]))
+    final, rep = gk.fit_asgd(data, covs, gk.NegBinomial(st.nb_shape), gk.Log(), pen, cfg, st,
+                             dtype="f32", k1_impl=impl)
+    assert normwise(rep.objective_trace, g["trace"]) < TOL
+    assert normwise(final.u @ final.v.T, g["final_u"] @ g["final_v"].T) < 1e-3
