@@ -312,7 +312,14 @@ def main():
         phases = {nm: buf[i] / nst / 1e3 for i, nm in enumerate(names)}
         for i, nm in ((6, "p2_totals"), (7, "p2_rows"), (8, "p2_cols"), (9, "p2_rest"), (10, "p2_norms")):
             phases[nm + "_cum"] = buf[i] / nst / 1e3
-        st_ = np.array(buf[16:]).reshape(-1, 8)[:, :5]
+        per = np.array(buf[16:]).reshape(-1, 16)
+        st_ = per[:, :5]
+        kc = per[:, 8:16] / nst   # K1 sub-phase clocks per step (tensor path)
+        if kc.any():
+            names_k = ["col_operands", "staging_wait", "y_a1_gemm1", "d2_readout_b3", "barrier",
+                       "next_stage_rowside", "elementwise_gemm23", "drain_d3"]
+            phases["k1_subphases_us(mean over CTAs)"] = {
+                nm: float(kc[:, i].mean() / 1965.0) for i, nm in enumerate(names_k)}
         t0 = st_[:, 0].min()
         rel = (st_ - t0) / 1e3
         phases["last_step_per_cta_us"] = {

@@ -214,10 +214,11 @@ int gmf_status_decode(const void* raw, gmf_status* out);
 int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_ms, void* stream);
 /* Profiling hook: phase timers of the persistent kernel (globaltimer ns):
  * out[0..5] = CTA 0's {objective partials, K1 tiles, barrier 1, phase 2,
- * barrier 2, steps}, out[6..10] phase-2 sub-timers, out[16 + 8 c + i] the
+ * barrier 2, steps}, out[6..10] phase-2 sub-timers, out[16 + 16 c + i] the
  * last profiled step's stamps of CTA c (i: start, K1 start, K1 end, after
- * barrier 1, phase-2 end).  `out` holds gmf_profile_len(h) doubles; reads
- * (if out) and resets the counters, then enables/disables. */
+ * barrier 1, phase-2 end) and out[16 + 16 c + 8 + i], i < 8, CTA c's summed
+ * SM clocks of the tensor-core K1 sub-phases.  `out` holds gmf_profile_len(h)
+ * doubles; reads (if out) and resets the counters, then enables/disables. */
 int64_t gmf_profile_len(gmf_handle* h);
 /* launch geometry: {persistent CTAs, its row splits, column tiles, tile
  * width, per-step-kernel row splits, feature bucket, K1 smem bytes, max |I|} */

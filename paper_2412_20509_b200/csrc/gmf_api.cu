@@ -182,10 +182,17 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.est_alpha = cfg->est_alpha && desc->family == GMF_NEG_BINOMIAL;
   P.snap_stride = cfg->snapshot_stride; P.world = desc->world_size;
   // K1 implementation: tensor cores when eligible unless CUDA cores requested
-  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA);
+  if (desc->y_format == GMF_Y_CSR_I32 && desc->n > 0)
+    GMF_CUDA(cudaMemcpy(&P.nnz, bufs->csr_ptr + desc->n, 8, cudaMemcpyDeviceToHost));
+  // the tensor-core K1 stages rows with 16-byte copies: 16-byte aligned bases
+  auto al16 = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
+  const bool aligned = al16(bufs->theta_row) && (p == 0 || al16(bufs->x)) &&
+                       (!P.has_off || al16(bufs->offset)) &&
+                       (desc->y_format != GMF_Y_CSR_I32 || (al16(bufs->csr_col) && al16(bufs->csr_val)));
+  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA) && aligned;
   if (cfg->k1_impl == GMF_K1_TENSOR && !tc_ok) {
-    set_error("k1_impl=tensor needs fp32, no prior weights, q+d <= 16, p+d <= 16 (got Kr=%d Kc=%d)",
-              Kr, Kc);
+    set_error("k1_impl=tensor needs fp32, no prior weights, q+d <= 16, p+d <= 16 and 16-byte "
+              "aligned row/CSR buffers (got Kr=%d Kc=%d)", Kr, Kc);
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }
@@ -480,7 +487,7 @@ int gmf_snapshot_blocks(gmf_handle* h, int64_t* ver, int64_t* period, void* stre
   return GMF_OK;
 }
 
-int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 8 * (int64_t)h->fit_grid : 0; }
+int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 16 * (int64_t)h->fit_grid : 0; }
 
 int gmf_geometry(gmf_handle* h, int64_t* out8) {
   if (!h || !out8) { set_error("null handle/out"); return GMF_ERR_STATE; }

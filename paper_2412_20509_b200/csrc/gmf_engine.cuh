@@ -39,6 +39,7 @@ struct Params {
   int fam, yfmt, has_w, has_off;
   const int32_t* y;
   const int64_t* rp;
+  int64_t nnz;          // rp[n] (CSR)
   const int32_t* ci;
   const int32_t* cv;
   const void* w;

@@ -47,7 +47,7 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   if constexpr (TCM) {
     tc::Ctx tcx;
     tc::ctx_open(tcx, &s_tmem, s_bar);
-    tc::grad_cta<FAM, NK>(P, blk, s, alpha, rs, ct, RS, smem, tcx);
+    tc::grad_cta<FAM, NK>(P, blk, s, alpha, rs, ct, RS, smem, tcx, nullptr);
     tc::ctx_close(tcx);
   } else {
     grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
@@ -147,24 +147,33 @@ GMF_D unsigned int ld_acquire_u32(const unsigned int* p) {
   return v;
 }
 
+GMF_D unsigned int ld_relaxed_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long timeout_ns) {
   __shared__ int ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     int res = 1;
-    const unsigned int gen = ld_acquire_u32(gb + 1);
-    __threadfence();
+    const unsigned int gen = ld_relaxed_u32(gb + 1);
+    __threadfence();   // release this CTA's writes
     if (atomicAdd(gb, 1u) == G - 1) {
       atomicExch(gb, 0u);
       __threadfence();
       atomicAdd(gb + 1, 1u);
     } else {
+      // spin on relaxed loads (an acquire load per iteration would invalidate
+      // the SM's L1 every time); one acquire after the wait
       const unsigned long long t0 = gtimer();
-      while (ld_acquire_u32(gb + 1) == gen) {
-        if (ld_acquire_u32(gb + 2)) { res = 0; break; }
+      while (ld_relaxed_u32(gb + 1) == gen) {
+        if (ld_relaxed_u32(gb + 2)) { res = 0; break; }
         if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); res = 0; break; }
       }
     }
+    (void)ld_acquire_u32(gb + 1);   // acquire: later loads see other CTAs' writes
     __threadfence();
     ok = res;
   }
@@ -236,7 +245,7 @@ k_fit(Params P, long long n_steps) {
   unsigned long long t_a = prof ? gtimer() : 0, t_b;
   for (long long it = 0; it < n_steps; ++it) {
     const long long t = C.t;
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 0] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 0] = gtimer(); }
     const bool boundary = (t % P.S) == 0;
     const bool run_grad = t < P.max_steps;
     const long long blk = run_grad ? (long long)P.bseq[t] : -1;
@@ -265,13 +274,15 @@ k_fit(Params P, long long n_steps) {
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
     }
     if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 1] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
     if (run_grad && rs < RS) {
-      if constexpr (TCM) tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx);
+      if constexpr (TCM)
+        tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
+                              profc ? P.prof + 16 + 16 * blockIdx.x + 8 : nullptr);
       else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
     }
     if (prof) { t_b = gtimer(); P.prof[1] += t_b - t_a; t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 2] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 2] = gtimer(); }
     // Phase-2 inputs that phase 1 does not write are read before the barrier
     // so their latency hides behind it: this thread's first two row
     // coordinates (theta, EMA state) and the block's snapshot version.
@@ -288,7 +299,7 @@ k_fit(Params P, long long n_steps) {
       phb[u] = ldcg_t<T>(tptr<T>(P.hb_row) + o);
     }
     if (!gsync(kBarrierTimeoutNs)) break;
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 3] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
     // ------------------------- phase 2 -------------------------
     // totals, redundantly in every CTA: deviance, ||B||^2, ||V||^2,
@@ -434,7 +445,7 @@ k_fit(Params P, long long n_steps) {
     C = N;
     prev_blk = upd ? blk : -1;
     if (prof) { t_b = gtimer(); P.prof[3] += t_b - t_a; t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 8 * blockIdx.x + 4] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 4] = gtimer(); }
     if (D.stop) break;
     if (!gsync(kBarrierTimeoutNs)) break;
     if (prof) { t_b = gtimer(); P.prof[4] += t_b - t_a; t_a = t_b; P.prof[5] += 1; }

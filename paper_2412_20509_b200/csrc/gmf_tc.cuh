@@ -13,8 +13,8 @@
 //          written as the stacked bf16 tile P = [dd_hi; hh_hi; dd_lo; hh_lo]
 //   GEMM2  D2[128 x 64]    = P . R          row side, K = tile columns
 //          (R = [Rd_hi | Rd_lo | Rd2_hi | Rd2_lo], Rd = [z_j | v_j])
-//   GEMM3  D3[128 x 64]   += P^T . B3        column side, K = chunk rows
-//          (P read MN-major, B3 = [Ac_hi | Ac_lo | Ac2_hi | Ac2_lo], Ac = [x|u])
+//   GEMM3  D3[128 x 2K]   += P^T . [A1 | A1^2]   column side, K = chunk rows
+//          (P and the chunk's A1 rows both read MN-major; [x|u] = first Kc of a)
 //
 // fp32 accuracy from bf16 operands: every operand is split x = hi + lo
 // (hi = bf16(x), lo = bf16(x - hi)); GEMM1 sums hi.hi + hi.lo + lo.hi,
@@ -35,16 +35,16 @@
 namespace gmf {
 namespace tc {
 
+static_assert(kThreads == 256, "tensor-core K1 assumes 8 warps: 4 TMEM lane quarters x 2 column halves");
 constexpr int TCC = 128;              // tile columns (GEMM1 N, GEMM3 M)
 constexpr int TRC = 32;               // rows per chunk (x4 replicas = UMMA M 128)
 constexpr int YP = 132;               // Y tile pitch (int32): conflict-free 16-byte row reads
 constexpr uint32_t kCols = 256;       // TMEM columns per CTA
 constexpr uint32_t T_ETA = 0, T_D2 = 128, T_D3 = 192;
 constexpr uint32_t SBO_P = 2048;      // P / R: 16 column cores x 128 B
-constexpr uint32_t SBO_B3 = 512;      // B3: 4 row cores x 128 B
 
 struct Smem {
-  int64_t P, R, B1h, B1l, A1h, A1l, B3, Y, stage, araw, off, rp, total;
+  int64_t P, R, B1h, B1l, A1h, A1l, Ash, Asl, Y, stage, araw, off, rp, scr, total;
   int nka;
 };
 
@@ -59,12 +59,14 @@ GMF_HD Smem smem_layout(int NK) {
   s.B1l = o; o = al(o + TCC * s.nka * 2);
   s.A1h = o; o = al(o + 128 * s.nka * 2);
   s.A1l = o; o = al(o + 128 * s.nka * 2);
-  s.B3 = o; o = al(o + 64 * TRC * 2);
+  s.Ash = o; o = al(o + TRC * s.nka * 2);
+  s.Asl = o; o = al(o + TRC * s.nka * 2);
   s.Y = o; o = al(o + TRC * YP * 4);
-  s.stage = o; o = al(o + (int64_t)kStageCap * 8);   // == TRC * TCC * 4 (dense)
-  s.araw = o; o = al(o + TRC * NK * 4);
-  s.off = o; o = al(o + TRC * 4);
+  s.stage = o; o = al(o + (int64_t)kStageCap * 8);   // == TRC * TCC * 4 (dense); CSR col | val
+  s.araw = o; o = al(o + (TRC * NK + 16) * 4);
+  s.off = o; o = al(o + (TRC + 8) * 4);
   s.rp = o; o = al(o + (kRpMax + 1) * 8);
+  s.scr = o; o = al(o + 2 * 32 * 17 * 4);
   s.total = o;
   return s;
 }
@@ -210,15 +212,74 @@ GMF_D void put_split16(const float (&x)[16], unsigned char* Pb, int m_hi, int m_
   *reinterpret_cast<uint4*>(Pb + kofs(m_lo, c0 + 8, SBO_P)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
 }
 
+GMF_D void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// Stage elements [begin, end) of a 4-byte array of `total` elements into
+// shared memory (block-cooperative): whole 16-byte quads inside the array by
+// 16-byte cp.async, the array's ragged tail by 4-byte copies.  The quad
+// containing `begin` starts at dst, so element `begin` lands at dst[begin % 4];
+// returns that offset.
+GMF_D int stage_range4(void* dst, const void* src, int64_t begin, int64_t end, int64_t total) {
+  const int64_t b4 = begin & ~int64_t(3);
+  const int64_t nq = (end - b4 + 3) >> 2;
+  const int64_t full = total >> 2;
+  for (int64_t qi = threadIdx.x; qi < nq; qi += kThreads) {
+    const int64_t qg = (b4 >> 2) + qi;
+    char* d = reinterpret_cast<char*>(dst) + qi * 16;
+    const char* sp = reinterpret_cast<const char*>(src);
+    if (qg < full) {
+      cp_async16(d, sp + qg * 16);
+    } else {
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = qg * 4 + u;
+        cp_async<4>(d + 4 * u, sp + (e < total ? e : 0) * 4, e < total);
+      }
+    }
+  }
+  return (int)(begin - b4);
+}
+
+// 8 fp32 values -> packed bf16 hi (4 words) and lo = bf16(x - hi) (4 words)
+GMF_D void split8(const float (&x)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+  #pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float a = x[2 * u], b = x[2 * u + 1];
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h[u]) : "f"(b), "f"(a));
+    const float ra = a - __uint_as_float(h[u] << 16);
+    const float rb = b - __uint_as_float(h[u] & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l[u]) : "f"(rb), "f"(ra));
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 template <int FAM, int NK>
 GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct, int RS,
-                    unsigned char* smem, Ctx& X) {
+                    unsigned char* smem, Ctx& X, unsigned long long* kp) {
+  // optional sub-phase clocks (thread 0, accumulated): 0 column operands,
+  // 1 staging wait + GEMM2/3(c-1) wait, 2 Y + A1, 3 next staging + GEMM1
+  // issue, 4 D2 readout, 5 elementwise, 6 GEMM2/3 issue, 7 drain
+  long long tk = (kp && threadIdx.x == 0) ? clock64() : 0;
+  long long kacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto tick = [&](int i) {
+    if (kp && threadIdx.x == 0) {
+      const long long t = clock64();
+      kacc[i] += t - tk;
+      tk = t;
+    }
+  };
   using T = float;
   __shared__ double red_scr[kThreads / 32];
   __shared__ int stage_n;
+  __shared__ int s_oth, s_ox, s_oo, s_ocsr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = warp & 3, hf = warp >> 2;
-  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q, d = P.d;
+  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q;
   const int64_t r0 = P.rbp[blk], nI = P.rbp[blk + 1] - r0;
   const int64_t j0 = P.cbp[s], nJ = P.cbp[s + 1] - j0;
   const int64_t rlo = nI * rs / RS, rhi = nI * (rs + 1) / RS;
@@ -239,12 +300,14 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   unsigned char* B1l = smem + L.B1l;
   unsigned char* A1h = smem + L.A1h;
   unsigned char* A1l = smem + L.A1l;
-  unsigned char* B3b = smem + L.B3;
+  unsigned char* Ash = smem + L.Ash;
+  unsigned char* Asl = smem + L.Asl;
   int32_t* Y = reinterpret_cast<int32_t*>(smem + L.Y);
   unsigned char* st = smem + L.stage;
   T* araw = reinterpret_cast<T*>(smem + L.araw);
   T* off_s = reinterpret_cast<T*>(smem + L.off);
   int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
+  float* scr = reinterpret_cast<float*>(smem + L.scr);   // [2][32][17]
 
   const T* th_row = tptr<T>(P.th_row);
   const T* th_col = tptr<T>(P.th_col);
@@ -265,64 +328,18 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     return;
   }
 
-  // ---- column operands of the tile (once per call) ----
-  // B1 = [b | v | z] * log2(e), split hi/lo; K-major (N = columns)
-  for (int e = tid; e < TCC * nka; e += kThreads) {
-    const int c = e / nka, k = e % nka;
-    T v = T(0);
-    if (c < ncv && k < KA) {
-      const int64_t pos = cbase + c;
-      const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
-      v = (k < Kc ? th_col[j * Kc + k] : zg[j * q + (k - Kc)]) * pre;
-    }
-    __nv_bfloat16 h, l;
-    split_bf16(v, h, l);
-    const uint32_t o = kofs(c, k, sbo1);
-    *reinterpret_cast<__nv_bfloat16*>(B1h + o) = h;
-    *reinterpret_cast<__nv_bfloat16*>(B1l + o) = l;
-  }
-  // R = [Rd_hi | Rd_lo | Rd2_hi | Rd2_lo], Rd = [z_j | v_j]; K-major (N = 64 features)
-  for (int e = tid; e < TCC * 16; e += kThreads) {
-    const int c = e >> 4, k = e & 15;
-    T v = T(0);
-    if (c < ncv && k < Kr) {
-      const int64_t pos = cbase + c;
-      const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
-      v = k < q ? zg[j * q + k] : th_col[j * Kc + p + (k - q)];
-    }
-    __nv_bfloat16 h, l, h2, l2;
-    split_bf16(v, h, l);
-    split_bf16(v * v, h2, l2);
-    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(k, c, SBO_P)) = h;
-    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(16 + k, c, SBO_P)) = l;
-    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(32 + k, c, SBO_P)) = h2;
-    *reinterpret_cast<__nv_bfloat16*>(Rb + kofs(48 + k, c, SBO_P)) = l2;
-  }
-  if (rp_staged)
-    for (int64_t e = tid; e <= nrows; e += kThreads) rp_s[e] = P.rp[r0 + rlo + e];
-  for (int e = tid; e < TRC * YP; e += kThreads) Y[e] = 0;
-  __syncthreads();
-
-  // ---- asynchronous staging of one chunk (row features, offsets, Y) ----
+  // ---- asynchronous staging of one chunk: its rows are contiguous in the
+  // block-major layout, so theta_row, x, offsets and the CSR range are four
+  // contiguous ranges (16-byte cp.async) ----
+  T* thr_s = araw;                          // rows x Kr (+ alignment slack)
+  T* xr_s = araw + TRC * Kr + 8;            // rows x p
   auto issue = [&](int64_t rowbase) {
     const int rows = (int)((rhi - rowbase) < TRC ? (rhi - rowbase) : TRC);
     const int64_t i0 = r0 + rowbase;
-    for (int e = tid; e < TRC * NK; e += kThreads) {
-      const int rr = e / NK, k = e % NK;
-      const T* src = xg;
-      bool ok = false;
-      if (rr < rows) {
-        const int64_t i = i0 + rr;
-        if (k < p) { src = xg + i * p + k; ok = true; }
-        else if (k < p + d) { src = th_row + i * Kr + q + (k - p); ok = true; }
-        else if (k < KA) { src = th_row + i * Kr + (k - p - d); ok = true; }
-      }
-      cp_async<4>(araw + e, src, ok);
-    }
-    if (tid < TRC) {
-      const bool ok = tid < rows && P.has_off;
-      cp_async<4>(off_s + tid, ok ? offg + i0 + tid : offg, ok);
-    }
+    const int oth = stage_range4(thr_s, th_row, i0 * Kr, (i0 + rows) * Kr, P.n * Kr);
+    const int ox = p ? stage_range4(xr_s, xg, i0 * p, (i0 + rows) * p, P.n * p) : 0;
+    const int oo = P.has_off ? stage_range4(off_s, offg, i0, i0 + rows, P.n) : 0;
+    int ocsr = 0;
     if (!csr) {
       int32_t* y_b = reinterpret_cast<int32_t*>(st);
       for (int e = tid; e < TRC * TCC; e += kThreads) {
@@ -334,23 +351,99 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       }
     } else if (rp_staged) {
       const int64_t lo = rp_s[rowbase - rlo], hi = rp_s[rowbase - rlo + rows];
-      const int64_t nnz = hi - lo;
-      if (nnz <= kStageCap) {
+      if (hi - lo + 6 <= kStageCap) {
         int32_t* col_b = reinterpret_cast<int32_t*>(st);
         int32_t* val_b = col_b + kStageCap;
-        for (int64_t e = tid; e < nnz; e += kThreads) {
-          cp_async<4>(col_b + e, P.ci + lo + e, true);
-          cp_async<4>(val_b + e, P.cv + lo + e, true);
-        }
-        if (tid == 0) stage_n = (int)nnz;
+        ocsr = stage_range4(col_b, P.ci, lo, hi, P.nnz);
+        stage_range4(val_b, P.cv, lo, hi, P.nnz);
+        if (tid == 0) stage_n = (int)(hi - lo);
       } else if (tid == 0) {
         stage_n = -1;
       }
     } else if (tid == 0) {
       stage_n = -1;
     }
+    if (tid == 0) { s_oth = oth; s_ox = ox; s_oo = oo; s_ocsr = ocsr; }
     cp_async_commit();
   };
+
+  // ---- column operands of the tile (once per call); global loads first ----
+  // feature order a = [x | u | gamma], c = [b | v | z]
+  // B1: thread per (column, 8 features); R: thread per (feature, 8 columns)
+  const int ng1 = nka / 8;
+  float b1v[8], rv[8];
+  int b1c = 0, b1g = 0, rk = 0, rcg = 0;
+  const bool b1_task = tid < TCC * ng1 / 2;         // first half of the B1 tasks
+  {
+    const int t = tid;
+    b1c = t / ng1; b1g = t % ng1;
+    const int64_t pos = cbase + b1c;
+    const bool ok = b1c < ncv;
+    const int64_t j = ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = 8 * b1g + u;
+      const bool in_c = ok && k < Kc, in_z = ok && k >= Kc && k < KA;
+      const float* src = in_c ? th_col + j * Kc + k : (in_z ? zg + j * q + (k - Kc) : th_col);
+      const float x = *src;
+      b1v[u] = (in_c || in_z) ? x * pre : 0.f;
+    }
+    rk = t / (TCC / 8); rcg = t % (TCC / 8);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = 8 * rcg + u;
+      const bool okr = c < ncv && rk < Kr;
+      const int64_t posr = cbase + c;
+      const int64_t jr = okr ? (P.col_identity ? posr : (int64_t)P.cidx[j0 + posr]) : 0;
+      const float* src = !okr ? th_col : (rk < q ? zg + jr * q + rk : th_col + jr * Kc + p + (rk - q));
+      const float x = *src;
+      rv[u] = okr ? x : 0.f;
+    }
+  }
+  if (rp_staged)
+    for (int64_t e = tid; e <= nrows; e += kThreads) rp_s[e] = P.rp[r0 + rlo + e];
+  for (int e = tid; e < TRC * YP; e += kThreads) Y[e] = 0;
+  __syncthreads();   // rp staged
+  issue(rlo);
+  {
+    uint4 h, l;
+    if (b1_task || ng1 == 2) {
+      split8(b1v, h, l);
+      *reinterpret_cast<uint4*>(B1h + kofs(b1c, 8 * b1g, sbo1)) = h;
+      *reinterpret_cast<uint4*>(B1l + kofs(b1c, 8 * b1g, sbo1)) = l;
+    }
+    float r2[8];
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) r2[u] = rv[u] * rv[u];
+    uint4 h2, l2;
+    split8(rv, h, l);
+    split8(r2, h2, l2);
+    *reinterpret_cast<uint4*>(Rb + kofs(rk, 8 * rcg, SBO_P)) = h;
+    *reinterpret_cast<uint4*>(Rb + kofs(16 + rk, 8 * rcg, SBO_P)) = l;
+    *reinterpret_cast<uint4*>(Rb + kofs(32 + rk, 8 * rcg, SBO_P)) = h2;
+    *reinterpret_cast<uint4*>(Rb + kofs(48 + rk, 8 * rcg, SBO_P)) = l2;
+  }
+  if (ng1 == 4) {   // K = 32: the second half of the B1 tasks
+    const int t = tid + kThreads;
+    const int c = t / ng1, g = t % ng1;
+    const int64_t pos = cbase + c;
+    const bool ok = c < ncv;
+    const int64_t j = ok ? (P.col_identity ? pos : (int64_t)P.cidx[j0 + pos]) : 0;
+    float v[8];
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = 8 * g + u;
+      const bool in_c = ok && k < Kc, in_z = ok && k >= Kc && k < KA;
+      const float* src = in_c ? th_col + j * Kc + k : (in_z ? zg + j * q + (k - Kc) : th_col);
+      const float x = *src;
+      v[u] = (in_c || in_z) ? x * pre : 0.f;
+    }
+    uint4 h, l;
+    split8(v, h, l);
+    *reinterpret_cast<uint4*>(B1h + kofs(c, 8 * g, sbo1)) = h;
+    *reinterpret_cast<uint4*>(B1l + kofs(c, 8 * g, sbo1)) = l;
+  }
+  tick(0);
 
   const T rphi = T(1.0 / P.phi);
   const T ralpha = T(1.0 / alpha);
@@ -359,55 +452,58 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const uint32_t tm = X.tmem;
   constexpr uint32_t ID1 = idesc(128, 128, 0, 0);
   constexpr uint32_t ID2 = idesc(128, 64, 0, 0);
-  constexpr uint32_t ID3 = idesc(128, 32, 1, 0);
+  const uint32_t ID3 = idesc(128, nka, 1, 1);
   const int c0 = 32 * qd + 16 * hf;                 // this thread's first tile column
   const int vcols = ncv - c0 < 0 ? 0 : (ncv - c0 > 16 ? 16 : ncv - c0);
   const uint32_t lane_base = (uint32_t)(32 * qd) << 16;
   double nb_num = 0.0, nb_den = 0.0;
   T* rowpart = tptr<T>(P.rowpart);
   const int rkk = 2 * Kr;
+  // A1 task of this thread: (replica, row, 8-feature group)
+  const int a_rep = tid / (TRC * 2), a_rr = (tid / 2) % TRC, a_g2 = tid & 1;
 
-  // row side of the previous chunk: wait GEMM2/3, read D2 (warps 0-3:
-  // quarter 0 = dd_hi rows, 1 = hh_hi, 2 = dd_lo, 3 = hh_lo), combine the
-  // hi and lo halves through shared memory, write rowpart
+  // D2 readout (warps 0-3; quarter 0 = dd_hi rows, 1 = hh_hi, 2 = dd_lo,
+  // 3 = hh_lo); hi and lo halves combined through shared memory under a
+  // 128-thread named barrier
   auto readout_d2 = [&](int64_t rowbase, int rows) {
-    mbar_wait(&X.bar[1], X.n23 & 1u);
-    ++X.n23;
-    fence_after();
-    float* scr = reinterpret_cast<float*>(st);   // [2][32][17]
-    float v[16];
-    if (hf == 0) {
-      uint32_t a[16], b[16];
-      const uint32_t col = tm + lane_base + T_D2 + ((qd & 1) ? 32u : 0u);
-      tmem_ld16(col, a);
-      tmem_ld16(col + 16, b);
+    float dv[16];
+    uint32_t a[16], b[16];
+    const uint32_t col = tm + lane_base + T_D2 + ((qd & 1) ? 32u : 0u);
+    tmem_ld16(col, a);
+    tmem_ld16(col + 16, b);
+    #pragma unroll
+    for (int k = 0; k < 16; ++k) dv[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
+    if (qd >= 2) {
       #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
-      if (qd >= 2) {
-        #pragma unroll
-        for (int k = 0; k < 16; ++k) scr[((qd - 2) * 32 + lane) * 17 + k] = v[k];
-      }
+      for (int k = 0; k < 16; ++k) scr[((qd - 2) * 32 + lane) * 17 + k] = dv[k];
     }
     fence_before();
-    __syncthreads();
-    if (hf == 0 && qd < 2 && lane < rows) {
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (qd < 2 && lane < rows) {
       T* outp = rowpart + ((int64_t)ct * P.nstar_max + rowbase + lane) * rkk + (qd == 0 ? 0 : Kr);
       #pragma unroll
       for (int k = 0; k < 16; ++k)
-        if (k < Kr) outp[k] = v[k] + scr[(qd * 32 + lane) * 17 + k];
+        if (k < Kr) outp[k] = dv[k] + scr[(qd * 32 + lane) * 17 + k];
     }
+    asm volatile("bar.sync 1, 128;" ::: "memory");   // scratch reused by the next readout
   };
 
-  issue(rlo);
   int64_t prev_rowbase = -1;
   int prev_rows = 0;
   bool first3 = true;
   for (int64_t rowbase = rlo; rowbase < rhi; rowbase += TRC) {
     const int rows = (int)((rhi - rowbase) < TRC ? (rhi - rowbase) : TRC);
     const int64_t i0 = r0 + rowbase;
+    // ---- S1: chunk staged; GEMM2/3 of the previous chunk done (frees P, A1, D2) ----
     cp_async_wait0();
-    __syncthreads();   // chunk staged; previous elementwise done with Y
-    // ---- Y tile ----
+    if (prev_rowbase >= 0) {
+      mbar_wait(&X.bar[1], X.n23 & 1u);
+      ++X.n23;
+    }
+    fence_after();
+    __syncthreads();
+    tick(1);
+    // ---- S2: Y tile and A1 = a_i (hi/lo, four replicas) + a_i^2 (hi/lo) ----
     if (!csr) {
       const int32_t* y_b = reinterpret_cast<const int32_t*>(st);
       for (int e = tid; e < TRC * TCC; e += kThreads) Y[(e / TCC) * YP + (e % TCC)] = y_b[e];
@@ -417,7 +513,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         const int32_t* col_b = reinterpret_cast<const int32_t*>(st);
         const int32_t* val_b = col_b + kStageCap;
         const int64_t* rpc = rp_s + (rowbase - rlo);
-        const int lo = (int)rpc[0];
+        const int lo = (int)rpc[0] - s_ocsr;
         for (int rr = warp; rr < rows; rr += kThreads / 32) {
           const int a = (int)rpc[rr] - lo, bnd = (int)rpc[rr + 1] - lo;
           for (int e = a + lane; e < bnd; e += 32) {
@@ -439,22 +535,41 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         }
       }
     }
-    // ---- A1: [x | u | gamma] of the chunk rows, hi/lo, four replicas ----
-    for (int e = tid; e < TRC * nka; e += kThreads) {
-      const int rr = e / nka, k = e % nka;
-      const T v = (rr < rows && k < KA) ? araw[rr * NK + k] : T(0);
-      __nv_bfloat16 h, l;
-      split_bf16(v, h, l);
-      #pragma unroll
-      for (int rep = 0; rep < 4; ++rep) {
-        const uint32_t o = kofs(32 * rep + rr, k, sbo1);
-        *reinterpret_cast<__nv_bfloat16*>(A1h + o) = h;
-        *reinterpret_cast<__nv_bfloat16*>(A1l + o) = l;
+    {
+      const T* thr = thr_s + s_oth + a_rr * Kr;
+      const T* xr = xr_s + s_ox + a_rr * p;
+      const bool rok = a_rr < rows;
+      for (int g = a_g2; g < ng1; g += 2) {
+        float v[8], v2[8];
+        #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = 8 * g + u;
+          // a_k: x_k (k < p), else theta_row[(k - p + q) mod Kr] = u then gamma
+          int kt = k - p + q;
+          kt = kt >= Kr ? kt - Kr : kt;
+          kt = (k >= p && k < KA) ? kt : 0;
+          const int kx = k < p ? k : 0;
+          const float tv = thr[kt], xv = xr[kx];
+          v[u] = !rok ? 0.f : (k < p ? xv : (k < KA ? tv : 0.f));
+          v2[u] = v[u] * v[u];
+        }
+        uint4 h, l;
+        split8(v, h, l);
+        *reinterpret_cast<uint4*>(A1h + kofs(32 * a_rep + a_rr, 8 * g, sbo1)) = h;
+        *reinterpret_cast<uint4*>(A1l + kofs(32 * a_rep + a_rr, 8 * g, sbo1)) = l;
+        if (a_rep == 0) {
+          split8(v2, h, l);
+          *reinterpret_cast<uint4*>(Ash + kofs(a_rr, 8 * g, sbo1)) = h;
+          *reinterpret_cast<uint4*>(Asl + kofs(a_rr, 8 * g, sbo1)) = l;
+        }
       }
     }
+    const T offr = (lane < rows && P.has_off) ? off_s[s_oo + lane] * pre : T(0);
     fence_async_smem();
-    __syncthreads();
-    // ---- GEMM1: eta = A1 . B1^T (hi.hi + hi.lo + lo.hi) ----
+    __syncthreads();   // Y, A1 written; staging consumed
+    tick(2);
+    // ---- S3: prefetch the next chunk, GEMM1 eta = A1 . B1^T ----
+    if (rowbase + TRC < rhi) issue(rowbase + TRC);
     if (tid == 0) {
       fence_after();
       for (int kt = 0; kt < nka / 16; ++kt) {
@@ -469,25 +584,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       }
       umma_commit(&X.bar[0]);
     }
-    // ---- previous chunk's row side (frees P, D2 and B3) ----
-    if (prev_rowbase >= 0) readout_d2(prev_rowbase, prev_rows);
-    // ---- B3: [Ac_hi | Ac_lo | Ac2_hi | Ac2_lo] x chunk rows, K-major ----
-    for (int e = tid; e < TRC * 16; e += kThreads) {
-      const int rr = e >> 4, k = e & 15;
-      const T v = (rr < rows && k < Kc) ? araw[rr * NK + k] : T(0);
-      __nv_bfloat16 h, l, h2, l2;
-      split_bf16(v, h, l);
-      split_bf16(v * v, h2, l2);
-      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(k, rr, SBO_B3)) = h;
-      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(16 + k, rr, SBO_B3)) = l;
-      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(32 + k, rr, SBO_B3)) = h2;
-      *reinterpret_cast<__nv_bfloat16*>(B3b + kofs(48 + k, rr, SBO_B3)) = l2;
-    }
-    const T offr = (lane < rows && P.has_off) ? off_s[lane] * pre : T(0);
-    __syncthreads();   // staging buffers consumed
-    if (rowbase + TRC < rhi) issue(rowbase + TRC);
-
-    // ---- elementwise: thread = chunk row `lane`, columns c0..c0+15 ----
+    tick(3);
+    // ---- S4: previous chunk's row side (warps 0-3) ----
+    if (prev_rowbase >= 0 && hf == 0) readout_d2(prev_rowbase, prev_rows);
+    tick(4);
+    // ---- S5: elementwise, thread = chunk row `lane`, columns c0..c0+15 ----
     mbar_wait(&X.bar[0], X.n1 & 1u);
     ++X.n1;
     fence_after();
@@ -532,7 +633,8 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     fence_async_smem();
     fence_before();
     __syncthreads();
-    // ---- GEMM2 (row side) and GEMM3 (column side) ----
+    tick(5);
+    // ---- S6: GEMM2 (row side) and GEMM3 (column side) ----
     if (tid == 0) {
       fence_after();
       #pragma unroll
@@ -541,37 +643,45 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         umma(tm + T_D2, sdesc(sb + (uint32_t)L.P + ko, 128, SBO_P),
              sdesc(sb + (uint32_t)L.R + ko, 128, SBO_P), ID2, kt > 0 ? 1u : 0u);
       }
-      // P^T (MN-major: column chunks +128 B, 8-row K groups +2048 B) . B3
-      const uint32_t ao[4] = {0u, 4096u, 16384u, 20480u};   // stacked rows 0,16 (hi) 64,80 (lo)
-      const uint32_t bo[4] = {0u, 256u, 0u, 256u};          // chunk rows 0, 16
+      // D3[col][k] += P^T . A1 (dd) and P^T . A1^2 (hh): P read MN-major
+      // (column chunks +128 B, 8-row K groups +2048 B), A1 read MN-major
+      // (feature chunks +128 B, 8-row K groups +sbo1); K = chunk rows 0-15, 16-31
       #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t acc = (first3 && u == 0) ? 0u : 1u;
-        umma(tm + T_D3, sdesc(sb + (uint32_t)L.P + ao[u], 2048, 128),
-             sdesc(sb + (uint32_t)L.B3 + bo[u], 128, SBO_B3), ID3, acc);
-        umma(tm + T_D3 + 32, sdesc(sb + (uint32_t)L.P + ao[u] + 8192u, 2048, 128),
-             sdesc(sb + (uint32_t)L.B3 + 4 * SBO_B3 + bo[u], 128, SBO_B3), ID3, acc);
+        const uint32_t pa = (u & 2 ? 16384u : 0u) + (u & 1) * 4096u;   // dd_hi / dd_lo rows
+        const uint32_t bo = (uint32_t)(u & 1) * 2u * sbo1;               // chunk rows 0 / 16
+        const uint32_t acc0 = (first3 && u == 0) ? 0u : 1u;
+        const uint64_t pd = sdesc(sb + (uint32_t)L.P + pa, 2048, 128);
+        const uint64_t ph = sdesc(sb + (uint32_t)L.P + pa + 8192u, 2048, 128);
+        umma(tm + T_D3, pd, sdesc(sb + (uint32_t)L.A1h + bo, sbo1, 128), ID3, acc0);
+        umma(tm + T_D3, pd, sdesc(sb + (uint32_t)L.A1l + bo, sbo1, 128), ID3, 1u);
+        umma(tm + T_D3 + nka, ph, sdesc(sb + (uint32_t)L.Ash + bo, sbo1, 128), ID3, acc0);
+        umma(tm + T_D3 + nka, ph, sdesc(sb + (uint32_t)L.Asl + bo, sbo1, 128), ID3, 1u);
       }
       umma_commit(&X.bar[1]);
     }
     first3 = false;
+    tick(6);
     prev_rowbase = rowbase;   // block-relative row index of the chunk
     prev_rows = rows;
   }
   cp_async_wait0();
   // ---- drain: last chunk's row side, then the column side ----
-  readout_d2(prev_rowbase, prev_rows);
+  mbar_wait(&X.bar[1], X.n23 & 1u);
+  ++X.n23;
+  fence_after();
+  if (hf == 0) readout_d2(prev_rowbase, prev_rows);
   {
-    fence_after();
-    uint32_t a[16], b[16];
-    const uint32_t col = tm + lane_base + T_D3 + 32u * (uint32_t)hf;
-    tmem_ld16(col, a);
-    tmem_ld16(col + 16, b);
+    // lane = tile column; D3 columns = a-features [x | u | gamma], whose first
+    // Kc are the column side's [x | u]
+    uint32_t a[16];
+    const uint32_t col = tm + lane_base + T_D3 + (hf ? (uint32_t)nka : 0u);
     const int c = 32 * qd + lane;
     T* outp = colpart + cpb + (int64_t)c * (2 * Kc) + (hf ? Kc : 0);
+    tmem_ld16(col, a);
     #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < Kc) outp[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
+    for (int f = 0; f < 16; ++f)
+      if (f < Kc) outp[f] = __uint_as_float(a[f]);
   }
   fence_before();
   const double bn = block_sum<kThreads>(nb_num, red_scr);
@@ -580,6 +690,9 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     P.nbpart[2 * ((int64_t)ct * RS + rs)] = bn;
     P.nbpart[2 * ((int64_t)ct * RS + rs) + 1] = bd;
   }
+  tick(7);
+  if (kp && tid == 0)
+    for (int i = 0; i < 8; ++i) kp[i] += (unsigned long long)kacc[i];
 }
 
 }  // namespace tc

@@ -30,3 +30,6 @@ for d in data:
 print("--- opcode mix (executed)")
 for op, v in c.most_common(25):
     print(f"{op:12s} {v / ti * 100:5.1f}%")
+print("--- by executed count")
+for d in sorted(data, key=lambda d: -num(d[ki]))[:N]:
+    print(f"{d['idx']:5d} s={num(d[ks]) / ts * 100:5.2f}% i={num(d[ki]) / ti * 100:5.2f}%  {d['Source'][:100]}")
