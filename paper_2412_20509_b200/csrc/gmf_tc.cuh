@@ -5,15 +5,16 @@
 // (128 columns of block J) and a balanced contiguous row range of block I,
 // and writes rowpart / colpart / nbpart identically.  Per 32-row chunk:
 //
-//   GEMM1  eta[128 x 128]   = A1 . B1^T      rows x columns, K = p+q+d
-//          (A1 = [x|u|gamma] of the 32 rows, replicated into the four TMEM
-//          lane quarters so all 8 warps read eta; B1 = [b|v|z] * log2 e)
+//   GEMM1  eta[128 x 128]  = A1 . B1^T        rows x columns, K = p+q+d
+//          (A1 = a_i = [x|u|gamma] of the 32 rows, replicated into the four
+//          TMEM lane quarters so all 8 warps read eta; B1 = [b|v|z] * log2 e)
 //   elementwise (CUDA cores, thread = row, 16 columns):
 //          mu = 2^eta, dotD / ddotD (NB or Poisson, log link), NB moments,
-//          written as the stacked bf16 tile P = [dd_hi; hh_hi; dd_lo; hh_lo]
-//   GEMM2  D2[128 x 64]    = P . R          row side, K = tile columns
+//          written as the stacked bf16 tile P (dd rows, then hh rows; hi and
+//          lo split rows interleaved by 8, see stack_hi)
+//   GEMM2  D2[128 x 64]    = P . R           row side, K = tile columns
 //          (R = [Rd_hi | Rd_lo | Rd2_hi | Rd2_lo], Rd = [z_j | v_j])
-//   GEMM3  D3[128 x 2K]   += P^T . [A1 | A1^2]   column side, K = chunk rows
+//   GEMM3  D3[128 x 64]   += P^T . [A1 | A1^2]   column side, K = chunk rows
 //          (P and the chunk's A1 rows both read MN-major; [x|u] = first Kc of a)
 //
 // fp32 accuracy from bf16 operands: every operand is split x = hi + lo
@@ -22,11 +23,12 @@
 // per product ~2^-17, inside the fp32 north-star tolerance (1e-4).
 //
 // Shared-memory operands use the canonical no-swizzle core-matrix layout
-// (8 rows x 16 bytes): K-major tiles for every operand, and the same P tile
-// read MN-major by GEMM3 (verified layouts: tools/umma_test.cu).
+// (8 rows x 16 bytes): K-major tiles for GEMM1/GEMM2 and the same P and A1
+// tiles read MN-major by GEMM3 (verified layouts: tools/umma_test.cu).
 // TMEM: 256 columns per CTA (two CTAs per SM): eta [0,128), D2 [128,192),
-// D3 [192,256).  One thread issues the MMAs; completion is tracked with
-// tcgen05.commit -> mbarrier.
+// D3 [192,256).  One thread issues the MMAs (19 per chunk: tiny MMAs cost
+// ~47 cycles each on the tensor pipe, tools/umma_bench.cu); completion is
+// tracked with tcgen05.commit -> mbarrier.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -44,7 +46,7 @@ constexpr uint32_t T_ETA = 0, T_D2 = 128, T_D3 = 192;
 constexpr uint32_t SBO_P = 2048;      // P / R: 16 column cores x 128 B
 
 struct Smem {
-  int64_t P, R, B1h, B1l, A1h, A1l, Ash, Asl, Y, stage, araw, off, rp, scr, total;
+  int64_t P, R, B1h, B1l, A1, As, Y, stage, araw, off, rp, total;
   int nka;
 };
 
@@ -57,16 +59,13 @@ GMF_HD Smem smem_layout(int NK) {
   s.R = o; o = al(o + 64 * TCC * 2);
   s.B1h = o; o = al(o + TCC * s.nka * 2);
   s.B1l = o; o = al(o + TCC * s.nka * 2);
-  s.A1h = o; o = al(o + 128 * s.nka * 2);
-  s.A1l = o; o = al(o + 128 * s.nka * 2);
-  s.Ash = o; o = al(o + TRC * s.nka * 2);
-  s.Asl = o; o = al(o + TRC * s.nka * 2);
+  s.A1 = o; o = al(o + 128 * s.nka * 2 * 2);   // hi | lo interleaved per 16 features
+  s.As = o; o = al(o + TRC * 16 * 2 * 2);       // squares of features 0..15, hi | lo
   s.Y = o; o = al(o + TRC * YP * 4);
   s.stage = o; o = al(o + (int64_t)kStageCap * 8);   // == TRC * TCC * 4 (dense); CSR col | val
   s.araw = o; o = al(o + (TRC * NK + 16) * 4);
   s.off = o; o = al(o + (TRC + 8) * 4);
   s.rp = o; o = al(o + (kRpMax + 1) * 8);
-  s.scr = o; o = al(o + 2 * 32 * 17 * 4);
   s.total = o;
   return s;
 }
@@ -78,6 +77,21 @@ GMF_HD uint32_t kofs(int mn, int k, uint32_t sbo) {
   return (uint32_t)(mn >> 3) * sbo + (uint32_t)(k >> 3) * 128u + (uint32_t)(mn & 7) * 16u +
          (uint32_t)(k & 7) * 2u;
 }
+
+// A1 (row features, K-major) with hi and lo interleaved per 16 features:
+// row group of 8 rows = per K-step [hi core 0 | hi core 1 | lo core 0 | lo core 1];
+// GEMM1 reads hi or lo (LBO 128), GEMM3 reads hi|lo of features 0..15 as one
+// MN-major N=32 operand.  sboc = (nka / 16) * 512.
+GMF_HD uint32_t a1ofs(int row, int k, int lo, uint32_t sboc) {
+  return (uint32_t)(row >> 3) * sboc + (uint32_t)((k >> 4) * 4 + lo * 2 + ((k >> 3) & 1)) * 128u +
+         (uint32_t)(row & 7) * 16u + (uint32_t)(k & 7) * 2u;
+}
+
+// stacked P rows: dd rows in lane quarters 0-1, hh rows in 2-3; within a
+// quarter, chunk rows 8g..8g+7 as hi (8 rows) then lo (8 rows), so a hi row
+// and its lo row sit 8 lanes apart in one warp and GEMM3 pairs them with the
+// same 8 feature rows (LBO 0)
+GMF_HD int stack_hi(int r) { return 32 * (r >> 4) + 16 * ((r >> 3) & 1) + (r & 7); }
 
 GMF_D uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -291,23 +305,21 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const int ncv = ncv64 < 0 ? 0 : (ncv64 > TCC ? TCC : (int)ncv64);   // valid tile columns
   const Smem L = smem_layout(NK);
   const int nka = L.nka;
-  const uint32_t sbo1 = (uint32_t)(nka / 8) * 128u;
+  const uint32_t sbo1 = (uint32_t)(nka / 8) * 128u;   // B1
+  const uint32_t sboc = (uint32_t)(nka / 16) * 512u;  // A1 (hi | lo)
   const uint32_t sb = smem_addr(smem);
 
   unsigned char* Pb = smem + L.P;
   unsigned char* Rb = smem + L.R;
   unsigned char* B1h = smem + L.B1h;
   unsigned char* B1l = smem + L.B1l;
-  unsigned char* A1h = smem + L.A1h;
-  unsigned char* A1l = smem + L.A1l;
-  unsigned char* Ash = smem + L.Ash;
-  unsigned char* Asl = smem + L.Asl;
+  unsigned char* A1b = smem + L.A1;
+  unsigned char* Asb = smem + L.As;
   int32_t* Y = reinterpret_cast<int32_t*>(smem + L.Y);
   unsigned char* st = smem + L.stage;
   T* araw = reinterpret_cast<T*>(smem + L.araw);
   T* off_s = reinterpret_cast<T*>(smem + L.off);
   int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
-  float* scr = reinterpret_cast<float*>(smem + L.scr);   // [2][32][17]
 
   const T* th_row = tptr<T>(P.th_row);
   const T* th_col = tptr<T>(P.th_col);
@@ -452,7 +464,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const uint32_t tm = X.tmem;
   constexpr uint32_t ID1 = idesc(128, 128, 0, 0);
   constexpr uint32_t ID2 = idesc(128, 64, 0, 0);
-  const uint32_t ID3 = idesc(128, nka, 1, 1);
+  constexpr uint32_t ID3 = idesc(128, 32, 1, 1);
   const int c0 = 32 * qd + 16 * hf;                 // this thread's first tile column
   const int vcols = ncv - c0 < 0 ? 0 : (ncv - c0 > 16 ? 16 : ncv - c0);
   const uint32_t lane_base = (uint32_t)(32 * qd) << 16;
@@ -462,30 +474,27 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   // A1 task of this thread: (replica, row, 8-feature group)
   const int a_rep = tid / (TRC * 2), a_rr = (tid / 2) % TRC, a_g2 = tid & 1;
 
-  // D2 readout (warps 0-3; quarter 0 = dd_hi rows, 1 = hh_hi, 2 = dd_lo,
-  // 3 = hh_lo); hi and lo halves combined through shared memory under a
-  // 128-thread named barrier
+  // D2 readout (warps 0-3): quarters 0-1 hold dd rows, 2-3 hh rows (stack_hi);
+  // each lane adds its Rd_hi and Rd_lo halves, then its hi/lo partner 8
+  // lanes away; the hi lane writes the row's Kr values
   auto readout_d2 = [&](int64_t rowbase, int rows) {
     float dv[16];
     uint32_t a[16], b[16];
-    const uint32_t col = tm + lane_base + T_D2 + ((qd & 1) ? 32u : 0u);
+    const uint32_t col = tm + lane_base + T_D2 + (qd >= 2 ? 32u : 0u);
     tmem_ld16(col, a);
     tmem_ld16(col + 16, b);
     #pragma unroll
-    for (int k = 0; k < 16; ++k) dv[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
-    if (qd >= 2) {
-      #pragma unroll
-      for (int k = 0; k < 16; ++k) scr[((qd - 2) * 32 + lane) * 17 + k] = dv[k];
+    for (int k = 0; k < 16; ++k) {
+      dv[k] = __uint_as_float(a[k]) + __uint_as_float(b[k]);
+      dv[k] += __shfl_xor_sync(0xffffffffu, dv[k], 8);
     }
-    fence_before();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (qd < 2 && lane < rows) {
-      T* outp = rowpart + ((int64_t)ct * P.nstar_max + rowbase + lane) * rkk + (qd == 0 ? 0 : Kr);
+    const int r = 16 * (qd & 1) + 8 * (lane >> 4) + (lane & 7);
+    if (!(lane & 8) && r < rows) {
+      T* outp = rowpart + ((int64_t)ct * P.nstar_max + rowbase + r) * rkk + (qd < 2 ? 0 : Kr);
       #pragma unroll
       for (int k = 0; k < 16; ++k)
-        if (k < Kr) outp[k] = dv[k] + scr[(qd * 32 + lane) * 17 + k];
+        if (k < Kr) outp[k] = dv[k];
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");   // scratch reused by the next readout
   };
 
   int64_t prev_rowbase = -1;
@@ -555,12 +564,12 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         }
         uint4 h, l;
         split8(v, h, l);
-        *reinterpret_cast<uint4*>(A1h + kofs(32 * a_rep + a_rr, 8 * g, sbo1)) = h;
-        *reinterpret_cast<uint4*>(A1l + kofs(32 * a_rep + a_rr, 8 * g, sbo1)) = l;
-        if (a_rep == 0) {
+        *reinterpret_cast<uint4*>(A1b + a1ofs(32 * a_rep + a_rr, 8 * g, 0, sboc)) = h;
+        *reinterpret_cast<uint4*>(A1b + a1ofs(32 * a_rep + a_rr, 8 * g, 1, sboc)) = l;
+        if (a_rep == 0 && g < 2) {   // squares of features 0..15 (the column side's [x | u])
           split8(v2, h, l);
-          *reinterpret_cast<uint4*>(Ash + kofs(a_rr, 8 * g, sbo1)) = h;
-          *reinterpret_cast<uint4*>(Asl + kofs(a_rr, 8 * g, sbo1)) = l;
+          *reinterpret_cast<uint4*>(Asb + a1ofs(a_rr, 8 * g, 0, 512u)) = h;
+          *reinterpret_cast<uint4*>(Asb + a1ofs(a_rr, 8 * g, 1, 512u)) = l;
         }
       }
     }
@@ -574,8 +583,8 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       fence_after();
       for (int kt = 0; kt < nka / 16; ++kt) {
         const uint32_t ko = (uint32_t)kt * 256u;
-        const uint64_t ah = sdesc(sb + (uint32_t)L.A1h + ko, 128, sbo1);
-        const uint64_t al = sdesc(sb + (uint32_t)L.A1l + ko, 128, sbo1);
+        const uint64_t ah = sdesc(sb + (uint32_t)L.A1 + (uint32_t)kt * 512u, 128, sboc);
+        const uint64_t al = sdesc(sb + (uint32_t)L.A1 + (uint32_t)kt * 512u + 256u, 128, sboc);
         const uint64_t bh = sdesc(sb + (uint32_t)L.B1h + ko, 128, sbo1);
         const uint64_t bl = sdesc(sb + (uint32_t)L.B1l + ko, 128, sbo1);
         umma(tm + T_ETA, ah, bh, ID1, kt > 0 ? 1u : 0u);
@@ -623,8 +632,8 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     }
     nb_num += (double)cn;
     nb_den += (double)cdn;
-    put_split16(dd, Pb, lane, 64 + lane, c0);
-    put_split16(hh, Pb, 32 + lane, 96 + lane, c0);
+    put_split16(dd, Pb, stack_hi(lane), stack_hi(lane) + 8, c0);
+    put_split16(hh, Pb, 64 + stack_hi(lane), 64 + stack_hi(lane) + 8, c0);
     if (csr) {
       const int4 z4 = make_int4(0, 0, 0, 0);
       #pragma unroll
@@ -643,20 +652,17 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         umma(tm + T_D2, sdesc(sb + (uint32_t)L.P + ko, 128, SBO_P),
              sdesc(sb + (uint32_t)L.R + ko, 128, SBO_P), ID2, kt > 0 ? 1u : 0u);
       }
-      // D3[col][k] += P^T . A1 (dd) and P^T . A1^2 (hh): P read MN-major
-      // (column chunks +128 B, 8-row K groups +2048 B), A1 read MN-major
-      // (feature chunks +128 B, 8-row K groups +sbo1); K = chunk rows 0-15, 16-31
+      // D3[col][f] += P^T . [a_hi | a_lo] (dd) and P^T . [a2_hi | a2_lo] (hh),
+      // features 0..15; K-step u = stacked rows 16u..16u+15 = chunk rows
+      // 8u..8u+7 hi then lo, paired with feature rows 8u..8u+7 twice (LBO 0).
+      // P read MN-major (column chunks +128 B, 8-row K groups +2048 B).
       #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t pa = (u & 2 ? 16384u : 0u) + (u & 1) * 4096u;   // dd_hi / dd_lo rows
-        const uint32_t bo = (uint32_t)(u & 1) * 2u * sbo1;               // chunk rows 0 / 16
         const uint32_t acc0 = (first3 && u == 0) ? 0u : 1u;
-        const uint64_t pd = sdesc(sb + (uint32_t)L.P + pa, 2048, 128);
-        const uint64_t ph = sdesc(sb + (uint32_t)L.P + pa + 8192u, 2048, 128);
-        umma(tm + T_D3, pd, sdesc(sb + (uint32_t)L.A1h + bo, sbo1, 128), ID3, acc0);
-        umma(tm + T_D3, pd, sdesc(sb + (uint32_t)L.A1l + bo, sbo1, 128), ID3, 1u);
-        umma(tm + T_D3 + nka, ph, sdesc(sb + (uint32_t)L.Ash + bo, sbo1, 128), ID3, acc0);
-        umma(tm + T_D3 + nka, ph, sdesc(sb + (uint32_t)L.Asl + bo, sbo1, 128), ID3, 1u);
+        umma(tm + T_D3, sdesc(sb + (uint32_t)L.P + 4096u * u, 2048, 128),
+             sdesc(sb + (uint32_t)L.A1 + sboc * u, 0, 128), ID3, acc0);
+        umma(tm + T_D3 + 32, sdesc(sb + (uint32_t)L.P + 16384u + 4096u * u, 2048, 128),
+             sdesc(sb + (uint32_t)L.As + 512u * u, 0, 128), ID3, acc0);
       }
       umma_commit(&X.bar[1]);
     }
@@ -674,14 +680,15 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   {
     // lane = tile column; D3 columns = a-features [x | u | gamma], whose first
     // Kc are the column side's [x | u]
-    uint32_t a[16];
-    const uint32_t col = tm + lane_base + T_D3 + (hf ? (uint32_t)nka : 0u);
+    uint32_t a[16], b[16];
+    const uint32_t col = tm + lane_base + T_D3 + (hf ? 32u : 0u);
     const int c = 32 * qd + lane;
     T* outp = colpart + cpb + (int64_t)c * (2 * Kc) + (hf ? Kc : 0);
     tmem_ld16(col, a);
+    tmem_ld16(col + 16, b);
     #pragma unroll
     for (int f = 0; f < 16; ++f)
-      if (f < Kc) outp[f] = __uint_as_float(a[f]);
+      if (f < Kc) outp[f] = __uint_as_float(a[f]) + __uint_as_float(b[f]);
   }
   fence_before();
   const double bn = block_sum<kThreads>(nb_num, red_scr);

@@ -163,6 +163,7 @@ int main() {
       {M, N, 1, {0, 0, 128, 256}, {1, 0, 1024, 128}},       // bf16 B MN-major none
       {M, N, 1, {1, 2, 1024, 2048}, {0, 0, 128, 256}},      // bf16 A MN-major SW128
       {M, N, 1, {1, 0, 128, 2048}, {0, 0, 128, 256}},       // bf16 A MN-major none, swapped
+      {M, N, 1, {1, 0, 2048, 128}, {1, 0, 0, 128}},         // bf16 B MN-major, LBO 0 (K groups alias)
   };
   for (auto& cs : cases) {
     const int K = cs.bf ? 16 : 8;
@@ -170,6 +171,9 @@ int main() {
       for (int k = 0; k < K; ++k) hA[r * K + k] = (float)((r * 7 + k * 3) % 17 - 8);
     for (int n = 0; n < N; ++n)
       for (int k = 0; k < K; ++k) hB[n * K + k] = (float)((n * 5 + k * 11) % 13 - 6);
+    if (cs.b.mn && cs.b.lbo == 0)   // aliased K groups: B[n][k] == B[n][k % 8]
+      for (int n = 0; n < N; ++n)
+        for (int k = 8; k < K; ++k) hB[n * K + k] = hB[n * K + k - 8];
     for (int r = 0; r < M; ++r)
       for (int n = 0; n < N; ++n) {
         float s = 0;
