@@ -14,7 +14,7 @@ namespace gmf {
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha);
 int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
-                 int* fit_blocks_per_sm);
+                 int fit_extra_smem, int* fit_blocks_per_sm);
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
@@ -101,6 +101,7 @@ int residency_probe(gmf_handle* h, cudaStream_t st) {
     GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->desc.device));
     h->fit_grid = (n_sm / P.CT) * P.CT;
     h->fit_rs = h->fit_grid / P.CT;
+    h->P.ep_cap = 0;   // sized for the larger grid
     if (getenv("GMF_VERBOSE"))
       fprintf(stderr, "[gmf] fit kernel CTAs not co-resident; %d CTAs (one per SM)\n", h->fit_grid);
   }
@@ -217,8 +218,29 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
 
   // persistent kernel geometry: every co-resident CTA, a multiple of CT
   int fit_bps = 0;
-  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, &fit_bps);
+  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, 0, &fit_bps);
   if (rc) { delete h; return rc; }
+  {
+    // cache each fit CTA's tracked entries in shared memory when that keeps
+    // the same number of CTAs per SM
+    int n_sm0 = kSMs;
+    GMF_CUDA(cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, desc->device));
+    const int grid0 = P.CT > 0 ? (fit_bps * n_sm0 / P.CT) * P.CT : 0;   // = fit_grid below
+    const int64_t cap = grid0 > 0 ? (bufs->n_eval + grid0 - 1) / grid0 : 0;
+    if (cap > 0 && cap <= 1024) {
+      int bps2 = 0;
+      rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm,
+                        (int)(cap * 16), &bps2);
+      if (rc) { delete h; return rc; }
+      if (bps2 == fit_bps) {
+        P.ep_cap = (int)cap;
+        P.ep_soff = grad_smem_bytes(desc->dtype, h->NK, P.has_w, Kr, Kc, P.tcm);
+      } else {
+        rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, 0, &bps2);
+        if (rc) { delete h; return rc; }
+      }
+    }
+  }
   int n_sm = kSMs;
   GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
   int coop = 0;

@@ -75,6 +75,8 @@ struct Params {
   double nbfloor, nbceil, escale, phi;
   int est_alpha, snap_stride, world;
   int tcm;             // K1 on the tensor cores (gmf_tc.cuh)
+  int ep_cap;          // tracked entries cached per fit CTA in shared memory (0 = none)
+  int64_t ep_soff;     // their shared-memory offset (bytes, after K1's region)
   const double* rho_tab;     // learning_rate(t)        (optim.py:130-134)
   const double* alpt_tab;    // bias_correction(t + 1)  (optim.py:142-148)
   // workspace

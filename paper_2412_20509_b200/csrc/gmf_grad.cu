@@ -86,50 +86,71 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
 // persistent fit kernel (single rank)
 // ---------------------------------------------------------------------------
 
-// this CTA's share of the tracked-sample deviance, predictor in fp64 from
-// unrolled feature loads (all gathers of an entry in flight together)
+// tracked objective (optim.py:283-290): deviance of the fixed eval sample
+// this CTA's share of the tracked-sample deviance over entries ents[0, n)
+// (shared-memory cache or global).  Four lanes cooperate on one entry: lane k
+// loads features k, k+4, ... of u_i, v_j and the covariate pairs, so each warp
+// load touches 8 entries' contiguous runs instead of 32 scattered words; the
+// predictor is reduced over the 4 lanes (fixed xor order) and lane 0 of the
+// group evaluates the deviance.  Two groups of entries are in flight per lane.
 template <typename T, int NK>
-GMF_D double obj_dev_partial(const Params& P, double alpha, int64_t first, int64_t stride) {
+GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, int64_t n) {
+  constexpr int MU = (NK + 3) / 4;                         // features per lane
+  constexpr int RB = 2;                                    // rounds in flight
   const T* tr = tptr<T>(P.th_row);
   const T* tc = tptr<T>(P.th_col);
   const T* xg = tptr<T>(P.x);
   const T* zg = tptr<T>(P.z);
   const T* wg = tptr<T>(P.w);
-  const int p = P.p, q = P.q, d = P.d, Kr = P.Kr, Kc = P.Kc;
   const T* offg = tptr<T>(P.off);
+  const int p = P.p, q = P.q, d = P.d, Kr = P.Kr, Kc = P.Kc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, k = lane & 3, g = lane >> 2;
+  const int64_t per_round = (int64_t)(kThreads / 32) * 8;   // entries per CTA round
   double s = 0.0;
-  // every gather of an entry in flight before any math (branch-free bounds)
-  constexpr int W = 4;   // covariate widths p, q handled 4 at a time
-  for (int64_t e = first; e < P.E; e += stride) {
-    const int4 en = P.ep[e];
-    const int64_t i = en.x, j = en.y;
-    T uu[NK], vv[NK];
-    gather_vec<NK>(tr + i * Kr + q, d, uu);
-    gather_vec<NK>(tc + j * Kc + p, d, vv);
-    const T of = P.has_off ? offg[i] : T(0);
-    const T wv = P.has_w ? wg[i * P.m + j] : T(1);
-    double eta = (double)of;
-    for (int k0 = 0; k0 < p; k0 += W) {
-      T xb[W], bb[W];
-      gather_vec<W>(xg + i * p + k0, p - k0, xb);
-      gather_vec<W>(tc + j * Kc + k0, p - k0, bb);
+  for (int64_t base = (int64_t)warp * 8; base < n; base += RB * per_round) {
+    // every load of RB rounds issued before any math
+    T uu[RB][MU], vv[RB][MU], cx[RB], cb[RB];
+    int4 en[RB];
+    #pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int64_t e = base + r * per_round + g;
+      en[r] = ents[e < n ? e : 0];
+      const int64_t i = en[r].x, j = en[r].y;
+      const T* ur = tr + i * Kr + q;
+      const T* vr = tc + j * Kc + p;
       #pragma unroll
-      for (int k = 0; k < W; ++k) eta += (double)xb[k] * (double)bb[k];
-    }
-    for (int k0 = 0; k0 < q; k0 += W) {
-      T gg[W], zz[W];
-      gather_vec<W>(tr + i * Kr + k0, q - k0, gg);
-      gather_vec<W>(zg + j * q + k0, q - k0, zz);
-      #pragma unroll
-      for (int k = 0; k < W; ++k) eta += (double)gg[k] * (double)zz[k];
+      for (int m = 0; m < MU; ++m) {
+        const int f = k + 4 * m;
+        const bool ok = f < d;
+        const T a = ur[ok ? f : 0], b = vr[ok ? f : 0];
+        uu[r][m] = ok ? a : T(0);
+        vv[r][m] = ok ? b : T(0);
+      }
+      const bool okx = k < p;   // first covariate pair in the same batch
+      const T a = xg[okx ? i * p + k : 0], b = tc[okx ? j * Kc + k : 0];
+      cx[r] = okx ? a : T(0);
+      cb[r] = okx ? b : T(0);
     }
     #pragma unroll
-    for (int k = 0; k < NK; ++k) eta += (double)uu[k] * (double)vv[k];
-    if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
-      s += (double)wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta),
-                                                (float)alpha);
-    else
-      s += (double)wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
+    for (int r = 0; r < RB; ++r) {
+      const int64_t e = base + r * per_round + g;
+      const int64_t i = en[r].x, j = en[r].y;
+      double eta = (double)cx[r] * (double)cb[r];
+      for (int f = k + 4; f < p; f += 4) eta += (double)xg[i * p + f] * (double)tc[j * Kc + f];
+      for (int f = k; f < q; f += 4) eta += (double)tr[i * Kr + f] * (double)zg[j * q + f];
+      #pragma unroll
+      for (int m = 0; m < MU; ++m) eta += (double)uu[r][m] * (double)vv[r][m];
+      eta += __shfl_xor_sync(0xffffffffu, eta, 1);
+      eta += __shfl_xor_sync(0xffffffffu, eta, 2);
+      if (k == 0 && e < n) {
+        eta += P.has_off ? (double)offg[i] : 0.0;
+        const double wv = P.has_w ? (double)wg[i * P.m + j] : 1.0;
+        if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
+          s += wv * (double)unit_deviance_f(P.fam, (float)en[r].z, __expf((float)eta), (float)alpha);
+        else
+          s += wv * unit_deviance(P.fam, (double)en[r].z, exp(eta), alpha);
+      }
+    }
   }
   return s;
 }
@@ -239,6 +260,17 @@ k_fit(Params P, long long n_steps) {
     if (threadIdx.x == 0) { P.cnpart[2 * blockIdx.x] = v[0]; P.cnpart[2 * blockIdx.x + 1] = v[1]; }
   }
 
+  // this CTA's tracked entries (static for the whole fit) cached in shared memory
+  const bool ep_cached = P.ep_cap > 0;
+  const int4* ep_src = P.ep;
+  if (ep_cached) {
+    int4* ep_s = reinterpret_cast<int4*>(smem + P.ep_soff);
+    const int64_t per = (P.E + G - 1) / G;
+    const int64_t lo = per * blockIdx.x, hi = lo + per < P.E ? lo + per : P.E;
+    for (int64_t e = threadIdx.x; e < hi - lo; e += kThreads) ep_s[e] = P.ep[lo + e];
+    __syncthreads();
+    ep_src = ep_s;
+  }
   const bool prof = P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   // per-CTA stamps of the last profiled step (block-uniform condition)
   const bool profc = P.prof != nullptr;
@@ -265,13 +297,16 @@ k_fit(Params P, long long n_steps) {
       const int64_t per = (P.E + G - 1) / G;
       const int64_t lo = per * blockIdx.x, hi = lo + per < P.E ? lo + per : P.E;
       double v[1] = {0.0};
-      {
-        Params Q = P;
-        Q.E = hi;
-        v[0] = obj_dev_partial<T, NK>(Q, C.nb_shape, lo + threadIdx.x, kThreads);
-      }
+      const long long c0 = profc ? clock64() : 0;
+      v[0] = obj_dev_partial<T, NK>(P, C.nb_shape, ep_src + (ep_cached ? 0 : lo),
+                                    hi > lo ? hi - lo : 0);
+      const long long c1 = profc ? clock64() : 0;
       block_sum_vec<1>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
+      if (profc && threadIdx.x == 0) {   // objective sub-phases (SM clocks): loop, reduction
+        P.prof[16 + 16 * blockIdx.x + 5] += (unsigned long long)(c1 - c0);
+        P.prof[16 + 16 * blockIdx.x + 6] += (unsigned long long)(clock64() - c1);
+      }
     }
     if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
@@ -514,12 +549,13 @@ int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm) {
 // opt in to >48 KB dynamic shared memory (outside any graph capture) and
 // report how many k_fit CTAs can be co-resident per SM
 int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
-                 int* fit_blocks_per_sm) {
+                 int fit_extra_smem, int* fit_blocks_per_sm) {
   void* g = kernel_for(dtype, family, NK, false, tcm);
   void* f = kernel_for(dtype, family, NK, true, tcm);
   if (!g || !f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const int smem = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc, tcm);
-  GMF_CUDA(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int smem_g = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc, tcm);
+  const int smem = smem_g + fit_extra_smem;
+  GMF_CUDA(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g));
   GMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nb = 0;
   GMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem));
@@ -569,7 +605,8 @@ int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long x
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st) {
   void* f = kernel_for(dtype, P.fam, NK, true, P.tcm);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm);
+  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm) +
+                     (size_t)P.ep_cap * sizeof(int4);
   void* args[] = {(void*)&P, (void*)&n_steps};
   if (P.tcm) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
     GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 4 * sizeof(unsigned int), st));
