@@ -3,6 +3,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <vector>
 
@@ -281,6 +282,12 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
   const int64_t o_gbar = take(16);
+  const int64_t E1 = bufs->n_eval > 0 ? bufs->n_eval : 1;
+  const int64_t o_esr = take(E1 * 8);                          // eval rows, sorted
+  const int64_t o_esc = take(E1 * 4);                          // eval cols, same order
+  const int64_t o_rfi = take((desc->n + 1) * 4);               // entries per row
+  const int64_t o_ecache = take(E1 * (h->NK + 4) * h->tsz);    // objective row cache
+  const int64_t o_vpad = take(desc->m * h->NK * h->tsz);       // padded column features
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -304,6 +311,35 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   h->full_part = (double*)(base + o_fp);
   h->full_ticket = (unsigned int*)(base + o_ft);
   GMF_CUDA(cudaMemset(h->ws, 0, off));
+  P.rfirst = (const int32_t*)(base + o_rfi);
+  P.ecache = base + o_ecache;
+  P.vpad = base + o_vpad;
+  if (bufs->n_eval > 0) {
+    // the tracked sample sorted by (block-major) row, with each row's first
+    // entry: phase 2 writes an updated row straight into its entries' cache
+    // rows (the objective is an order-free sum)
+    const int64_t E = bufs->n_eval;
+    std::vector<int64_t> er(E), ers(E);
+    std::vector<int32_t> ec(E), ecs(E);
+    GMF_CUDA(cudaMemcpy(er.data(), bufs->eval_row, E * 8, cudaMemcpyDeviceToHost));
+    GMF_CUDA(cudaMemcpy(ec.data(), bufs->eval_col, E * 4, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> idx(E);
+    for (int64_t k = 0; k < E; ++k) idx[k] = k;
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return er[a] < er[b]; });
+    for (int64_t k = 0; k < E; ++k) { ers[k] = er[idx[k]]; ecs[k] = ec[idx[k]]; }
+    if (E >= (int64_t)1 << 31) { set_error("more than 2^31 tracked entries"); gmf_destroy(h); return GMF_ERR_CONFIG; }
+    std::vector<int32_t> rfi(desc->n + 1);
+    int64_t f = 0;
+    for (int64_t i = 0; i <= desc->n; ++i) {
+      while (f < E && ers[f] < i) ++f;
+      rfi[i] = (int32_t)f;
+    }
+    GMF_CUDA(cudaMemcpy(base + o_esr, ers.data(), E * 8, cudaMemcpyHostToDevice));
+    GMF_CUDA(cudaMemcpy(base + o_esc, ecs.data(), E * 4, cudaMemcpyHostToDevice));
+    GMF_CUDA(cudaMemcpy(base + o_rfi, rfi.data(), (desc->n + 1) * 4, cudaMemcpyHostToDevice));
+    P.erow = (const int64_t*)(base + o_esr);
+    P.ecol = (const int32_t*)(base + o_esc);
+  }
   P.ep = (const int4*)(base + o_ep);
   if (bufs->n_eval > 0) {   // tracked sample packed with its Y, once per fit
     rc = launch_eval_pack(P, (int4*)(base + o_ep), 0);

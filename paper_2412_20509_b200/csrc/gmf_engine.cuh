@@ -77,6 +77,10 @@ struct Params {
   int tcm;             // K1 on the tensor cores (gmf_tc.cuh)
   int ep_cap;          // tracked entries cached per fit CTA in shared memory (0 = none)
   int64_t ep_soff;     // their shared-memory offset (bytes, after K1's region)
+  // tracked-objective caches of the persistent kernel (entries sorted by row):
+  const int32_t* rfirst; // [n+1] entries of row i: [rfirst[i], rfirst[i+1])
+  void* ecache;          // [E][NK+4] T: a_i = [x | u | gamma | 0..] then offset_i
+  void* vpad;            // [m][NK]   T: c_j = [b | v | z | 0..] (16-byte rows)
   const double* rho_tab;     // learning_rate(t)        (optim.py:130-134)
   const double* alpt_tab;    // bias_correction(t + 1)  (optim.py:142-148)
   // workspace

@@ -86,71 +86,60 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
 // persistent fit kernel (single rank)
 // ---------------------------------------------------------------------------
 
-// tracked objective (optim.py:283-290): deviance of the fixed eval sample
-// this CTA's share of the tracked-sample deviance over entries ents[0, n)
-// (shared-memory cache or global).  Four lanes cooperate on one entry: lane k
-// loads features k, k+4, ... of u_i, v_j and the covariate pairs, so each warp
-// load touches 8 entries' contiguous runs instead of 32 scattered words; the
-// predictor is reduced over the 4 lanes (fixed xor order) and lane 0 of the
-// group evaluates the deviance.  Two groups of entries are in flight per lane.
+// tracked objective of the persistent kernel (optim.py:283-290).  The
+// sample is fixed and sorted by row, so each entry keeps its row's features
+// in a cache row a_i = [x | u | gamma | 0 | offset] and the columns'
+// [b | v | z] sit in 16-byte padded rows; phase 2 writes both together with
+// theta (row i's entries are [rfirst[i], rfirst[i+1])), so eta is a few
+// 16-byte loads per entry instead of ~2K scattered words.  fp64 predictor,
+// fixed order.
 template <typename T, int NK>
-GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, int64_t n) {
-  constexpr int MU = (NK + 3) / 4;                         // features per lane
-  constexpr int RB = 2;                                    // rounds in flight
-  const T* tr = tptr<T>(P.th_row);
-  const T* tc = tptr<T>(P.th_col);
-  const T* xg = tptr<T>(P.x);
-  const T* zg = tptr<T>(P.z);
-  const T* wg = tptr<T>(P.w);
-  const T* offg = tptr<T>(P.off);
-  const int p = P.p, q = P.q, d = P.d, Kr = P.Kr, Kc = P.Kc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, k = lane & 3, g = lane >> 2;
-  const int64_t per_round = (int64_t)(kThreads / 32) * 8;   // entries per CTA round
+GMF_D void ecache_fill(const Params& P, int64_t e, int64_t i) {
+  T* row = tptr<T>(P.ecache) + e * (NK + 4);
+  const T* th = tptr<T>(P.th_row) + i * P.Kr;
+  const T* xg = tptr<T>(P.x) + i * P.p;
+  const int p = P.p, d = P.d, KA = P.KA, q = P.q;
+  #pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    T v = T(0);
+    if (k < p) v = xg[k];
+    else if (k < p + d) v = th[q + (k - p)];
+    else if (k < KA) v = th[k - p - d];
+    row[k] = v;
+  }
+  row[NK] = P.has_off ? tptr<T>(P.off)[i] : T(0);
+  row[NK + 1] = T(0); row[NK + 2] = T(0); row[NK + 3] = T(0);
+}
+
+template <typename T>
+struct Vec16;   // 16-byte vector of T
+template <> struct Vec16<float> { using V = float4; static constexpr int N = 4; };
+template <> struct Vec16<double> { using V = double2; static constexpr int N = 2; };
+
+template <typename T, int NK>
+GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, int64_t lo,
+                             int64_t hi) {
+  using V = typename Vec16<T>::V;
+  constexpr int VN = Vec16<T>::N;
   double s = 0.0;
-  for (int64_t base = (int64_t)warp * 8; base < n; base += RB * per_round) {
-    // every load of RB rounds issued before any math
-    T uu[RB][MU], vv[RB][MU], cx[RB], cb[RB];
-    int4 en[RB];
+  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+    const int4 en = ents[e - lo];
+    const int64_t i = en.x, j = en.y;
+    const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + e * (NK + 4));
+    const V* c = reinterpret_cast<const V*>(tptr<T>(P.vpad) + j * NK);
+    T av[NK + 4], cv[NK];
     #pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int64_t e = base + r * per_round + g;
-      en[r] = ents[e < n ? e : 0];
-      const int64_t i = en[r].x, j = en[r].y;
-      const T* ur = tr + i * Kr + q;
-      const T* vr = tc + j * Kc + p;
-      #pragma unroll
-      for (int m = 0; m < MU; ++m) {
-        const int f = k + 4 * m;
-        const bool ok = f < d;
-        const T a = ur[ok ? f : 0], b = vr[ok ? f : 0];
-        uu[r][m] = ok ? a : T(0);
-        vv[r][m] = ok ? b : T(0);
-      }
-      const bool okx = k < p;   // first covariate pair in the same batch
-      const T a = xg[okx ? i * p + k : 0], b = tc[okx ? j * Kc + k : 0];
-      cx[r] = okx ? a : T(0);
-      cb[r] = okx ? b : T(0);
-    }
+    for (int u = 0; u < (NK + 4) / VN; ++u) *reinterpret_cast<V*>(av + VN * u) = a[u];
     #pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int64_t e = base + r * per_round + g;
-      const int64_t i = en[r].x, j = en[r].y;
-      double eta = (double)cx[r] * (double)cb[r];
-      for (int f = k + 4; f < p; f += 4) eta += (double)xg[i * p + f] * (double)tc[j * Kc + f];
-      for (int f = k; f < q; f += 4) eta += (double)tr[i * Kr + f] * (double)zg[j * q + f];
-      #pragma unroll
-      for (int m = 0; m < MU; ++m) eta += (double)uu[r][m] * (double)vv[r][m];
-      eta += __shfl_xor_sync(0xffffffffu, eta, 1);
-      eta += __shfl_xor_sync(0xffffffffu, eta, 2);
-      if (k == 0 && e < n) {
-        eta += P.has_off ? (double)offg[i] : 0.0;
-        const double wv = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-        if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
-          s += wv * (double)unit_deviance_f(P.fam, (float)en[r].z, __expf((float)eta), (float)alpha);
-        else
-          s += wv * unit_deviance(P.fam, (double)en[r].z, exp(eta), alpha);
-      }
-    }
+    for (int u = 0; u < NK / VN; ++u) *reinterpret_cast<V*>(cv + VN * u) = __ldcg(c + u);
+    double eta = (double)av[NK];
+    #pragma unroll
+    for (int k = 0; k < NK; ++k) eta += (double)av[k] * (double)cv[k];
+    const double wv = P.has_w ? (double)tptr<T>(P.w)[i * P.m + j] : 1.0;
+    if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
+      s += wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta), (float)alpha);
+    else
+      s += wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
   }
   return s;
 }
@@ -271,6 +260,25 @@ k_fit(Params P, long long n_steps) {
     __syncthreads();
     ep_src = ep_s;
   }
+  const int64_t e_per = (P.E + G - 1) / G;
+  const int64_t e_lo = e_per * blockIdx.x < P.E ? e_per * blockIdx.x : P.E;
+  const int64_t e_hi = e_lo + e_per < P.E ? e_lo + e_per : P.E;
+  {
+    // objective caches: this CTA's entry rows, every column's padded features
+    for (int64_t e = e_lo + threadIdx.x; e < e_hi; e += kThreads)
+      ecache_fill<T, NK>(P, e, (int64_t)ep_src[e - e_lo + (ep_cached ? 0 : e_lo)].x);
+    const T* tc = tptr<T>(P.th_col);
+    const T* zg = tptr<T>(P.z);
+    for (int64_t e = gtid; e < P.m * NK; e += gstride) {
+      const int64_t j = e / NK;
+      const int k = (int)(e % NK);
+      T v = T(0);
+      if (k < Kc) v = tc[j * Kc + k];
+      else if (k < P.KA) v = zg[j * P.q + (k - Kc)];
+      tptr<T>(P.vpad)[e] = v;
+    }
+    if (!gsync(kBarrierTimeoutNs)) n_steps = 0;   // vpad complete before the first objective
+  }
   const bool prof = P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   // per-CTA stamps of the last profiled step (block-uniform condition)
   const bool profc = P.prof != nullptr;
@@ -294,12 +302,9 @@ k_fit(Params P, long long n_steps) {
     }
     if (boundary) {
       // contiguous, equal entry ranges per CTA keep the objective balanced
-      const int64_t per = (P.E + G - 1) / G;
-      const int64_t lo = per * blockIdx.x, hi = lo + per < P.E ? lo + per : P.E;
       double v[1] = {0.0};
       const long long c0 = profc ? clock64() : 0;
-      v[0] = obj_dev_partial<T, NK>(P, C.nb_shape, ep_src + (ep_cached ? 0 : lo),
-                                    hi > lo ? hi - lo : 0);
+      v[0] = obj_dev_partial<T, NK>(P, C.nb_shape, ep_src + (ep_cached ? 0 : e_lo), e_lo, e_hi);
       const long long c1 = profc ? clock64() : 0;
       block_sum_vec<1>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
@@ -390,6 +395,12 @@ k_fit(Params P, long long n_steps) {
         tptr<T>(P.gb_row)[o] = gn;
         tptr<T>(P.hb_row)[o] = hn;
         tptr<T>(P.th_row)[o] = nvv;
+        {   // the objective's cache rows of this row's tracked entries
+          const int64_t i = rI0 + il;
+          const int apos = k < P.q ? P.p + P.d + k : P.p + (k - P.q);   // a = [x | u | gamma]
+          for (int32_t f = P.rfirst[i]; f < P.rfirst[i + 1]; ++f)
+            tptr<T>(P.ecache)[(int64_t)f * (NK + 4) + apos] = nvv;
+        }
         nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
       }
     }
@@ -441,6 +452,7 @@ k_fit(Params P, long long n_steps) {
           const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k,
                                       tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
                                       k < P.p ? P.lam_b : P.lam_v, rho, at);
+          tptr<T>(P.vpad)[j * NK + k] = nvv;   // the objective's padded copy of [b | v | z]
           nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
         }
       }
