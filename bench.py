@@ -127,22 +127,23 @@ def _dist():
     return ws, dist.get_rank(), lr, dist.group.WORLD
 
 
-def _k1_bytes(spec, nI, nnz_I, e):
+def _k1_bytes(spec, nI, nnz_I, e, nnz_bytes=8):
     """Algorithmic HBM bytes of one K1 launch: the block's
-    counts, row features and offset read once, column features read once,
-    row-side and column-side gradient partials written once."""
+    counts (nnz_bytes per stored nonzero: 8 CSR int32, 4 packed), row
+    features and offset read once, column features read once, row-side and
+    column-side gradient partials written once."""
     p, q, d, m = spec.p, spec.q, spec.d, spec.m
-    y = 8 * nnz_I + 8 * (nI + 1) if spec.y_format == "csr" else 4 * nI * m
+    y = nnz_bytes * nnz_I + 8 * (nI + 1) if spec.y_format == "csr" else 4 * nI * m
     rows = nI * e * (p + q + d + (1 if spec.offset else 0)) + nI * e * 2 * (q + d)
     cols = m * e * (p + q + d) + m * e * 2 * (p + d)
     return y + rows + cols
 
 
-def _step_bytes(spec, nI, nnz_I, e):
+def _step_bytes(spec, nI, nnz_I, e, nnz_bytes=8):
     """Algorithmic bytes of a whole step: K1 + the EMA/update
     traffic (read gbar, hbar, theta; write them back) of rows I and columns J."""
     kr, kc = spec.q + spec.d, spec.p + spec.d
-    return _k1_bytes(spec, nI, nnz_I, e) + nI * e * 6 * kr + spec.m * e * 6 * kc
+    return _k1_bytes(spec, nI, nnz_I, e, nnz_bytes) + nI * e * 6 * kr + spec.m * e * 6 * kc
 
 
 def _cpu_baseline(wl, steps, time_budget=25.0):
@@ -219,7 +220,7 @@ def _workload_desc(name):
         "c1": "c1: Poisson GMF 1,000 x 100, k=5, X=Z=1, dense int32, mb 100 rows x all columns, fp64",
         "c2": "c2: NB GMF 26,472 x 500, k=15, 7-group mixture, log-library offset, dense int32, mb 2,000 rows, fp64",
         "c3": "c3: NB GMF 100,000 x 1,000, k=10, X=[1,batch], Z=1, CSR int32 ~90% zeros, mb 5,000 rows, fp32",
-        "c4": "c4: NB GMF 1,300,000 x 500, k=10, intercept + log-library offset, CSR int32 ~92% zeros, mb 10,000 rows x all 500 columns, fp32",
+        "c4": "c4: NB GMF 1,300,000 x 500, k=10, intercept + log-library offset, CSR ~92% zeros, mb 10,000 rows x all 500 columns, fp32",
     }[name]
 
 
@@ -366,10 +367,11 @@ def main():
     avg = C.c_double()
     _lib.check(fit.lib.gmf_time_grad(fit.h, blk, 200, C.byref(avg), fit.stream()), "gmf_time_grad")
     k1_ms = avg.value
-    k1_bytes = _k1_bytes(workloads.WorkloadSpec(**{**sp.__dict__}), nI_loc, nnz_blk, e_sz)
+    nnzb = 4 if fit.y_format == "packed" else 8
+    k1_bytes = _k1_bytes(workloads.WorkloadSpec(**{**sp.__dict__}), nI_loc, nnz_blk, e_sz, nnzb)
     peak, peak_src = _peak_hbm()
     ms_step = ms / K
-    step_bytes = _step_bytes(sp, nI_loc, nnz_blk, e_sz)
+    step_bytes = _step_bytes(sp, nI_loc, nnz_blk, e_sz, nnzb)
     achieved = step_bytes / (ms_step / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(REPO, "profiles", f"kfit_traffic_{args.config}.json")
@@ -389,70 +391,65 @@ def main():
                                   "GB_s": k1_bytes / (k1_ms / 1e3) / 1e9}}
 
     # ---- e2e: stream each step's block from pinned host memory ----
-    # Every step's drawn row block (its CSR slice, or dense rows) is copied
-    # host -> device inside the timed region on a copy stream, one step ahead
-    # of the compute stream (double buffering in time: the copy of step k+1
-    # overlaps the fit kernel of step k); each step's status word is read back
-    # asynchronously.  Through the C ABI: gmf_run(1) per step.
+    # ONE persistent launch (C-ABI gmf_run_stream) runs the E steps; step t
+    # waits, before its gradient, for its drawn row block (CSR slice, or
+    # dense rows) to be copied host -> device on a copy stream, which then
+    # bumps the ready counter (gmf_stream_signal).  Each step's status word is
+    # written by the kernel into pinned host memory (device -> host per step).
     e2e = None
-    if E > 0:
+    if E > 0 and world == 1:
+        packed = fit.csr_ptr is not None and fit.csr_val is None
         if fit.csr_ptr is not None:
             h_col = fit.csr_col.cpu().pin_memory()
-            h_val = fit.csr_val.cpu().pin_memory()
+            h_val = None if packed else fit.csr_val.cpu().pin_memory()
             h_ptr = fit.csr_ptr.cpu().pin_memory()
             cptr = h_ptr.numpy()
         else:
             h_y = fit.y_dense.cpu().pin_memory()
-        raw = torch.empty(int(fit.lib.gmf_status_raw_bytes()), dtype=torch.uint8).pin_memory()
+        sbytes = int(fit.lib.gmf_status_raw_bytes())
+        status_h = torch.zeros(E * sbytes, dtype=torch.uint8).pin_memory()
         cs = torch.cuda.Stream(dev)
         main = torch.cuda.current_stream(dev)
-        copied = [torch.cuda.Event() for _ in range(E)]
-        h2d = [0]
-
-        def copy_block(k):
-            b = int(seq[W + K + K2 + k])
-            r0, r1 = int(rbp[b]), int(rbp[b + 1])
-            with torch.cuda.stream(cs):
-                if fit.csr_ptr is not None:
-                    a0, a1 = int(cptr[r0]), int(cptr[r1])
-                    fit.csr_col[a0:a1].copy_(h_col[a0:a1], non_blocking=True)
-                    fit.csr_val[a0:a1].copy_(h_val[a0:a1], non_blocking=True)
-                    fit.csr_ptr[r0:r1 + 1].copy_(h_ptr[r0:r1 + 1], non_blocking=True)
-                    h2d[0] += (a1 - a0) * 8 + (r1 - r0 + 1) * 8
-                else:
-                    fit.y_dense[r0:r1].copy_(h_y[r0:r1], non_blocking=True)
-                    h2d[0] += (r1 - r0) * sp.m * 4
-                copied[k].record(cs)
-
+        t_first = W + K + K2
+        h2d = 0
         barrier()
         launches0 = fit.launch_count()
         e0.record(main)
         cs.wait_event(e0)
-        copy_block(0)
-        for k in range(E):
-            if k + 1 < E:
-                copy_block(k + 1)          # next step's block, overlapping step k
-            main.wait_event(copied[k])
-            steps(1)
-            _lib.check(fit.lib.gmf_status_copy_async(fit.h, C.c_void_p(raw.data_ptr()),
-                                                     fit.stream()), "status copy")
+        fit.run_stream(E, status_h)
+        with torch.cuda.stream(cs):
+            for k in range(E):
+                b = int(seq[t_first + k])
+                r0, r1 = int(rbp[b]), int(rbp[b + 1])
+                if fit.csr_ptr is not None:
+                    a0, a1 = int(cptr[r0]), int(cptr[r1])
+                    fit.csr_col[a0:a1].copy_(h_col[a0:a1], non_blocking=True)
+                    if not packed:
+                        fit.csr_val[a0:a1].copy_(h_val[a0:a1], non_blocking=True)
+                    fit.csr_ptr[r0:r1 + 1].copy_(h_ptr[r0:r1 + 1], non_blocking=True)
+                    h2d += (a1 - a0) * (4 if packed else 8) + (r1 - r0 + 1) * 8
+                else:
+                    fit.y_dense[r0:r1].copy_(h_y[r0:r1], non_blocking=True)
+                    h2d += (r1 - r0) * sp.m * 4
+                fit.stream_signal(t_first + k + 1, cs)
+                h2d += 8
         e1.record(main)
         barrier()
         e_launches = fit.launch_count() - launches0
         e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            t_ = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t_, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(t_.item())
         st_e = _lib.GmfStatus()
-        fit.lib.gmf_status_decode(C.c_void_p(raw.data_ptr()), C.byref(st_e))
+        import ctypes as C
+        fit.lib.gmf_status_decode(C.c_void_p(status_h.data_ptr() + (E - 1) * sbytes), C.byref(st_e))
         assert st_e.t == W + K + K2 + E, st_e.t
-        e_entries = float(sizes[seq[W + K + K2:W + K + K2 + E]].sum()) * sp.m
+        assert fit.status().t == W + K + K2 + E
+        e_entries = float(sizes[seq[t_first:t_first + E]].sum()) * sp.m
         e2e = {"value": e_entries / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d[0] // E), "d2h_bytes_per_step": raw.numel(),
+               "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": sbytes,
                "steps": E, "ms_per_step": e_ms / E, "gpu_launches": int(e_launches),
-               "path": "C-ABI gmf_run(1) per step; the step's row block copied from pinned host "
-                       "memory on a copy stream one step ahead; async status read-back"}
+               "path": "C-ABI gmf_run_stream: one persistent launch; step t's row block copied from "
+                       "pinned host memory on a copy stream, then gmf_stream_signal(t+1); the kernel "
+                       "waits for the signal before step t's gradient and writes each step's status "
+                       "word to pinned host memory"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -470,9 +467,9 @@ def main():
                        "nnz": wl.meta.get("nnz"), "zero_frac": round(wl.meta.get("zero_frac", 0), 4),
                        "y_format": sp.y_format,
                        "l2": "inputs (CSR %.0f MB + factors) exceed the 126 MB L2; each step draws "
-                             "a random row block" % (wl.meta.get("nnz", 0) * 8 / 1e6),
+                             "a random row block" % (wl.meta.get("nnz", 0) * (4 if fit.y_format == "packed" else 8) / 1e6),
                        "parallelism": f"rows of each block split x{world}" if world > 1 else "1 GPU",
-                       "geometry": geometry, "k1_impl": fit.k1_impl},
+                       "geometry": geometry, "k1_impl": fit.k1_impl, "y_storage": fit.y_format},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(timed_launches), "clocks": clocks,
         }

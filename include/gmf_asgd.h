@@ -62,7 +62,10 @@ enum gmf_link {
   GMF_IDENTITY = 0, GMF_LOG = 1, GMF_LOGIT = 2, GMF_INVERSE = 3, GMF_INVERSE_SQUARED = 4
 };
 
-enum gmf_yfmt { GMF_Y_DENSE_I32 = 0, GMF_Y_CSR_I32 = 1 };
+/* Y formats: dense int32 n x m; CSR with int32 columns and counts; packed CSR
+ * with one uint32 per nonzero, (count << 16) | column, for m <= 65536 and
+ * counts <= 65535 (half the bytes of CSR_I32; csr_val unused) */
+enum gmf_yfmt { GMF_Y_DENSE_I32 = 0, GMF_Y_CSR_I32 = 1, GMF_Y_CSR_PACK32 = 2 };
 /* K1 (fused minibatch gradient) implementation: AUTO = tensor cores
  * (tcgen05, bf16-split operands) when eligible -- fp32, no prior weights,
  * q+d <= 16, p+d <= 16 -- else CUDA cores; TENSOR fails if ineligible. */
@@ -124,7 +127,7 @@ typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py
 typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
   const int32_t* y_dense;     /* n x m                          (DENSE_I32) */
   const int64_t* csr_ptr;     /* n + 1                          (CSR_I32)   */
-  const int32_t* csr_col;     /* nnz, sorted within a row                   */
+  const int32_t* csr_col;     /* nnz, sorted within a row (PACK32: packed)  */
   const int32_t* csr_val;     /* nnz                                        */
   const void* weights;        /* n x m or NULL                              */
   const void* x;              /* n x p                                      */
@@ -223,6 +226,20 @@ int64_t gmf_profile_len(gmf_handle* h);
 /* launch geometry: {persistent CTAs, its row splits, column tiles, tile
  * width, per-step-kernel row splits, feature bucket, K1 smem bytes, max |I|} */
 int gmf_geometry(gmf_handle* h, int64_t* out8);
+/* Streaming run (single rank, persistent kernel): ONE launch of n_steps
+ * steps in which step t (global index) waits, before its gradient, until the
+ * device counter at gmf_stream_ready_ptr(h) reaches t + 1 -- the caller
+ * uploads step t's row block (Y rows of the drawn block, in place) on another
+ * stream and then copies the value t + 1 into the counter.  After every step
+ * the status word (gmf_status_raw_bytes() bytes, decode with
+ * gmf_status_decode) is written to host_status[step of this launch]: mapped
+ * pinned host memory, or NULL.  A block that does not arrive within 10 s
+ * aborts the run (gmf_status_read reports it).  gmf_reset zeroes the counter. */
+void* gmf_stream_ready_ptr(gmf_handle* h);
+int gmf_run_stream(gmf_handle* h, int64_t n_steps, void* host_status, void* stream);
+/* enqueue "counter = value" on `stream` (H2D copy from handle-owned pinned
+ * memory), i.e. step value - 1's block is complete on that stream */
+int gmf_stream_signal(gmf_handle* h, int64_t value, void* stream);
 /* K1 implementation the handle runs (GMF_K1_CUDA_CORES or GMF_K1_TENSOR) */
 int gmf_k1_impl(gmf_handle* h);
 /* number of kernels this handle has launched so far (graph nodes counted) */

@@ -22,7 +22,7 @@ GMF_ERR_UNSUPPORTED = -4
 GMF_ERR_STATE = -5
 
 F32, F64 = 0, 1
-Y_DENSE_I32, Y_CSR_I32 = 0, 1
+Y_DENSE_I32, Y_CSR_I32, Y_CSR_PACK32 = 0, 1, 2
 K1_IMPL_CODES = {"auto": 0, "cuda_cores": 1, "tensor": 2}
 K1_IMPL_NAMES = {v: k for k, v in K1_IMPL_CODES.items()}
 FAMILY_CODES = {"gaussian": 0, "gamma": 1, "inverse_gaussian": 2, "poisson": 3,
@@ -110,6 +110,9 @@ SIGNATURES = {
     "gmf_profile_len": (_i64, [_P]),
     "gmf_geometry": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "gmf_k1_impl": (C.c_int, [_P]),
+    "gmf_stream_ready_ptr": (_P, [_P]),
+    "gmf_run_stream": (C.c_int, [_P, _i64, _P, _P]),
+    "gmf_stream_signal": (C.c_int, [_P, _i64, _P]),
     "gmf_launch_count": (_i64, [_P]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),

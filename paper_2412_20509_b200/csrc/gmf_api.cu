@@ -56,6 +56,8 @@ struct gmf_handle {
   int64_t launches = 0;         // kernels this handle launched (gmf_launch_count)
   bool residency_checked = false;
   unsigned int* host_abort = nullptr;   // pinned: abort flag of the software grid barrier
+  unsigned long long* ready_vals = nullptr;   // pinned: 0..max_steps, sources of gmf_stream_signal
+  int64_t n_ready_vals = 0;
 };
 
 namespace {
@@ -74,8 +76,9 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
   }
   if (d->y_format == GMF_Y_DENSE_I32) {
     if (!b->y_dense && d->n > 0) { set_error("dense Y pointer is NULL"); return GMF_ERR_CONFIG; }
-  } else if (d->y_format == GMF_Y_CSR_I32) {
+  } else if (d->y_format == GMF_Y_CSR_I32 || d->y_format == GMF_Y_CSR_PACK32) {
     if (!b->csr_ptr) { set_error("CSR row pointer is NULL"); return GMF_ERR_CONFIG; }
+    if (d->y_format == GMF_Y_CSR_PACK32 && d->m > 65536) { set_error("packed CSR needs m <= 65536"); return GMF_ERR_CONFIG; }
   } else { set_error("unknown y_format %d", d->y_format); return GMF_ERR_CONFIG; }
   if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) { set_error("bad rank/world"); return GMF_ERR_CONFIG; }
   if (b->n_row_blocks < 1 || b->n_col_blocks < 1 || b->max_steps < 0) { set_error("empty schedule"); return GMF_ERR_CONFIG; }
@@ -184,13 +187,14 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.est_alpha = cfg->est_alpha && desc->family == GMF_NEG_BINOMIAL;
   P.snap_stride = cfg->snapshot_stride; P.world = desc->world_size;
   // K1 implementation: tensor cores when eligible unless CUDA cores requested
-  if (desc->y_format == GMF_Y_CSR_I32 && desc->n > 0)
+  if (desc->y_format != GMF_Y_DENSE_I32 && desc->n > 0)
     GMF_CUDA(cudaMemcpy(&P.nnz, bufs->csr_ptr + desc->n, 8, cudaMemcpyDeviceToHost));
   // the tensor-core K1 stages rows with 16-byte copies: 16-byte aligned bases
   auto al16 = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
   const bool aligned = al16(bufs->theta_row) && (p == 0 || al16(bufs->x)) &&
                        (!P.has_off || al16(bufs->offset)) &&
-                       (desc->y_format != GMF_Y_CSR_I32 || (al16(bufs->csr_col) && al16(bufs->csr_val)));
+                       (desc->y_format == GMF_Y_DENSE_I32 || al16(bufs->csr_col)) &&
+                       (desc->y_format != GMF_Y_CSR_I32 || al16(bufs->csr_val));
   const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA) && aligned;
   if (cfg->k1_impl == GMF_K1_TENSOR && !tc_ok) {
     set_error("k1_impl=tensor needs fp32, no prior weights, q+d <= 16, p+d <= 16 and 16-byte "
@@ -282,6 +286,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
   const int64_t o_gbar = take(16);
+  const int64_t o_ready = take(8);                              // streaming ready counter
   const int64_t E1 = bufs->n_eval > 0 ? bufs->n_eval : 1;
   const int64_t o_esr = take(E1 * 8);                          // eval rows, sorted
   const int64_t o_esc = take(E1 * 4);                          // eval cols, same order
@@ -304,6 +309,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.rnpart = (double*)(base + o_rnp);
   P.cnpart = (double*)(base + o_cnp);
   P.gbar = (unsigned int*)(base + o_gbar);
+  P.ready = (const unsigned long long*)(base + o_ready);
   P.blocksum = (double*)(base + o_bs);
   P.snap_ver = (long long*)(base + o_lm);
   P.rho_tab = (double*)(base + o_rho);
@@ -378,6 +384,7 @@ int gmf_destroy(gmf_handle* h) {
   if (h->prof_buf) cudaFree(h->prof_buf);
   if (h->host_ctrl) cudaFreeHost(h->host_ctrl);
   if (h->host_abort) cudaFreeHost(h->host_abort);
+  if (h->ready_vals) cudaFreeHost(h->ready_vals);
   if (h->internal) cudaStreamDestroy(h->internal);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_b) cudaEventDestroy(h->ev_b);
@@ -409,6 +416,8 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
     GMF_CUDA(cudaMemsetAsync(P.gb_col, 0, cb, st));
     GMF_CUDA(cudaMemsetAsync(P.hb_col, 0, cb, st));
   }
+  GMF_CUDA(cudaMemsetAsync((void*)P.ready, 0, 8, st));
+  GMF_CUDA(cudaMemsetAsync((void*)P.gbar, 0, 16, st));
   int rc = launch_blocknorm(P, h->desc.dtype, st);
   if (rc) return rc;
   h->launches += 1;
@@ -523,10 +532,10 @@ int gmf_status_read(gmf_handle* h, gmf_status* out, void* stream) {
   GMF_CUDA(cudaSetDevice(h->desc.device));
   cudaStream_t st = (cudaStream_t)stream;
   GMF_CUDA(cudaMemcpyAsync(h->host_ctrl, h->P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  if (h->P.tcm) GMF_CUDA(cudaMemcpyAsync(h->host_abort, h->P.gbar + 2, 4, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaMemcpyAsync(h->host_abort, h->P.gbar + 2, 4, cudaMemcpyDeviceToHost, st));
   GMF_CUDA(cudaStreamSynchronize(st));
-  if (h->P.tcm && *h->host_abort) {
-    set_error("persistent fit kernel aborted: a grid barrier timed out (CTAs lost co-residency)");
+  if (*h->host_abort) {
+    set_error("persistent fit kernel aborted: a grid barrier or a streamed block timed out");
     return GMF_ERR_STATE;
   }
   return gmf_status_decode(h->host_ctrl, out);
@@ -648,6 +657,36 @@ int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
   h->launches += 1;
   return launch_objfull(h->P, h->desc.dtype, s.nb_shape, h->full_part, h->full_ticket, dev_sum,
                         (cudaStream_t)stream);
+}
+
+void* gmf_stream_ready_ptr(gmf_handle* h) { return h ? (void*)h->P.ready : nullptr; }
+
+int gmf_run_stream(gmf_handle* h, int64_t n_steps, void* host_status, void* stream) {
+  if (!h || !h->reset_done) { set_error("gmf_run_stream before gmf_reset"); return GMF_ERR_STATE; }
+  if (h->desc.world_size != 1) { set_error("gmf_run_stream is single-rank"); return GMF_ERR_STATE; }
+  if (h->fit_grid <= 0) { set_error("gmf_run_stream needs the persistent fit kernel"); return GMF_ERR_UNSUPPORTED; }
+  if (n_steps <= 0) return GMF_OK;
+  GMF_CUDA(cudaSetDevice(h->desc.device));
+  Params P = h->P;
+  P.RS = h->fit_rs;
+  P.stream_mode = 1;
+  P.host_status = host_status;
+  h->launches += 1;
+  return launch_fit(P, h->desc.dtype, h->NK, h->fit_grid, n_steps, (cudaStream_t)stream);
+}
+
+int gmf_stream_signal(gmf_handle* h, int64_t value, void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  const int64_t ms = h->bufs.max_steps;
+  if (value < 0 || value > ms) { set_error("stream signal %lld outside [0, %lld]", (long long)value, (long long)ms); return GMF_ERR_CONFIG; }
+  if (!h->ready_vals) {
+    GMF_CUDA(cudaMallocHost(&h->ready_vals, (ms + 1) * sizeof(unsigned long long)));
+    for (int64_t t = 0; t <= ms; ++t) h->ready_vals[t] = (unsigned long long)t;
+    h->n_ready_vals = ms + 1;
+  }
+  GMF_CUDA(cudaMemcpyAsync((void*)h->P.ready, h->ready_vals + value, sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return GMF_OK;
 }
 
 int gmf_k1_impl(gmf_handle* h) { return h ? (h->P.tcm ? GMF_K1_TENSOR : GMF_K1_CUDA_CORES) : -1; }

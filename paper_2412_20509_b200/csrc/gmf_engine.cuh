@@ -81,6 +81,12 @@ struct Params {
   const int32_t* rfirst; // [n+1] entries of row i: [rfirst[i], rfirst[i+1])
   void* ecache;          // [E][NK+4] T: a_i = [x | u | gamma | 0..] then offset_i
   void* vpad;            // [m][NK]   T: c_j = [b | v | z | 0..] (16-byte rows)
+  // streaming mode (gmf_run_stream): step t's row block is uploaded while the
+  // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;
+  // each step's status word is written to mapped pinned host memory
+  int stream_mode;
+  const unsigned long long* ready;
+  void* host_status;
   const double* rho_tab;     // learning_rate(t)        (optim.py:130-134)
   const double* alpt_tab;    // bias_correction(t + 1)  (optim.py:142-148)
   // workspace
@@ -266,20 +272,26 @@ GMF_D Ctrl advance(const Params& P, const Ctrl& C, const Decision& D, double nb_
 // ---------------------------------------------------------------------------
 // EMA + adaptive update of one coordinate (optim.py:450-462)
 // ---------------------------------------------------------------------------
+// same, with the old theta / EMA values already loaded (prefetched)
 template <typename T>
-GMF_D T ema_update(const Params& P, T* th, T* gb, T* hb, T gsum, T hsum, double scale, double lam,
-                   double rho, double at) {
-  const T old = *th;
+GMF_D T ema_update_from(const Params& P, T* th, T* gb, T* hb, T old, T ogb, T ohb, T gsum, T hsum,
+                        double scale, double lam, double rho, double at) {
   const T G = T(scale) * gsum + T(lam) * old;
   const T H = T(scale) * hsum + T(lam);
-  const T gn = (T(1) - T(P.a1)) * *gb + T(P.a1) * G;
-  const T hn = (T(1) - T(P.a2)) * *hb + T(P.a2) * H;
+  const T gn = (T(1) - T(P.a1)) * ogb + T(P.a1) * G;
+  const T hn = (T(1) - T(P.a2)) * ohb + T(P.a2) * H;
   *gb = gn;
   *hb = hn;
   const T delta = -T(at) * gn / (hn + T(P.damp));
   const T nv = old + T(rho) * delta;
   *th = nv;
   return nv;
+}
+
+template <typename T>
+GMF_D T ema_update(const Params& P, T* th, T* gb, T* hb, T gsum, T hsum, double scale, double lam,
+                   double rho, double at) {
+  return ema_update_from<T>(P, th, gb, hb, *th, *gb, *hb, gsum, hsum, scale, lam, rho, at);
 }
 
 }  // namespace gmf

@@ -163,6 +163,12 @@ GMF_D unsigned int ld_relaxed_u32(const unsigned int* p) {
   return v;
 }
 
+GMF_D unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long timeout_ns) {
   __shared__ int ok;
   __syncthreads();
@@ -315,6 +321,17 @@ k_fit(Params P, long long n_steps) {
     }
     if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
+    if (P.stream_mode && run_grad) {
+      // streaming: this step's row block is being uploaded; wait for its flag
+      if (threadIdx.x == 0) {
+        const unsigned long long want = (unsigned long long)t + 1, t0 = gtimer();
+        while (ld_relaxed_u64(P.ready) < want) {
+          if (gtimer() - t0 > kBarrierTimeoutNs) { atomicExch(P.gbar + 2, 1u); break; }
+        }
+        (void)ld_acquire_u32(P.gbar + 1);   // acquire: the uploaded block is visible
+      }
+      __syncthreads();
+    }
     if (run_grad && rs < RS) {
       if constexpr (TCM)
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
@@ -488,6 +505,7 @@ k_fit(Params P, long long n_steps) {
       }
       if (cow) P.snap_ver[blk] = per_now;
       *P.ctrl = N;
+      if (P.host_status) reinterpret_cast<Ctrl*>(P.host_status)[it] = N;   // per-step D2H
     }
     C = N;
     prev_blk = upd ? blk : -1;

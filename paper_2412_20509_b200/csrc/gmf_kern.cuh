@@ -8,13 +8,25 @@ namespace gmf {
 // ---------------------------------------------------------------------------
 // value of Y and eta at a tracked entry (optim.py:274-280)
 // ---------------------------------------------------------------------------
+// stored nonzero k of the CSR formats: column and count
+GMF_D int csr_col_at(const Params& P, int64_t k) {
+  const int32_t w = P.ci[k];
+  return P.yfmt == GMF_Y_CSR_PACK32 ? (int)((uint32_t)w & 0xFFFFu) : (int)w;
+}
+GMF_D int csr_val_at(const Params& P, int64_t k) {
+  return P.yfmt == GMF_Y_CSR_PACK32 ? (int)((uint32_t)P.ci[k] >> 16) : (int)P.cv[k];
+}
+// a staged word pair (col, val) of either CSR format
+GMF_D int stg_col(int pack, int32_t w) { return pack ? (int)((uint32_t)w & 0xFFFFu) : (int)w; }
+GMF_D int stg_val(int pack, int32_t w, int32_t v) { return pack ? (int)((uint32_t)w >> 16) : (int)v; }
+
 GMF_D double y_lookup(const Params& P, int64_t i, int64_t j) {
   if (P.yfmt == GMF_Y_DENSE_I32) return (double)P.y[i * P.m + j];
   int64_t lo = P.rp[i], hi = P.rp[i + 1];
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    const int cm = P.ci[mid];
-    if (cm == j) return (double)P.cv[mid];
+    const int cm = csr_col_at(P, mid);
+    if (cm == j) return (double)csr_val_at(P, mid);
     if (cm < j) lo = mid + 1; else hi = mid;
   }
   return 0.0;
@@ -310,9 +322,10 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       if (nnz <= kStageCap) {
         int32_t* col_b = reinterpret_cast<int32_t*>(st);
         int32_t* val_b = col_b + kStageCap;
+        const bool pack = P.yfmt == GMF_Y_CSR_PACK32;
         for (int64_t e = tid; e < nnz; e += kThreads) {
           cp_async<4>(col_b + e, P.ci + lo + e, true);
-          cp_async<4>(val_b + e, P.cv + lo + e, true);
+          if (!pack) cp_async<4>(val_b + e, P.cv + lo + e, true);
         }
         if (tid == 0) stage_n[b] = (int)nnz;
       } else if (tid == 0) {
@@ -369,21 +382,23 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         const int lane = tid & 31;
         for (int rr = tid >> 5; rr < rows; rr += kThreads / 32) {
           const int a = (int)rpc[rr] - lo, bnd = (int)rpc[rr + 1] - lo;
+          const int pack = P.yfmt == GMF_Y_CSR_PACK32;
           for (int e = a + lane; e < bnd; e += 32) {
-            const int col = col_b[e];
+            const int32_t w = col_b[e];
+            const int col = stg_col(pack, w);
             const int pp = P.col_identity ? col : ((P.cbof[col] == s) ? P.cpos[col] : -1);
             const int cl = pp - (int)cbase;
-            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = val_b[e];
+            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = stg_val(pack, w, pack ? 0 : val_b[e]);
           }
         }
       } else {   // row range too long or chunk too dense: direct loads
         for (int rr = tid >> 5; rr < rows; rr += kThreads / 32) {
           const int64_t i = i0 + rr;
           for (int64_t k = P.rp[i] + (tid & 31); k < P.rp[i + 1]; k += 32) {
-            const int col = P.ci[k];
+            const int col = csr_col_at(P, k);
             const int64_t pp = P.col_identity ? col : ((P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1);
             const int64_t cl = pp - cbase;
-            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = P.cv[k];
+            if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = csr_val_at(P, k);
           }
         }
       }

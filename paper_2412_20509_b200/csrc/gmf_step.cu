@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, do
       for (int64_t j = lane; j < P.m; j += 32)
         s += unit_deviance(P.fam, 0.0, exp(eta_at<T>(P, i, j)), alpha);
       for (int64_t k = P.rp[i] + lane; k < P.rp[i + 1]; k += 32) {
-        const int64_t j = P.ci[k];
+        const int64_t j = csr_col_at(P, k);
         const double mu = exp(eta_at<T>(P, i, j));
-        s += unit_deviance(P.fam, (double)P.cv[k], mu, alpha) - unit_deviance(P.fam, 0.0, mu, alpha);
+        s += unit_deviance(P.fam, (double)csr_val_at(P, k), mu, alpha) - unit_deviance(P.fam, 0.0, mu, alpha);
       }
     }
   }

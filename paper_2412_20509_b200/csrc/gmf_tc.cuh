@@ -367,7 +367,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         int32_t* col_b = reinterpret_cast<int32_t*>(st);
         int32_t* val_b = col_b + kStageCap;
         ocsr = stage_range4(col_b, P.ci, lo, hi, P.nnz);
-        stage_range4(val_b, P.cv, lo, hi, P.nnz);
+        if (P.yfmt != GMF_Y_CSR_PACK32) stage_range4(val_b, P.cv, lo, hi, P.nnz);
         if (tid == 0) stage_n = (int)(hi - lo);
       } else if (tid == 0) {
         stage_n = -1;
@@ -525,21 +525,23 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         const int lo = (int)rpc[0] - s_ocsr;
         for (int rr = warp; rr < rows; rr += kThreads / 32) {
           const int a = (int)rpc[rr] - lo, bnd = (int)rpc[rr + 1] - lo;
+          const int pack = P.yfmt == GMF_Y_CSR_PACK32;
           for (int e = a + lane; e < bnd; e += 32) {
-            const int col = col_b[e];
+            const int32_t w = col_b[e];
+            const int col = stg_col(pack, w);
             const int pp = P.col_identity ? col : ((P.cbof[col] == s) ? P.cpos[col] : -1);
             const int cl = pp - (int)cbase;
-            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = val_b[e];
+            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = stg_val(pack, w, pack ? 0 : val_b[e]);
           }
         }
       } else {
         for (int rr = warp; rr < rows; rr += kThreads / 32) {
           const int64_t i = i0 + rr;
           for (int64_t k = P.rp[i] + lane; k < P.rp[i + 1]; k += 32) {
-            const int col = P.ci[k];
+            const int col = csr_col_at(P, k);
             const int64_t pp = P.col_identity ? col : ((P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1);
             const int64_t cl = pp - cbase;
-            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = P.cv[k];
+            if (pp >= 0 && cl >= 0 && cl < TCC) Y[rr * YP + cl] = csr_val_at(P, k);
           }
         }
       }

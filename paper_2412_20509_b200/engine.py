@@ -137,7 +137,7 @@ class DeviceFit:
 
     def __init__(self, data, covs, fam, lnk, penalty, cfg, state: FactorizationState, *,
                  schedule: Schedule, offset=None, dtype="f64", device=None, world=1, rank=0,
-                 est_alpha=False, k1_impl="auto"):
+                 est_alpha=False, k1_impl="auto", y_format="auto"):
         import torch
         _lib.require_cuda()
         lib = _lib.lib()
@@ -178,13 +178,26 @@ class DeviceFit:
             p2, c2, v2 = permute_csr(indptr, indices, vals, order)
             self.y_dense = None
             self.csr_ptr = up(p2)
-            self.csr_col = up(c2.astype(np.int32))
-            self.csr_val = up(_counts_int32(v2, "response"))
-            y_format = _lib.Y_CSR_I32
+            counts = _counts_int32(v2, "response")
+            if y_format not in ("auto", "csr32", "packed"):
+                raise ConfigError(f"y_format must be 'auto', 'csr32' or 'packed', got {y_format!r}")
+            fits = self.m <= 65536 and (counts.size == 0 or int(counts.max()) <= 65535)
+            if y_format == "packed" and not fits:
+                raise ConfigError("packed CSR needs m <= 65536 and counts <= 65535")
+            if y_format != "csr32" and fits:
+                # one uint32 per nonzero: (count << 16) | column -- half the bytes
+                packed = (counts.astype(np.uint32) << np.uint32(16)) | c2.astype(np.uint32)
+                self.csr_col = up(packed.view(np.int32))
+                self.csr_val = None
+                y_format_code = _lib.Y_CSR_PACK32
+            else:
+                self.csr_col = up(c2.astype(np.int32))
+                self.csr_val = up(counts)
+                y_format_code = _lib.Y_CSR_I32
         else:
             self.y_dense = up(_counts_int32(data.values[order], "response"))
             self.csr_ptr = self.csr_col = self.csr_val = None
-            y_format = _lib.Y_DENSE_I32
+            y_format_code = _lib.Y_DENSE_I32
         self.weights = None
         if data.weights is not None:
             if data.csr is not None:
@@ -226,10 +239,12 @@ class DeviceFit:
         self.eval_col = up(schedule.eval_cols[keep].astype(np.int32)) if keep.any() else None
         n_eval = int(keep.sum())
 
+        self.y_format = {_lib.Y_DENSE_I32: "dense", _lib.Y_CSR_I32: "csr32",
+                         _lib.Y_CSR_PACK32: "packed"}[y_format_code]
         self.desc = _lib.GmfDesc(n=self.n_local, m=self.m, p=self.p, q=self.q, d=self.d,
                                  dtype=_lib.F64 if dtype == "f64" else _lib.F32,
                                  family=_lib.FAMILY_CODES[fam.kind], link=_lib.LINK_CODES[lnk.kind],
-                                 y_format=y_format, has_offset=int(offset is not None),
+                                 y_format=y_format_code, has_offset=int(offset is not None),
                                  has_weights=int(self.weights is not None), world_size=world,
                                  rank=rank, device=dev_index, reserved=0)
         self.cfg = _lib.GmfConfig(
@@ -262,6 +277,21 @@ class DeviceFit:
         self.lib = lib
         self.rec_bytes = int(lib.gmf_record_bytes(h))
         self.k1_impl = _lib.K1_IMPL_NAMES[int(lib.gmf_k1_impl(h))]
+
+    def ready_ptr(self):
+        """Device address of the streaming ready counter (gmf_stream_ready_ptr)."""
+        return int(self.lib.gmf_stream_ready_ptr(self.h))
+
+    def run_stream(self, n_steps, host_status=None):
+        """One launch of n_steps steps, each waiting for its block's ready flag
+        (gmf_run_stream); host_status: pinned uint8 tensor of n_steps status words."""
+        hs = C.c_void_p(host_status.data_ptr()) if host_status is not None else None
+        _lib.check(self.lib.gmf_run_stream(self.h, int(n_steps), hs, self.stream()), "gmf_run_stream")
+
+    def stream_signal(self, value, stream):
+        """Enqueue ready = value on `stream` (a torch.cuda.Stream): step value-1's block is there."""
+        _lib.check(self.lib.gmf_stream_signal(self.h, int(value), C.c_void_p(stream.cuda_stream)),
+                   "gmf_stream_signal")
 
     def launch_count(self):
         """Kernels this handle has launched so far (C-ABI gmf_launch_count)."""

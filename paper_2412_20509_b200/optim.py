@@ -183,7 +183,7 @@ def _gather_rows(fit: DeviceFit, tensor, group, mode):
 
 def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, rank=None,
              identify_mode="B1", dispersion="auto", callback=None, offset=None, dtype="f64",
-             device=None, process_group=None, exchange="device", k1_impl="auto"):
+             device=None, process_group=None, exchange="device", k1_impl="auto", y_format="auto"):
     """Block-wise adaptive stochastic quasi-Newton descent on the GPU.
 
     Drop-in for gmfkit.fit_asgd (optim.py:383-489); returns ``(state,
@@ -192,7 +192,9 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
     in eta), ``dtype`` ('f64' | 'f32'), ``device``, and ``process_group``
     (rows of every block split across the group's ranks, one GPU each), and
     ``k1_impl`` ('auto' | 'tensor' | 'cuda_cores'): the fused-gradient kernel
-    (tensor cores for fp32 when eligible).
+    (tensor cores for fp32 when eligible), ``y_format`` ('auto' | 'csr32' |
+    'packed') for a sparse response: packed CSR (one uint32 per nonzero) is
+    used when m <= 65536 and counts <= 65535.
     """
     started = time.perf_counter()
     if init_state is None:
@@ -213,7 +215,7 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
     sched = Schedule(n, m, cfg, mask=mask)
     fit = DeviceFit(data, covs, fam, lnk, penalty, cfg, init_state, schedule=sched,
                     offset=offset, dtype=dtype, device=device, world=world, rank=my_rank,
-                    est_alpha=est_alpha, k1_impl=k1_impl)
+                    est_alpha=est_alpha, k1_impl=k1_impl, y_format=y_format)
     try:
         fit.reset()
         _drive(fit, callback, process_group, exchange)

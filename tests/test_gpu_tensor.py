@@ -150,3 +150,26 @@ def test_fit_fp32_trajectory_per_impl(impl):
                              dtype="f32", k1_impl=impl)
     assert normwise(rep.objective_trace, g["trace"]) < TOL
     assert normwise(final.u @ final.v.T, g["final_u"] @ g["final_v"].T) < 1e-3
+
+
+def test_packed_csr_equals_csr32_bitwise():
+    """Packed CSR (one uint32 per nonzero) and int32 CSR hold the same counts:
+    identical trajectories on both K1 implementations."""
+    from conftest import golden
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    g = golden("nb_offset")
+    y = g["y"]
+    data = gk.ResponseMatrix(csr=dense_to_csr(y), shape=y.shape)
+    covs = gk.CovariateSet(x=g["x"], z=g["z"] if g["z"].shape[1] else None, n=y.shape[0], m=y.shape[1])
+    st = gk.FactorizationState(g["init_b"], g["init_gamma"], g["init_u"], g["init_v"], 1.0,
+                               float(g["init_nb"]))
+    me, mr, mc, seed, cap = (int(v) for v in g["cfg"])
+    cfg = gk.SgdConfig(max_epochs=me, mb_rows=mr, mb_cols=mc, seed=seed, tol=1e-30)
+    pen = gk.PenaltyConfig(lam=1.0, blocks=tuple(float(v) for v in g["lam"]))
+    for impl in ("tensor", "cuda_cores"):
+        out = []
+        for yf in ("csr32", "packed"):
+            _, rep = gk.fit_asgd(data, covs, gk.NegBinomial(st.nb_shape), gk.Log(), pen, cfg, st,
+                                 offset=g["offset"], dtype="f32", k1_impl=impl, y_format=yf)
+            out.append(rep.objective_trace)
+        assert out[0] == out[1], impl
