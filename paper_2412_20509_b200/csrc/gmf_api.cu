@@ -17,6 +17,7 @@ int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long x
 int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
                  int fit_extra_smem, int* fit_blocks_per_sm);
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
+int64_t colimg_bytes_total(int NK, int CT);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int tile_cols(int dtype);
@@ -293,6 +294,8 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_rfi = take((desc->n + 1) * 4);               // entries per row
   const int64_t o_ecache = take(E1 * (h->NK + 4) * h->tsz);    // objective row cache
   const int64_t o_vpad = take(desc->m * h->NK * h->tsz);       // padded column features
+  const bool want_img = P.tcm && col_identity;
+  const int64_t o_cimg = take(want_img ? colimg_bytes_total(h->NK, P.CT) : 16);
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -320,6 +323,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.rfirst = (const int32_t*)(base + o_rfi);
   P.ecache = base + o_ecache;
   P.vpad = base + o_vpad;
+  P.colimg = want_img ? (void*)(base + o_cimg) : nullptr;
   if (bufs->n_eval > 0) {
     // the tracked sample sorted by (block-major) row, with each row's first
     // entry: phase 2 writes an updated row straight into its entries' cache

@@ -85,6 +85,11 @@ struct Params {
   // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;
   // each step's status word is written to mapped pinned host memory
   int stream_mode;
+  // tensor-core K1 column operands (R | B1h | B1l per column tile, bf16, in the
+  // shared-memory byte layout), kept current by the persistent kernel's column
+  // updates when every step uses all columns; colimg_on only inside k_fit
+  void* colimg;
+  int colimg_on;
   const unsigned long long* ready;
   void* host_status;
   const double* rho_tab;     // learning_rate(t)        (optim.py:130-134)

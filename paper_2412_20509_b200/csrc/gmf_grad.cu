@@ -283,7 +283,14 @@ k_fit(Params P, long long n_steps) {
       else if (k < P.KA) v = zg[j * P.q + (k - Kc)];
       tptr<T>(P.vpad)[e] = v;
     }
-    if (!gsync(kBarrierTimeoutNs)) n_steps = 0;   // vpad complete before the first objective
+    if constexpr (TCM) {
+      if (P.colimg_on) {   // K1's column-operand images, one task per thread
+        const int nt = tc::colimg_tasks<NK>();
+        for (int64_t e = gtid; e < (int64_t)P.CT * nt; e += gstride)
+          tc::colimg_task<NK>(P, (int)(e / nt), (int)(e % nt));
+      }
+    }
+    if (!gsync(kBarrierTimeoutNs)) n_steps = 0;   // vpad / images complete before the first step
   }
   const bool prof = P.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   // per-CTA stamps of the last profiled step (block-uniform condition)
@@ -470,6 +477,9 @@ k_fit(Params P, long long n_steps) {
                                       tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
                                       k < P.p ? P.lam_b : P.lam_v, rho, at);
           tptr<T>(P.vpad)[j * NK + k] = nvv;   // the objective's padded copy of [b | v | z]
+          if constexpr (TCM) {
+            if (P.colimg_on) tc::colimg_write<NK>(P, j, k, (float)nvv);
+          }
           nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
         }
       }
@@ -571,6 +581,8 @@ int grad_bucket(int KA) {
 
 int tile_cols(int dtype) { return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC; }
 
+int64_t colimg_bytes_total(int NK, int CT) { return (int64_t)CT * tc::colimg_bytes(NK); }
+
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm) {
   if (tcm) return tc::smem_layout(NK).total;
   return grad_smem(tile_cols(dtype), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
@@ -637,7 +649,9 @@ int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, 
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm) +
                      (size_t)P.ep_cap * sizeof(int4);
-  void* args[] = {(void*)&P, (void*)&n_steps};
+  Params Q = P;
+  Q.colimg_on = P.tcm && P.colimg != nullptr;   // images maintained by k_fit's own updates
+  void* args[] = {(void*)&Q, (void*)&n_steps};
   if (P.tcm) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
     GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 4 * sizeof(unsigned int), st));
     GMF_CUDA(cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, st));

@@ -272,6 +272,93 @@ GMF_D void split8(const float (&x)[8], uint4& hi, uint4& lo) {
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// ---- column-operand images (persistent kernel, all columns every step) ----
+GMF_HD int64_t colimg_bytes(int NK) {
+  const Smem L = smem_layout(NK);
+  return L.B1l + (L.B1l - L.B1h) - L.R;   // R | B1h | B1l, contiguous in smem
+}
+
+// task t of column tile ct: R rows (feature k, 8 columns) then B1 rows
+// (column, 8 features), written into the tile's image exactly as K1 would
+// build them in shared memory
+template <int NK>
+GMF_D void colimg_task(const Params& P, int ct, int t) {
+  const Smem L = smem_layout(NK);
+  const int nka = L.nka, ng1 = nka / 8;
+  const uint32_t sbo1 = (uint32_t)(nka / 8) * 128u;
+  unsigned char* img = reinterpret_cast<unsigned char*>(P.colimg) + (int64_t)ct * colimg_bytes(NK);
+  unsigned char* Rb = img, *B1h = img + (L.B1h - L.R), *B1l = img + (L.B1l - L.R);
+  const float* th_col = tptr<float>(P.th_col);
+  const float* zg = tptr<float>(P.z);
+  const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q;
+  const int64_t cbase = (int64_t)ct * TCC;
+  const int ncv = (int)(P.m - cbase < TCC ? P.m - cbase : TCC);
+  if (t < 16 * (TCC / 8)) {
+    const int rk = t / (TCC / 8), rcg = t % (TCC / 8);
+    float v[8], v2[8];
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = 8 * rcg + u;
+      const bool ok = c < ncv && rk < Kr;
+      const int64_t j = cbase + c;
+      v[u] = !ok ? 0.f : (rk < q ? zg[j * q + rk] : th_col[j * Kc + p + (rk - q)]);
+      v2[u] = v[u] * v[u];
+    }
+    uint4 h, l, h2, l2;
+    split8(v, h, l);
+    split8(v2, h2, l2);
+    *reinterpret_cast<uint4*>(Rb + kofs(rk, 8 * rcg, SBO_P)) = h;
+    *reinterpret_cast<uint4*>(Rb + kofs(16 + rk, 8 * rcg, SBO_P)) = l;
+    *reinterpret_cast<uint4*>(Rb + kofs(32 + rk, 8 * rcg, SBO_P)) = h2;
+    *reinterpret_cast<uint4*>(Rb + kofs(48 + rk, 8 * rcg, SBO_P)) = l2;
+    return;
+  }
+  t -= 16 * (TCC / 8);
+  if (t >= TCC * ng1) return;
+  const int c = t / ng1, g = t % ng1;
+  const bool ok = c < ncv;
+  const int64_t j = cbase + c;
+  float v[8];
+  #pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int k = 8 * g + u;
+    float x = 0.f;
+    if (ok && k < Kc) x = th_col[j * Kc + k];
+    else if (ok && k < KA) x = zg[j * q + (k - Kc)];
+    v[u] = x * 1.4426950408889634f;
+  }
+  uint4 h, l;
+  split8(v, h, l);
+  *reinterpret_cast<uint4*>(B1h + kofs(c, 8 * g, sbo1)) = h;
+  *reinterpret_cast<uint4*>(B1l + kofs(c, 8 * g, sbo1)) = l;
+}
+
+template <int NK>
+GMF_HD int colimg_tasks() { return 16 * (TCC / 8) + TCC * ((NK <= 16 ? 16 : 32) / 8); }
+
+// column j's coordinate k (of [b | v]) changed to v: its B1 and R entries
+template <int NK>
+GMF_D void colimg_write(const Params& P, int64_t j, int k, float v) {
+  const Smem L = smem_layout(NK);
+  const uint32_t sbo1 = (uint32_t)(L.nka / 8) * 128u;
+  const int ct = (int)(j / TCC), c = (int)(j % TCC);
+  unsigned char* img = reinterpret_cast<unsigned char*>(P.colimg) + (int64_t)ct * colimg_bytes(NK);
+  __nv_bfloat16 h, l;
+  split_bf16(v * 1.4426950408889634f, h, l);
+  *reinterpret_cast<__nv_bfloat16*>(img + (L.B1h - L.R) + kofs(c, k, sbo1)) = h;
+  *reinterpret_cast<__nv_bfloat16*>(img + (L.B1l - L.R) + kofs(c, k, sbo1)) = l;
+  if (k >= P.p) {
+    const int kr = P.q + (k - P.p);
+    __nv_bfloat16 h2, l2;
+    split_bf16(v, h, l);
+    split_bf16(v * v, h2, l2);
+    *reinterpret_cast<__nv_bfloat16*>(img + kofs(kr, c, SBO_P)) = h;
+    *reinterpret_cast<__nv_bfloat16*>(img + kofs(16 + kr, c, SBO_P)) = l;
+    *reinterpret_cast<__nv_bfloat16*>(img + kofs(32 + kr, c, SBO_P)) = h2;
+    *reinterpret_cast<__nv_bfloat16*>(img + kofs(48 + kr, c, SBO_P)) = l2;
+  }
+}
+
 template <int FAM, int NK>
 GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct, int RS,
                     unsigned char* smem, Ctx& X, unsigned long long* kp) {
@@ -381,12 +468,21 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
 
   // ---- column operands of the tile (once per call); global loads first ----
   // feature order a = [x | u | gamma], c = [b | v | z]
-  // B1: thread per (column, 8 features); R: thread per (feature, 8 columns)
+  // B1: thread per (column, 8 features); R: thread per (feature, 8 columns).
+  // In the persistent kernel with all columns every step, the column updates
+  // keep a byte image of R | B1h | B1l per tile: one 16-byte cp.async copy.
   const int ng1 = nka / 8;
+  const bool use_img = P.colimg_on != 0;
+  if (use_img) {
+    const int64_t nb = colimg_bytes(NK);
+    const unsigned char* img = reinterpret_cast<const unsigned char*>(P.colimg) + (int64_t)ct * nb;
+    for (int64_t o = (int64_t)tid * 16; o < nb; o += (int64_t)kThreads * 16)
+      cp_async16(Rb + o, img + o);
+  }
   float b1v[8], rv[8];
   int b1c = 0, b1g = 0, rk = 0, rcg = 0;
-  const bool b1_task = tid < TCC * ng1 / 2;         // first half of the B1 tasks
-  {
+  const bool b1_task = !use_img;
+  if (!use_img) {
     const int t = tid;
     b1c = t / ng1; b1g = t % ng1;
     const int64_t pos = cbase + b1c;
@@ -416,10 +512,10 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     for (int64_t e = tid; e <= nrows; e += kThreads) rp_s[e] = P.rp[r0 + rlo + e];
   for (int e = tid; e < TRC * YP; e += kThreads) Y[e] = 0;
   __syncthreads();   // rp staged
-  issue(rlo);
-  {
+  issue(rlo);   // (commits the image copy with the first chunk's staging)
+  if (!use_img) {
     uint4 h, l;
-    if (b1_task || ng1 == 2) {
+    if (b1_task) {
       split8(b1v, h, l);
       *reinterpret_cast<uint4*>(B1h + kofs(b1c, 8 * b1g, sbo1)) = h;
       *reinterpret_cast<uint4*>(B1l + kofs(b1c, 8 * b1g, sbo1)) = l;
@@ -435,7 +531,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     *reinterpret_cast<uint4*>(Rb + kofs(32 + rk, 8 * rcg, SBO_P)) = h2;
     *reinterpret_cast<uint4*>(Rb + kofs(48 + rk, 8 * rcg, SBO_P)) = l2;
   }
-  if (ng1 == 4) {   // K = 32: the second half of the B1 tasks
+  if (ng1 == 4 && !use_img) {   // K = 32: the second half of the B1 tasks
     const int t = tid + kThreads;
     const int c = t / ng1, g = t % ng1;
     const int64_t pos = cbase + c;
