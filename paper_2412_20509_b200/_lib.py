@@ -12,7 +12,7 @@ import os
 from .exceptions import ConfigError, DomainError, GmfError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgmf_asgd.so")
+LIB_PATH = os.environ.get("GMF_LIB_PATH") or os.path.join(PKG, "libgmf_asgd.so")   # override: experiments
 
 GMF_OK = 0
 GMF_ERR_CONFIG = -1

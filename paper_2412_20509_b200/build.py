@@ -23,7 +23,8 @@ LIB = os.path.join(PKG, "libgmf_asgd.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-              "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+              "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC] + \
+    os.environ.get("GMF_NVCC_EXTRA", "").split()   # experiments only (e.g. -DGMF_EXP_...)
 
 
 def nvcc():

@@ -354,14 +354,25 @@ k_fit(Params P, long long n_steps) {
     const int64_t rI0 = blk >= 0 ? P.rbp[blk] : 0;
     const int64_t nIK = blk >= 0 ? (P.rbp[blk + 1] - rI0) * Kr : 0;
     T pth[2], pgb[2], phb[2];
+    int32_t prf[2][2];
     #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t e = gtid + u * gstride;
-      const int64_t o = (rI0 * Kr) + (e < nIK ? e : 0);
+      const int64_t ec = e < nIK ? e : 0;
+      const int64_t o = (rI0 * Kr) + ec;
       pth[u] = ldcg_t<T>(tptr<T>(P.th_row) + o);
       pgb[u] = ldcg_t<T>(tptr<T>(P.gb_row) + o);
       phb[u] = ldcg_t<T>(tptr<T>(P.hb_row) + o);
+      const int64_t ii = rI0 + (int64_t)((uint32_t)ec / (uint32_t)Kr);
+      prf[u][0] = P.rfirst[ii];
+      prf[u][1] = P.rfirst[ii + 1];
     }
+    // and every scalar phase 2 reads (constant through the step)
+    const int64_t j0s = blk >= 0 ? P.cbp[sidx] : 0;
+    const int64_t nJs = blk >= 0 ? P.cbp[sidx + 1] - j0s : 1;
+    const double s_col_pre = blk >= 0 ? P.rbscale[blk] : 0.0;
+    const double rho_pre = run_grad ? P.rho_tab[t] : 0.0;
+    const double at_pre = run_grad ? P.alpt_tab[t] : 0.0;
     if (!gsync(kBarrierTimeoutNs)) break;
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
@@ -390,19 +401,21 @@ k_fit(Params P, long long n_steps) {
     if (prof) { t_b = gtimer(); P.prof[6] += t_b - t_a; }
     const Decision D = decide_from(P, C, v7[0], v7[3], v7[4], v7[1], v7[2]);
     const bool upd = !D.stop;
-    const double rho = upd ? P.rho_tab[t] : 0.0;
-    const double at = upd ? P.alpt_tab[t] : 0.0;
+    const double rho = upd ? rho_pre : 0.0;
+    const double at = upd ? at_pre : 0.0;
     // copy-on-write snapshot of block I (first update after a snapshot point)
     const long long per_now = C.snap_period + (D.snap ? 1 : 0);
     const bool cow = upd && sv != per_now;
     double nrm[4] = {0.0, 0.0, 0.0, 0.0};   // new ||Gamma_I||, ||U_I||, ||B||, ||V|| partials
     // rows of block I
     if (upd) {
-      const int64_t nJ = P.cbp[sidx + 1] - P.cbp[sidx];
-      const double s_row = (double)P.m / (double)nJ;
+      const double s_row = (double)P.m / (double)nJs;
       for (int64_t e = gtid, u = 0; e < nIK; e += gstride, ++u) {
-        const int64_t il = e / Kr;
-        const int k = (int)(e % Kr);
+        // 32-bit index split (a 64-bit division by a runtime divisor is a
+        // long software sequence); e < |I| (q+d) < 2^31
+        const uint32_t ue = (uint32_t)e, il32 = ue / (uint32_t)Kr;
+        const int64_t il = il32;
+        const int k = (int)(ue - il32 * (uint32_t)Kr);
         const int64_t o = rI0 * Kr + e;
         T gs, hs;
         rowpart_sum<T>(P, il, k, gs, hs);
@@ -422,8 +435,8 @@ k_fit(Params P, long long n_steps) {
         {   // the objective's cache rows of this row's tracked entries
           const int64_t i = rI0 + il;
           const int apos = k < P.q ? P.p + P.d + k : P.p + (k - P.q);   // a = [x | u | gamma]
-          for (int32_t f = P.rfirst[i]; f < P.rfirst[i + 1]; ++f)
-            tptr<T>(P.ecache)[(int64_t)f * (NK + 4) + apos] = nvv;
+          const int32_t f0 = u < 2 ? prf[u][0] : P.rfirst[i], f1 = u < 2 ? prf[u][1] : P.rfirst[i + 1];
+          for (int32_t f = f0; f < f1; ++f) tptr<T>(P.ecache)[(int64_t)f * (NK + 4) + apos] = nvv;
         }
         nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
       }
@@ -433,8 +446,8 @@ k_fit(Params P, long long n_steps) {
     // splits (all loads in flight), fixed xor-butterfly order inside the
     // group; the group's first lane snapshots and updates
     if (upd) {
-      const int64_t j0 = P.cbp[sidx], nJ = P.cbp[sidx + 1] - j0;
-      const double s_col = P.rbscale[blk];
+      const int64_t j0 = j0s, nJ = nJs;
+      const double s_col = s_col_pre;
       const T* cpart = tptr<T>(P.colpart);
       const int64_t rstride = (int64_t)TC * kk;
       const int sub = lane & 7;
@@ -445,8 +458,9 @@ k_fit(Params P, long long n_steps) {
         const int64_t e = gg + rd * ng;
         const bool live = e < ne;
         const int64_t ee = live ? e : 0;
-        const int64_t pos = ee / Kc;
-        const int k = (int)(ee % Kc);
+        const uint32_t uee = (uint32_t)ee, pos32 = uee / (uint32_t)Kc;   // ne < 2^31
+        const int64_t pos = pos32;
+        const int k = (int)(uee - pos32 * (uint32_t)Kc);
         const T* base = cpart + ((pos / TC) * RS * TC + (pos % TC)) * kk + k;
         constexpr int MAXU = 16;   // 128 row splits per pass
         T g = T(0), h = T(0);
@@ -489,7 +503,7 @@ k_fit(Params P, long long n_steps) {
     if ((upd || D.snap) && !(upd && P.col_identity)) {
       const T* tc = tptr<T>(P.th_col);
       for (int64_t e = gtid; e < P.m * Kc; e += gstride) {
-        const int64_t j = e / Kc;
+        const int64_t j = (int64_t)((uint64_t)e / (uint64_t)Kc);
         if (upd && P.cbof[j] == sidx) continue;
         const T x = tc[e];
         if (D.snap) tptr<T>(P.sn_col)[e] = x;
