@@ -322,11 +322,11 @@ k_fit(Params P, long long n_steps) {
       block_sum_vec<1>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
       if (profc && threadIdx.x == 0) {   // objective sub-phases (SM clocks): loop, reduction
-        P.prof[16 + 16 * blockIdx.x + 5] += (unsigned long long)(c1 - c0);
-        P.prof[16 + 16 * blockIdx.x + 6] += (unsigned long long)(clock64() - c1);
+        atomicAdd(P.prof + 16 + 16 * blockIdx.x + 5, (unsigned long long)(c1 - c0));
+        atomicAdd(P.prof + 16 + 16 * blockIdx.x + 6, (unsigned long long)(clock64() - c1));
       }
     }
-    if (prof) { t_b = gtimer(); P.prof[0] += t_b - t_a; t_a = t_b; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 0, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
     if (P.stream_mode && run_grad) {
       // streaming: this step's row block is being uploaded; wait for its flag
@@ -345,7 +345,7 @@ k_fit(Params P, long long n_steps) {
                               profc ? P.prof + 16 + 16 * blockIdx.x + 8 : nullptr);
       else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
     }
-    if (prof) { t_b = gtimer(); P.prof[1] += t_b - t_a; t_a = t_b; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 2] = gtimer(); }
     // Phase-2 inputs that phase 1 does not write are read before the barrier
     // so their latency hides behind it: this thread's first two row
@@ -375,7 +375,7 @@ k_fit(Params P, long long n_steps) {
     const double at_pre = run_grad ? P.alpt_tab[t] : 0.0;
     if (!gsync(kBarrierTimeoutNs)) break;
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 3] = gtimer(); }
-    if (prof) { t_b = gtimer(); P.prof[2] += t_b - t_a; t_a = t_b; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 2, t_b - t_a); t_a = t_b; }
     // ------------------------- phase 2 -------------------------
     // totals, redundantly in every CTA: deviance, ||B||^2, ||V||^2,
     // ||Gamma||^2, ||U||^2, NB moment sums (one merged reduction)
@@ -398,7 +398,7 @@ k_fit(Params P, long long n_steps) {
       }
     }
     block_sum_vec<7>(v7, scr);
-    if (prof) { t_b = gtimer(); P.prof[6] += t_b - t_a; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 6, t_b - t_a); }
     const Decision D = decide_from(P, C, v7[0], v7[3], v7[4], v7[1], v7[2]);
     const bool upd = !D.stop;
     const double rho = upd ? rho_pre : 0.0;
@@ -410,6 +410,21 @@ k_fit(Params P, long long n_steps) {
     // rows of block I
     if (upd) {
       const double s_row = (double)P.m / (double)nJs;
+      // the first two elements' row partials, all loads in flight together
+      constexpr int RTW = 4;
+      T rg[2][RTW], rh[2][RTW];
+      {
+        const T* rpb = tptr<T>(P.rowpart);
+        const int64_t cstride = P.nstar_max * (2 * Kr);
+        #pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t e = gtid + u * gstride;
+          const uint32_t ue = (uint32_t)(e < nIK ? e : 0), il32 = ue / (uint32_t)Kr;
+          const T* src = rpb + (int64_t)il32 * (2 * Kr) + (ue - il32 * (uint32_t)Kr);
+          gather_vec_cg<RTW>(src, cstride, P.CT, rg[u]);
+          gather_vec_cg<RTW>(src + Kr, cstride, P.CT, rh[u]);
+        }
+      }
       for (int64_t e = gtid, u = 0; e < nIK; e += gstride, ++u) {
         // 32-bit index split (a 64-bit division by a runtime divisor is a
         // long software sequence); e < |I| (q+d) < 2^31
@@ -418,7 +433,23 @@ k_fit(Params P, long long n_steps) {
         const int k = (int)(ue - il32 * (uint32_t)Kr);
         const int64_t o = rI0 * Kr + e;
         T gs, hs;
-        rowpart_sum<T>(P, il, k, gs, hs);
+        if (u < 2) {   // tiles in the same fixed order as rowpart_sum
+          gs = T(0);
+          hs = T(0);
+          #pragma unroll
+          for (int c = 0; c < RTW; ++c) { gs += rg[u][c]; hs += rh[u][c]; }
+          for (int c0 = RTW; c0 < P.CT; c0 += RTW) {
+            T gv[RTW], hv[RTW];
+            const int64_t cstride = P.nstar_max * (2 * Kr);
+            const T* src = tptr<T>(P.rowpart) + il * (2 * Kr) + k + c0 * cstride;
+            gather_vec_cg<RTW>(src, cstride, P.CT - c0, gv);
+            gather_vec_cg<RTW>(src + Kr, cstride, P.CT - c0, hv);
+            #pragma unroll
+            for (int c = 0; c < RTW; ++c) { gs += gv[c]; hs += hv[c]; }
+          }
+        } else {
+          rowpart_sum<T>(P, il, k, gs, hs);
+        }
         const T old = u < 2 ? pth[u] : ldcg_t<T>(tptr<T>(P.th_row) + o);
         const T ogb = u < 2 ? pgb[u] : ldcg_t<T>(tptr<T>(P.gb_row) + o);
         const T ohb = u < 2 ? phb[u] : ldcg_t<T>(tptr<T>(P.hb_row) + o);
@@ -441,7 +472,7 @@ k_fit(Params P, long long n_steps) {
         nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
       }
     }
-    if (prof) { t_b = gtimer(); P.prof[7] += t_b - t_a; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 7, t_b - t_a); }
     // columns of block J: a group of 8 lanes per coordinate splits the K1 row
     // splits (all loads in flight), fixed xor-butterfly order inside the
     // group; the group's first lane snapshots and updates
@@ -498,7 +529,7 @@ k_fit(Params P, long long n_steps) {
         }
       }
     }
-    if (prof) { t_b = gtimer(); P.prof[8] += t_b - t_a; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 8, t_b - t_a); }
     // columns outside J: snapshot and norms (nothing to do when J = all)
     if ((upd || D.snap) && !(upd && P.col_identity)) {
       const T* tc = tptr<T>(P.th_col);
@@ -510,9 +541,9 @@ k_fit(Params P, long long n_steps) {
         nrm[(int)(e % Kc) < P.p ? 2 : 3] += (double)x * (double)x;
       }
     }
-    if (prof) { t_b = gtimer(); P.prof[9] += t_b - t_a; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 9, t_b - t_a); }
     block_sum_vec<4>(nrm, scr);
-    if (prof) { t_b = gtimer(); P.prof[10] += t_b - t_a; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 10, t_b - t_a); }
     if (threadIdx.x == 0) {
       P.rnpart[2 * blockIdx.x] = nrm[0];
       P.rnpart[2 * blockIdx.x + 1] = nrm[1];
@@ -533,11 +564,11 @@ k_fit(Params P, long long n_steps) {
     }
     C = N;
     prev_blk = upd ? blk : -1;
-    if (prof) { t_b = gtimer(); P.prof[3] += t_b - t_a; t_a = t_b; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 3, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 4] = gtimer(); }
     if (D.stop) break;
     if (!gsync(kBarrierTimeoutNs)) break;
-    if (prof) { t_b = gtimer(); P.prof[4] += t_b - t_a; t_a = t_b; P.prof[5] += 1; }
+    if (prof) { t_b = gtimer(); atomicAdd(P.prof + 4, t_b - t_a); t_a = t_b; atomicAdd(P.prof + 5, 1ull); }
   }
   if (blockIdx.x == 0 && prev_blk >= 0) {
     double v[2] = {0.0, 0.0};

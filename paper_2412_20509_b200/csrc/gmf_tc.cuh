@@ -797,7 +797,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   }
   tick(7);
   if (kp && tid == 0)
-    for (int i = 0; i < 8; ++i) kp[i] += (unsigned long long)kacc[i];
+    for (int i = 0; i < 8; ++i) atomicAdd(kp + i, (unsigned long long)kacc[i]);   // no read-back
 }
 
 }  // namespace tc
