@@ -440,8 +440,15 @@ def main():
         st_e = _lib.GmfStatus()
         import ctypes as C
         fit.lib.gmf_status_decode(C.c_void_p(status_h.data_ptr() + (E - 1) * sbytes), C.byref(st_e))
-        assert st_e.t == W + K + K2 + E, st_e.t
-        assert fit.status().t == W + K + K2 + E
+        try:
+            streamed_ok = fit.status().t == W + K + K2 + E and st_e.t == W + K + K2 + E
+        except _lib.GmfError:   # a profiler serialising the copy stream: blocks never arrived
+            streamed_ok = False
+        if not streamed_ok:
+            print(json.dumps({"warning": "streaming e2e aborted (copy stream not concurrent, e.g. "
+                              "under a profiler); e2e not reported"}), file=sys.stderr)
+            E = 0
+    if E > 0 and world == 1:
         e_entries = float(sizes[seq[t_first:t_first + E]].sum()) * sp.m
         e2e = {"value": e_entries / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": sbytes,
