@@ -129,6 +129,28 @@ def _counts_int32(vals, what):
 
 
 # ---------------------------------------------------------------------------
+# packed CSR (GMF_Y_CSR_PACK32): one uint32 per nonzero, (count << 16) | column
+# ---------------------------------------------------------------------------
+
+def packable(m, counts):
+    """Packed CSR holds columns < 65536 and counts <= 65535."""
+    counts = np.asarray(counts)
+    return m <= 65536 and (counts.size == 0 or (int(counts.min()) >= 0 and int(counts.max()) <= 65535))
+
+
+def pack_csr(cols, counts):
+    """int32 view of the packed words (the C ABI's csr_col for PACK32)."""
+    w = (np.asarray(counts).astype(np.uint32) << np.uint32(16)) | np.asarray(cols).astype(np.uint32)
+    return w.view(np.int32)
+
+
+def unpack_csr(words):
+    """(columns, counts) of packed words (test/debug helper)."""
+    w = np.asarray(words).view(np.uint32)
+    return (w & np.uint32(0xFFFF)).astype(np.int32), (w >> np.uint32(16)).astype(np.int32)
+
+
+# ---------------------------------------------------------------------------
 # the device fit
 # ---------------------------------------------------------------------------
 
@@ -181,13 +203,11 @@ class DeviceFit:
             counts = _counts_int32(v2, "response")
             if y_format not in ("auto", "csr32", "packed"):
                 raise ConfigError(f"y_format must be 'auto', 'csr32' or 'packed', got {y_format!r}")
-            fits = self.m <= 65536 and (counts.size == 0 or int(counts.max()) <= 65535)
+            fits = packable(self.m, counts)
             if y_format == "packed" and not fits:
                 raise ConfigError("packed CSR needs m <= 65536 and counts <= 65535")
             if y_format != "csr32" and fits:
-                # one uint32 per nonzero: (count << 16) | column -- half the bytes
-                packed = (counts.astype(np.uint32) << np.uint32(16)) | c2.astype(np.uint32)
-                self.csr_col = up(packed.view(np.int32))
+                self.csr_col = up(pack_csr(c2, counts))
                 self.csr_val = None
                 y_format_code = _lib.Y_CSR_PACK32
             else:

@@ -156,3 +156,16 @@ def test_exception_taxonomy_matches_reference():
     assert issubclass(gk.DivergenceError, ArithmeticError)
     e = gk.DivergenceError("x", state=1)
     assert e.state == 1
+
+
+def test_packed_csr_round_trip():
+    from paper_2412_20509_b200.engine import pack_csr, packable, unpack_csr
+    rng = np.random.default_rng(4)
+    cols = rng.integers(0, 65536, size=1000)
+    counts = rng.integers(0, 65536, size=1000)
+    w = pack_csr(cols, counts)
+    assert w.dtype == np.int32 and w.size == 1000
+    c2, v2 = unpack_csr(w)
+    assert np.array_equal(c2, cols) and np.array_equal(v2, counts)
+    assert packable(65536, counts) and not packable(65537, counts)
+    assert not packable(10, np.array([0, 65536])) and packable(10, np.array([], dtype=int))
