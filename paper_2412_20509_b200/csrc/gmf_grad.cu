@@ -197,6 +197,50 @@ GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long t
   return ok != 0;
 }
 
+// Split form: arrive (release this CTA's writes, count in) and wait (spin,
+// acquire).  Loads issued between the two -- inputs of the next phase that
+// the current phase does not write -- overlap the barrier instead of
+// delaying the arriving thread's fence.
+struct SoftArrival { unsigned int gen; int last; };
+
+GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, SoftArrival& a) {
+  __shared__ SoftArrival s_a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SoftArrival r;
+    r.gen = ld_relaxed_u32(gb + 1);
+    __threadfence();   // release this CTA's writes
+    r.last = atomicAdd(gb, 1u) == G - 1;
+    if (r.last) {
+      atomicExch(gb, 0u);
+      __threadfence();
+      atomicAdd(gb + 1, 1u);
+    }
+    s_a = r;
+  }
+  __syncthreads();
+  a = s_a;
+}
+
+GMF_D bool soft_grid_wait(unsigned int* gb, const SoftArrival& a, unsigned long long timeout_ns) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int res = 1;
+    if (!a.last) {
+      const unsigned long long t0 = gtimer();
+      while (ld_relaxed_u32(gb + 1) == a.gen) {
+        if (ld_relaxed_u32(gb + 2)) { res = 0; break; }
+        if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); res = 0; break; }
+      }
+    }
+    (void)ld_acquire_u32(gb + 1);   // acquire: later loads see other CTAs' writes
+    __threadfence();
+    ok = res;
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
 constexpr unsigned long long kProbeTimeoutNs = 50ull * 1000 * 1000;        // residency probe
 constexpr unsigned long long kBarrierTimeoutNs = 10ull * 1000 * 1000 * 1000;  // hang guard
 
@@ -347,9 +391,13 @@ k_fit(Params P, long long n_steps) {
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 2] = gtimer(); }
-    // Phase-2 inputs that phase 1 does not write are read before the barrier
+    // Phase-2 inputs that phase 1 does not write are read across the barrier
     // so their latency hides behind it: this thread's first two row
-    // coordinates (theta, EMA state) and the block's snapshot version.
+    // coordinates (theta, EMA state) and the block's snapshot version.  The
+    // tensor-core kernel's split barrier arrives first, so these loads do not
+    // hold up the arriving thread's release fence.
+    SoftArrival arr;
+    if constexpr (TCM) soft_grid_arrive(P.gbar, (unsigned int)G, arr);
     const long long sv = blk >= 0 ? __ldcg(P.snap_ver + blk) : 0;
     const int64_t rI0 = blk >= 0 ? P.rbp[blk] : 0;
     const int64_t nIK = blk >= 0 ? (P.rbp[blk + 1] - rI0) * Kr : 0;
@@ -373,7 +421,11 @@ k_fit(Params P, long long n_steps) {
     const double s_col_pre = blk >= 0 ? P.rbscale[blk] : 0.0;
     const double rho_pre = run_grad ? P.rho_tab[t] : 0.0;
     const double at_pre = run_grad ? P.alpt_tab[t] : 0.0;
-    if (!gsync(kBarrierTimeoutNs)) break;
+    if constexpr (TCM) {
+      if (!soft_grid_wait(P.gbar, arr, kBarrierTimeoutNs)) break;
+    } else {
+      if (!gsync(kBarrierTimeoutNs)) break;
+    }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 2, t_b - t_a); t_a = t_b; }
     // ------------------------- phase 2 -------------------------
