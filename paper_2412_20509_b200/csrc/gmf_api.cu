@@ -19,6 +19,7 @@ int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int t
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
 int64_t colimg_bytes_total(int NK, int CT);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
+int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int tile_cols(int dtype);
 int grad_bucket(int KA);
@@ -252,6 +253,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   int coop = 0;
   GMF_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc->device));
   h->fit_grid = coop ? (fit_bps * n_sm / P.CT) * P.CT : 0;
+  if (getenv("GMF_NO_PERSISTENT")) h->fit_grid = 0;   // diagnostics: per-step kernels only
   h->fit_rs = h->fit_grid / (P.CT > 0 ? P.CT : 1);
 
   // ---- workspace carve-up ----
@@ -449,8 +451,9 @@ int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, doub
   GMF_CUDA(cudaSetDevice(h->desc.device));
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_grad(P, h->desc.dtype, h->NK, st, row_block, col_block, nb_shape);
+  if (!rc) rc = launch_colrec(P, h->desc.dtype, st, col_block);
   if (rc) return rc;
-  h->launches += 2;
+  h->launches += 3;
   const int64_t nI = h->rbp_host[row_block + 1] - h->rbp_host[row_block];
   const int64_t nJ = h->cbp_host[col_block + 1] - h->cbp_host[col_block];
   return launch_gradout(P, h->desc.dtype, row_block, col_block, nI, nJ, g_row, h_row, g_col,
@@ -462,8 +465,10 @@ int gmf_step_local(gmf_handle* h, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_obj(h->P, h->desc.dtype, st);
   if (rc) return rc;
-  h->launches += 2;
-  return launch_grad(h->P, h->desc.dtype, h->NK, st, -1, -1, 0.0);
+  h->launches += 3;
+  rc = launch_grad(h->P, h->desc.dtype, h->NK, st, -1, -1, 0.0);
+  if (rc) return rc;
+  return launch_colrec(h->P, h->desc.dtype, st, -1);
 }
 
 int gmf_step_apply(gmf_handle* h, const void* gathered, void* stream) {
@@ -511,6 +516,7 @@ int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
       for (int64_t s = 0; s < c && rc == GMF_OK; ++s) {
         rc = launch_obj(h->P, h->desc.dtype, h->internal);
         if (!rc) rc = launch_grad(h->P, h->desc.dtype, h->NK, h->internal, -1, -1, 0.0);
+        if (!rc) rc = launch_colrec(h->P, h->desc.dtype, h->internal, -1);
         if (!rc) rc = launch_apply(h->P, h->desc.dtype, nullptr, h->internal);
       }
       cudaError_t e = cudaStreamEndCapture(h->internal, &g);
@@ -523,7 +529,7 @@ int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
       it = h->graphs.emplace(c, ex).first;
     }
     GMF_CUDA(cudaGraphLaunch(it->second, h->internal));
-    h->launches += 3 * c;
+    h->launches += 4 * c;
     left -= c;
   }
   GMF_CUDA(cudaEventRecord(h->ev_b, h->internal));

@@ -53,22 +53,8 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
     grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
   }
 
-  const int64_t nJ = P.cbp[s + 1] - P.cbp[s];
-  const int kk = 2 * P.Kc;
-  // last CTA of this column tile: rank-level column partial (parallel)
-  if (last_block_ticket(P.tickets + ct, RS)) {
-    T* recp = reinterpret_cast<T*>(P.rec + REC_HDR);
-    for (int e = threadIdx.x; e < TC * P.Kc; e += kThreads) {
-      const int64_t pp = (int64_t)ct * TC + e / P.Kc;
-      const int k = e % P.Kc;
-      if (pp >= nJ) continue;
-      T g, h;
-      colpart_sum<T>(P, pp, k, RS, g, h);
-      recp[pp * kk + k] = g;
-      recp[pp * kk + P.Kc + k] = h;
-    }
-    if (threadIdx.x == 0) P.tickets[ct] = 0u;
-  }
+  (void)TC;
+  // (the rank-level column partials are reduced by k_colrec, many CTAs wide)
   // last CTA overall: NB moment sums in fixed CTA order (parallel)
   const unsigned int total = (unsigned int)(RS * gridDim.y);
   if (last_block_ticket(P.tickets + P.CT, total)) {
@@ -79,6 +65,58 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
       P.rec[R_NBDEN] = sd;
       P.tickets[P.CT] = 0u;
     }
+  }
+}
+
+// rank-level column partials of the step's column block into the rank record
+// (per-step path): a group of 8 lanes per coordinate sums the K1 row splits'
+// partials (all loads in flight, fixed xor-butterfly order inside the group)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_colrec(Params P, long long xs) {
+  long long s;
+  if (xs >= 0) {
+    s = xs;
+  } else {
+    const Ctrl* C = P.ctrl;
+    const long long t = C->t;
+    if (C->stopped || t >= P.max_steps) return;
+    s = t % P.S;
+  }
+  const int64_t nJ = P.cbp[s + 1] - P.cbp[s];
+  const int Kc = P.Kc, kk = 2 * Kc, TC = P.TC, RS = P.RS;
+  const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int sub = threadIdx.x & 7;
+  const int64_t e = gtid >> 3;
+  const bool live = e < nJ * Kc;
+  const uint32_t ue = (uint32_t)(live ? e : 0), pos = ue / (uint32_t)Kc;
+  const int k = (int)(ue - pos * (uint32_t)Kc);
+  const T* base = tptr<T>(P.colpart) + ((int64_t)(pos / TC) * RS * TC + (pos % TC)) * kk + k;
+  const int64_t rstride = (int64_t)TC * kk;
+  constexpr int MAXU = 16;
+  T g = T(0), h = T(0);
+  for (int r0 = 0; r0 < RS; r0 += 8 * MAXU) {
+    T gv[MAXU], hv[MAXU];
+    #pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      const int r = r0 + sub + 8 * u;
+      const int rc = r < RS ? r : 0;
+      const T gx = ldcg_t<T>(base + rc * rstride);
+      const T hx = ldcg_t<T>(base + rc * rstride + Kc);
+      gv[u] = r < RS ? gx : T(0);
+      hv[u] = r < RS ? hx : T(0);
+    }
+    #pragma unroll
+    for (int u = 0; u < MAXU; ++u) { g += gv[u]; h += hv[u]; }
+  }
+  #pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+  }
+  if (live && sub == 0) {
+    T* recp = reinterpret_cast<T*>(P.rec + REC_HDR);
+    recp[(int64_t)pos * kk + k] = g;
+    recp[(int64_t)pos * kk + Kc + k] = h;
   }
 }
 
@@ -738,6 +776,15 @@ int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long x
   const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm);
   void* args[] = {(void*)&P, (void*)&xb, (void*)&xs, (void*)&xalpha};
   GMF_CUDA(cudaLaunchKernel(f, grid, dim3(kThreads), args, smem, st));
+  return GMF_OK;
+}
+
+int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs) {
+  const int64_t ne = P.jmax * P.Kc;
+  const unsigned blocks = (unsigned)((ne * 8 + kThreads - 1) / kThreads);
+  void* args[] = {(void*)&P, (void*)&xs};
+  void* f = dtype == GMF_F64 ? (void*)k_colrec<double> : (void*)k_colrec<float>;
+  GMF_CUDA(cudaLaunchKernel(f, dim3(blocks > 0 ? blocks : 1), dim3(kThreads), args, 0, st));
   return GMF_OK;
 }
 
