@@ -293,8 +293,10 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t E1 = bufs->n_eval > 0 ? bufs->n_eval : 1;
   const int64_t o_esr = take(E1 * 8);                          // eval rows, sorted
   const int64_t o_esc = take(E1 * 4);                          // eval cols, same order
-  const int64_t o_rfi = take((desc->n + 1) * 4);               // entries per row
-  const int64_t o_ecache = take(E1 * (h->NK + 4) * h->tsz);    // objective row cache
+  const int64_t o_rsl = take((desc->n > 0 ? desc->n : 1) * 4);  // cache slot per row
+  const int64_t o_srw = take(E1 * 8);                          // row per cache slot
+  const int64_t o_esl = take(E1 * 4);                          // cache slot per entry
+  const int64_t o_ecache = take(E1 * (h->NK + 4) * h->tsz);    // objective row cache (<= E slots)
   const int64_t o_vpad = take(desc->m * h->NK * h->tsz);       // padded column features
   const bool want_img = P.tcm && col_identity;
   const int64_t o_cimg = take(want_img ? colimg_bytes_total(h->NK, P.CT) : 16);
@@ -322,14 +324,17 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   h->full_part = (double*)(base + o_fp);
   h->full_ticket = (unsigned int*)(base + o_ft);
   GMF_CUDA(cudaMemset(h->ws, 0, off));
-  P.rfirst = (const int32_t*)(base + o_rfi);
+  P.rslot = (const int32_t*)(base + o_rsl);
+  P.srow = (const int64_t*)(base + o_srw);
+  P.eslot = nullptr;
+  P.nslots = 0;
   P.ecache = base + o_ecache;
   P.vpad = base + o_vpad;
   P.colimg = want_img ? (void*)(base + o_cimg) : nullptr;
   if (bufs->n_eval > 0) {
-    // the tracked sample sorted by (block-major) row, with each row's first
-    // entry: phase 2 writes an updated row straight into its entries' cache
-    // rows (the objective is an order-free sum)
+    // the tracked sample sorted by (block-major) row; each tracked row owns a
+    // cache slot that phase 2 writes with the row (the objective is an
+    // order-free sum)
     const int64_t E = bufs->n_eval;
     std::vector<int64_t> er(E), ers(E);
     std::vector<int32_t> ec(E), ecs(E);
@@ -340,18 +345,25 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return er[a] < er[b]; });
     for (int64_t k = 0; k < E; ++k) { ers[k] = er[idx[k]]; ecs[k] = ec[idx[k]]; }
     if (E >= (int64_t)1 << 31) { set_error("more than 2^31 tracked entries"); gmf_destroy(h); return GMF_ERR_CONFIG; }
-    std::vector<int32_t> rfi(desc->n + 1);
-    int64_t f = 0;
-    for (int64_t i = 0; i <= desc->n; ++i) {
-      while (f < E && ers[f] < i) ++f;
-      rfi[i] = (int32_t)f;
+    // one cache slot per distinct tracked row (entries are sorted by row)
+    std::vector<int32_t> rsl(desc->n > 0 ? desc->n : 1, -1), esl(E);
+    std::vector<int64_t> srw;
+    for (int64_t k = 0; k < E; ++k) {
+      if (k == 0 || ers[k] != ers[k - 1]) srw.push_back(ers[k]);
+      esl[k] = (int32_t)(srw.size() - 1);
+      rsl[ers[k]] = esl[k];
     }
     GMF_CUDA(cudaMemcpy(base + o_esr, ers.data(), E * 8, cudaMemcpyHostToDevice));
     GMF_CUDA(cudaMemcpy(base + o_esc, ecs.data(), E * 4, cudaMemcpyHostToDevice));
-    GMF_CUDA(cudaMemcpy(base + o_rfi, rfi.data(), (desc->n + 1) * 4, cudaMemcpyHostToDevice));
+    if (desc->n > 0) GMF_CUDA(cudaMemcpy(base + o_rsl, rsl.data(), desc->n * 4, cudaMemcpyHostToDevice));
+    GMF_CUDA(cudaMemcpy(base + o_srw, srw.data(), srw.size() * 8, cudaMemcpyHostToDevice));
+    GMF_CUDA(cudaMemcpy(base + o_esl, esl.data(), E * 4, cudaMemcpyHostToDevice));
+    P.eslot = (const int32_t*)(base + o_esl);
+    P.nslots = (int64_t)srw.size();
     P.erow = (const int64_t*)(base + o_esr);
     P.ecol = (const int32_t*)(base + o_esc);
   }
+  if (bufs->n_eval <= 0 && desc->n > 0) GMF_CUDA(cudaMemset(base + o_rsl, 0xFF, desc->n * 4));   // no slots
   P.ep = (const int4*)(base + o_ep);
   if (bufs->n_eval > 0) {   // tracked sample packed with its Y, once per fit
     rc = launch_eval_pack(P, (int4*)(base + o_ep), 0);

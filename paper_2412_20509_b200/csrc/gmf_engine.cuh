@@ -78,8 +78,11 @@ struct Params {
   int ep_cap;          // tracked entries cached per fit CTA in shared memory (0 = none)
   int64_t ep_soff;     // their shared-memory offset (bytes, after K1's region)
   // tracked-objective caches of the persistent kernel (entries sorted by row):
-  const int32_t* rfirst; // [n+1] entries of row i: [rfirst[i], rfirst[i+1])
-  void* ecache;          // [E][NK+4] T: a_i = [x | u | gamma | 0..] then offset_i
+  const int32_t* rslot;  // [n] cache slot of row i (-1: no tracked entry)
+  const int64_t* srow;   // [nslots] row of each cache slot
+  const int32_t* eslot;  // [E] cache slot of each tracked entry (packed into ep.w)
+  int64_t nslots;
+  void* ecache;          // [nslots][NK+4] T: a_i = [x | u | gamma | 0..] then offset_i
   void* vpad;            // [m][NK]   T: c_j = [b | v | z | 0..] (16-byte rows)
   // streaming mode (gmf_run_stream): step t's row block is uploaded while the
   // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;

@@ -124,16 +124,15 @@ __global__ void __launch_bounds__(kThreads) k_colrec(Params P, long long xs) {
 // persistent fit kernel (single rank)
 // ---------------------------------------------------------------------------
 
-// tracked objective of the persistent kernel (optim.py:283-290).  The
-// sample is fixed and sorted by row, so each entry keeps its row's features
-// in a cache row a_i = [x | u | gamma | 0 | offset] and the columns'
-// [b | v | z] sit in 16-byte padded rows; phase 2 writes both together with
-// theta (row i's entries are [rfirst[i], rfirst[i+1])), so eta is a few
-// 16-byte loads per entry instead of ~2K scattered words.  fp64 predictor,
-// fixed order.
+// tracked objective of the persistent kernel (optim.py:283-290).  Every row
+// with a tracked entry owns a cache slot a_i = [x | u | gamma | 0 | offset]
+// (entries carry their slot in ep.w) and the columns' [b | v | z] sit in
+// 16-byte padded rows; phase 2 writes both together with theta (one store
+// per updated coordinate), so eta is a few 16-byte loads per entry instead of
+// ~2K scattered words.  fp64 predictor, fixed order.
 template <typename T, int NK>
-GMF_D void ecache_fill(const Params& P, int64_t e, int64_t i) {
-  T* row = tptr<T>(P.ecache) + e * (NK + 4);
+GMF_D void ecache_fill(const Params& P, int64_t slot, int64_t i) {
+  T* row = tptr<T>(P.ecache) + slot * (NK + 4);
   const T* th = tptr<T>(P.th_row) + i * P.Kr;
   const T* xg = tptr<T>(P.x) + i * P.p;
   const int p = P.p, d = P.d, KA = P.KA, q = P.q;
@@ -163,7 +162,7 @@ GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, in
   for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
     const int4 en = ents[e - lo];
     const int64_t i = en.x, j = en.y;
-    const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + e * (NK + 4));
+    const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + (int64_t)en.w * (NK + 4));
     const V* c = reinterpret_cast<const V*>(tptr<T>(P.vpad) + j * NK);
     T av[NK + 4], cv[NK];
     #pragma unroll
@@ -352,9 +351,8 @@ k_fit(Params P, long long n_steps) {
   const int64_t e_lo = e_per * blockIdx.x < P.E ? e_per * blockIdx.x : P.E;
   const int64_t e_hi = e_lo + e_per < P.E ? e_lo + e_per : P.E;
   {
-    // objective caches: this CTA's entry rows, every column's padded features
-    for (int64_t e = e_lo + threadIdx.x; e < e_hi; e += kThreads)
-      ecache_fill<T, NK>(P, e, (int64_t)ep_src[e - e_lo + (ep_cached ? 0 : e_lo)].x);
+    // objective caches: every tracked row's slot, every column's padded features
+    for (int64_t sl = gtid; sl < P.nslots; sl += gstride) ecache_fill<T, NK>(P, sl, P.srow[sl]);
     const T* tc = tptr<T>(P.th_col);
     const T* zg = tptr<T>(P.z);
     for (int64_t e = gtid; e < P.m * NK; e += gstride) {
@@ -440,7 +438,7 @@ k_fit(Params P, long long n_steps) {
     const int64_t rI0 = blk >= 0 ? P.rbp[blk] : 0;
     const int64_t nIK = blk >= 0 ? (P.rbp[blk + 1] - rI0) * Kr : 0;
     T pth[2], pgb[2], phb[2];
-    int32_t prf[2][2];
+    int32_t prs[2];
     #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t e = gtid + u * gstride;
@@ -450,8 +448,7 @@ k_fit(Params P, long long n_steps) {
       pgb[u] = ldcg_t<T>(tptr<T>(P.gb_row) + o);
       phb[u] = ldcg_t<T>(tptr<T>(P.hb_row) + o);
       const int64_t ii = rI0 + (int64_t)((uint32_t)ec / (uint32_t)Kr);
-      prf[u][0] = P.rfirst[ii];
-      prf[u][1] = P.rfirst[ii + 1];
+      prs[u] = P.rslot[ii];
     }
     // and every scalar phase 2 reads (constant through the step)
     const int64_t j0s = blk >= 0 ? P.cbp[sidx] : 0;
@@ -556,8 +553,8 @@ k_fit(Params P, long long n_steps) {
         {   // the objective's cache rows of this row's tracked entries
           const int64_t i = rI0 + il;
           const int apos = k < P.q ? P.p + P.d + k : P.p + (k - P.q);   // a = [x | u | gamma]
-          const int32_t f0 = u < 2 ? prf[u][0] : P.rfirst[i], f1 = u < 2 ? prf[u][1] : P.rfirst[i + 1];
-          for (int32_t f = f0; f < f1; ++f) tptr<T>(P.ecache)[(int64_t)f * (NK + 4) + apos] = nvv;
+          const int32_t sl = u < 2 ? prs[u] : P.rslot[i];
+          if (sl >= 0) tptr<T>(P.ecache)[(int64_t)sl * (NK + 4) + apos] = nvv;
         }
         nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
       }

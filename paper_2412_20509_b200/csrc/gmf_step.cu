@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_pack(Params P, int4* out) {
   for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < P.E;
        e += (int64_t)gridDim.x * kThreads) {
     const int64_t i = P.erow[e], j = P.ecol[e];
-    out[e] = make_int4((int)i, (int)j, (int)y_lookup(P, i, j), 0);
+    out[e] = make_int4((int)i, (int)j, (int)y_lookup(P, i, j), P.eslot ? P.eslot[e] : 0);
   }
 }
 

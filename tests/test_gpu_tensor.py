@@ -173,3 +173,44 @@ def test_packed_csr_equals_csr32_bitwise():
                                  offset=g["offset"], dtype="f32", k1_impl=impl, y_format=yf)
             out.append(rep.objective_trace)
         assert out[0] == out[1], impl
+
+
+def test_streaming_run_equals_resident_run_bitwise():
+    """gmf_run_stream (one launch; each step waits for its row block's ready
+    signal, statuses written to pinned host memory) reproduces gmf_run."""
+    import torch
+    from paper_2412_20509_b200 import _lib, workloads
+    from paper_2412_20509_b200.engine import DeviceFit, Schedule
+    y, x, z, off, st = _problem(9, 600, 140, 6, 1, 0, "nb", True)
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    data = gk.ResponseMatrix(csr=dense_to_csr(y), shape=y.shape)
+    covs = gk.CovariateSet(x=x, n=600, m=140)
+    cfg = gk.SgdConfig(max_epochs=40, mb_rows=100, mb_cols=140, tol=1e-30, seed=2)
+    sch = Schedule(600, 140, cfg)
+    out = []
+    for stream in (False, True):
+        fit = DeviceFit(data, covs, gk.NegBinomial(2.0), gk.Log(), gk.PenaltyConfig(), cfg, st,
+                        schedule=sch, offset=off, dtype="f32", est_alpha=True)
+        try:
+            fit.reset()
+            if not stream:
+                fit.run(30)
+            else:
+                sb = int(fit.lib.gmf_status_raw_bytes())
+                host = torch.zeros(30 * sb, dtype=torch.uint8).pin_memory()
+                cs = torch.cuda.Stream()
+                fit.run_stream(30, host)
+                for t in range(30):          # blocks are resident: signal each step
+                    fit.stream_signal(t + 1, cs)
+                torch.cuda.synchronize()
+                st_last = _lib.GmfStatus()
+                import ctypes as C
+                fit.lib.gmf_status_decode(C.c_void_p(host.data_ptr() + 29 * sb), C.byref(st_last))
+                assert st_last.t == 30
+            status = fit.status()
+            assert status.t == 30
+            out.append((fit.trace(int(status.trace_len))[0], fit.theta_col.cpu().numpy().copy()))
+        finally:
+            fit.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
