@@ -32,6 +32,8 @@
 #pragma once
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "gmf_kern.cuh"
 
 namespace gmf {
@@ -711,23 +713,29 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
     const bool row_ok = lane < rows;
     float dd[16], hh[16];
     float cn = 0.f, cdn = 0.f;
-    #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float w = (row_ok && i < vcols) ? 1.f : 0.f;
-      const float mu = exp_pre(__uint_as_float(ev[i]) + offr);
-      const float r = (float)yv[i] - mu;
-      if (FAM == 0) {
-        const float ws = w * rphi;
-        dd[i] = -ws * r;
-        hh[i] = ws * mu;
-      } else {
-        const float inv = w * rcp_fast(fmaf(mu, tra, tphi));
-        dd[i] = -r * inv;
-        hh[i] = mu * inv;
-        cn = fmaf(w * mu, mu, cn);
-        cdn = fmaf(w, fmaf(r, r, -mu), cdn);
+    // a full row of 16 valid columns (the common case) skips the masking
+    auto entries = [&](auto masked) {
+      #pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float w = masked ? ((row_ok && i < vcols) ? 1.f : 0.f) : 1.f;
+        const float mu = exp_pre(__uint_as_float(ev[i]) + offr);
+        const float r = (float)yv[i] - mu;
+        if (FAM == 0) {
+          const float ws = masked ? w * rphi : rphi;
+          dd[i] = -ws * r;
+          hh[i] = ws * mu;
+        } else {
+          const float rc = rcp_fast(fmaf(mu, tra, tphi));
+          const float inv = masked ? w * rc : rc;
+          dd[i] = -r * inv;
+          hh[i] = mu * inv;
+          cn = fmaf(masked ? w * mu : mu, mu, cn);
+          cdn = masked ? fmaf(w, fmaf(r, r, -mu), cdn) : cdn + fmaf(r, r, -mu);
+        }
       }
-    }
+    };
+    if (row_ok && vcols == 16) entries(std::false_type{});
+    else entries(std::true_type{});
     nb_num += (double)cn;
     nb_den += (double)cdn;
     put_split16(dd, Pb, stack_hi(lane), stack_hi(lane) + 8, c0);
