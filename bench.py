@@ -304,7 +304,7 @@ def main():
                          "step_row_splits", "feature_bucket", "k1_smem_bytes", "max_block_rows"],
                         [int(v) for v in geo]))
     phases = None
-    if args.phases and world == 1:
+    if args.phases and world == 1 and geometry["fit_ctas"] > 0:   # persistent k_fit only
         import ctypes as C
         nprof = int(fit.lib.gmf_profile_len(fit.h))
         buf = (C.c_double * nprof)()

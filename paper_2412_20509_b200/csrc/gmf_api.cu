@@ -21,6 +21,7 @@ int64_t colimg_bytes_total(int NK, int CT);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
+int launch_cache_fill(const Params& P, int dtype, cudaStream_t st);
 int tile_cols(int dtype);
 int grad_bucket(int KA);
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm);
@@ -330,6 +331,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.nslots = 0;
   P.ecache = base + o_ecache;
   P.vpad = base + o_vpad;
+  P.nkb = h->NK;
   P.colimg = want_img ? (void*)(base + o_cimg) : nullptr;
   if (bufs->n_eval > 0) {
     // the tracked sample sorted by (block-major) row; each tracked row owns a
@@ -437,8 +439,9 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
   GMF_CUDA(cudaMemsetAsync((void*)P.ready, 0, 8, st));
   GMF_CUDA(cudaMemsetAsync((void*)P.gbar, 0, 16, st));
   int rc = launch_blocknorm(P, h->desc.dtype, st);
+  if (!rc) rc = launch_cache_fill(P, h->desc.dtype, st);   // the per-step path's objective caches
   if (rc) return rc;
-  h->launches += 1;
+  h->launches += 2;
   GMF_CUDA(cudaStreamSynchronize(st));
   if (P.tcm && h->fit_grid > 0 && !h->residency_checked) {
     // the tensor-core fit kernel synchronises with a software grid barrier:

@@ -84,6 +84,7 @@ struct Params {
   int64_t nslots;
   void* ecache;          // [nslots][NK+4] T: a_i = [x | u | gamma | 0..] then offset_i
   void* vpad;            // [m][NK]   T: c_j = [b | v | z | 0..] (16-byte rows)
+  int nkb;               // NK, the feature bucket (cache row strides at run time)
   // streaming mode (gmf_run_stream): step t's row block is uploaded while the
   // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;
   // each step's status word is written to mapped pinned host memory

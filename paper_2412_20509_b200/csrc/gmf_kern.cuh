@@ -51,28 +51,21 @@ GMF_D double eta_at(const Params& P, int64_t i, int64_t j) {
 // (optim.py:283-290) -> out[0] deviance, out[1] ||B||^2, out[2] ||V||^2.
 // ---------------------------------------------------------------------------
 template <typename T>
-GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double* out) {
-  __shared__ double scr[kThreads / 32];
-  const T* wg = tptr<T>(P.w);
-  double s = 0.0;
+GMF_D void obj_partial(const Params& P, double alpha, int cta, int ncta, double* out,
+                       double dev_partial) {
+  __shared__ double scr[3 * (kThreads / 32)];
+  (void)alpha;
+  double s = dev_partial;   // this CTA's deviance share (gmf_step.cu: entry_dev_cached)
   const int64_t stride = (int64_t)ncta * kThreads;
-  for (int64_t e = (int64_t)cta * kThreads + threadIdx.x; e < P.E; e += stride) {
-    const int4 en = P.ep[e];
-    const int64_t i = en.x, j = en.y;
-    const double mu = exp(eta_at<T>(P, i, j));
-    const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-    s += w * unit_deviance(P.fam, (double)en.z, mu, alpha);
-  }
   const T* tc = tptr<T>(P.th_col);
   double nb = 0.0, nv = 0.0;
   for (int64_t e = (int64_t)cta * kThreads + threadIdx.x; e < P.m * P.Kc; e += stride) {
     const double v = (double)tc[e];
     if ((int)(e % P.Kc) < P.p) nb += v * v; else nv += v * v;
   }
-  s = block_sum<kThreads>(s, scr);
-  nb = block_sum<kThreads>(nb, scr);
-  nv = block_sum<kThreads>(nv, scr);
-  if (threadIdx.x == 0) { out[0] = s; out[1] = nb; out[2] = nv; }
+  double v3[3] = {s, nb, nv};
+  block_sum_vec<3>(v3, scr);
+  if (threadIdx.x == 0) { out[0] = v3[0]; out[1] = v3[1]; out[2] = v3[2]; }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,6 +1,8 @@
 // Per-step kernels of the multi-rank path -- K3 (tracked objective) and K2
 // (tracker + EMA/adaptive update + NB shape) -- plus helper kernels.  The
 // single-rank path runs the same bodies inside the persistent k_fit.
+#include <type_traits>
+
 #include "gmf_kern.cuh"
 
 namespace gmf {
@@ -11,19 +13,100 @@ namespace gmf {
 // norms and the column norms into the rank record.  It also folds the row
 // norms of the block updated by the previous k_apply (rnpart) into blocksum.
 // ---------------------------------------------------------------------------
+// ---- tracked-objective caches for the per-step path (bucket NK known at
+// run time; the persistent kernel's compile-time versions are in gmf_grad.cu)
+template <typename T>
+GMF_D void ecache_fill_rt(const Params& P, int64_t slot, int64_t i) {
+  const int NKr = P.nkb;
+  T* row = tptr<T>(P.ecache) + slot * (NKr + 4);
+  const T* th = tptr<T>(P.th_row) + i * P.Kr;
+  const T* xg = tptr<T>(P.x) + i * P.p;
+  const int p = P.p, d = P.d, KA = P.KA, q = P.q;
+  for (int k = 0; k < NKr; ++k) {
+    T v = T(0);
+    if (k < p) v = xg[k];
+    else if (k < p + d) v = th[q + (k - p)];
+    else if (k < KA) v = th[k - p - d];
+    row[k] = v;
+  }
+  row[NKr] = P.has_off ? tptr<T>(P.off)[i] : T(0);
+  row[NKr + 1] = T(0); row[NKr + 2] = T(0); row[NKr + 3] = T(0);
+}
+
+// every tracked row's slot and every column's padded [b | v | z] (gmf_reset)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_cache_fill(Params P) {
+  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x, gs = (int64_t)gridDim.x * kThreads;
+  for (int64_t sl = g; sl < P.nslots; sl += gs) ecache_fill_rt<T>(P, sl, P.srow[sl]);
+  const T* tc = tptr<T>(P.th_col);
+  const T* zg = tptr<T>(P.z);
+  for (int64_t e = g; e < P.m * P.nkb; e += gs) {
+    const int64_t j = e / P.nkb;
+    const int k = (int)(e % P.nkb);
+    T v = T(0);
+    if (k < P.Kc) v = tc[j * P.Kc + k];
+    else if (k < P.KA) v = zg[j * P.q + (k - P.Kc)];
+    tptr<T>(P.vpad)[e] = v;
+  }
+}
+
+// deviance of entry en from the caches: eta = a_slot . c_j (16-byte loads,
+// all in flight; nkb <= 32)
+template <typename T>
+GMF_D double entry_dev_cached(const Params& P, int4 en, double alpha) {
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int VN = 16 / sizeof(T);
+  constexpr int MAXV = 32 / VN;
+  const int nv = P.nkb / VN;
+  const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + (int64_t)en.w * (P.nkb + 4));
+  const V* c = reinterpret_cast<const V*>(tptr<T>(P.vpad) + (int64_t)en.y * P.nkb);
+  V av[MAXV], cv[MAXV];
+  #pragma unroll
+  for (int u = 0; u < MAXV; ++u) {
+    const int uu = u < nv ? u : 0;
+    av[u] = a[uu];
+    cv[u] = __ldcg(c + uu);
+  }
+  const T off = tptr<T>(P.ecache)[(int64_t)en.w * (P.nkb + 4) + P.nkb];
+  double eta = (double)off;
+  #pragma unroll
+  for (int u = 0; u < MAXV; ++u) {
+    if (u < nv) {
+      const T* ap = reinterpret_cast<const T*>(&av[u]);
+      const T* cp = reinterpret_cast<const T*>(&cv[u]);
+      #pragma unroll
+      for (int k = 0; k < VN; ++k) eta += (double)ap[k] * (double)cp[k];
+    }
+  }
+  const double wv = P.has_w ? (double)tptr<T>(P.w)[(int64_t)en.x * P.m + en.y] : 1.0;
+  if (sizeof(T) == 4)
+    return wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta), (float)alpha);
+  return wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_obj(Params P) {
-  __shared__ double scr[kThreads / 32];
+  __shared__ double scr5[5 * (kThreads / 32)];
   const Ctrl* C = P.ctrl;
   if (C->stopped || (C->t % P.S) != 0) return;
-  obj_partial<T>(P, C->nb_shape, blockIdx.x, gridDim.x, P.objpart + OBJ_W * blockIdx.x);
+  double dpart = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < P.E;
+       e += (int64_t)gridDim.x * kThreads)
+    dpart += entry_dev_cached<T>(P, P.ep[e], C->nb_shape);
+  obj_partial<T>(P, C->nb_shape, blockIdx.x, gridDim.x, P.objpart + OBJ_W * blockIdx.x, dpart);
   unsigned int* tk = P.tickets + 2 * P.CT + 1;
   if (!last_block_ticket(tk, gridDim.x)) return;
-  const double dev = sum_parts<kThreads>(P.objpart + 0, gridDim.x, OBJ_W, scr);
-  const double nb = sum_parts<kThreads>(P.objpart + 1, gridDim.x, OBJ_W, scr);
-  const double nv = sum_parts<kThreads>(P.objpart + 2, gridDim.x, OBJ_W, scr);
-  const double ng = sum_parts<kThreads>(P.blocksum + 0, P.R, 2, scr);
-  const double nu = sum_parts<kThreads>(P.blocksum + 1, P.R, 2, scr);
+  // one pass over all five partial arrays, one block reduction
+  double v5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) {
+    const double* op = P.objpart + (int64_t)OBJ_W * i;
+    v5[0] += __ldcg(op); v5[1] += __ldcg(op + 1); v5[2] += __ldcg(op + 2);
+  }
+  for (int64_t i = threadIdx.x; i < P.R; i += kThreads) {
+    v5[3] += __ldcg(P.blocksum + 2 * i); v5[4] += __ldcg(P.blocksum + 2 * i + 1);
+  }
+  block_sum_vec<5>(v5, scr5);
+  const double dev = v5[0], nb = v5[1], nv = v5[2], ng = v5[3], nu = v5[4];
   if (threadIdx.x == 0) {
     P.rec[R_DEV] = dev;
     P.rec[R_NGAM] = ng;
@@ -45,7 +128,7 @@ GMF_D const double* rec_of(const Params& P, const unsigned char* gathered, int r
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned char* gathered) {
-  __shared__ double scr[kThreads / 32];
+  __shared__ double scr2[2 * (kThreads / 32)];
   const Ctrl C = *P.ctrl;
   if (C.stopped) return;
   if (!gathered) gathered = reinterpret_cast<const unsigned char*>(P.rec);
@@ -87,13 +170,15 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
         const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_row) + i * Kr + k,
                                     tptr<T>(P.hb_row) + i * Kr + k, gs, hs,
                                     (double)P.m / (double)nJ, k < P.q ? P.lam_g : P.lam_u, rho, at);
+        const int32_t sl = P.rslot[i];   // the objective cache slot of this row
+        if (sl >= 0) tptr<T>(P.ecache)[(int64_t)sl * (P.nkb + 4) + (k < P.q ? P.p + P.d + k : P.p + (k - P.q))] = nvv;
         const double sq = (double)nvv * (double)nvv;
         if (k < P.q) rg = sq; else ru = sq;
       }
     }
-    rg = block_sum<kThreads>(rg, scr);
-    ru = block_sum<kThreads>(ru, scr);
-    if (threadIdx.x == 0) { P.rnpart[2 * bx] = rg; P.rnpart[2 * bx + 1] = ru; }
+    double v2[2] = {rg, ru};
+    block_sum_vec<2>(v2, scr2);
+    if (threadIdx.x == 0) { P.rnpart[2 * bx] = v2[0]; P.rnpart[2 * bx + 1] = v2[1]; }
   } else if (bx < P.n_row_ctas + P.n_col_ctas) {
     const int64_t e = (int64_t)(bx - P.n_row_ctas) * kThreads + threadIdx.x;
     if (e < P.m * Kc) {
@@ -113,8 +198,10 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
           gs += ldcg_t<T>(cp + k);
           hs += ldcg_t<T>(cp + Kc + k);
         }
-        ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k, tptr<T>(P.hb_col) + j * Kc + k, gs, hs,
-                      P.rbscale[blk], k < P.p ? P.lam_b : P.lam_v, rho, at);
+        const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k,
+                                    tptr<T>(P.hb_col) + j * Kc + k, gs, hs, P.rbscale[blk],
+                                    k < P.p ? P.lam_b : P.lam_v, rho, at);
+        tptr<T>(P.vpad)[j * P.nkb + k] = nvv;   // the objective's padded [b | v | z]
       }
     }
   }
@@ -124,8 +211,12 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
   if (!last_block_ticket(tk, gridDim.x)) return;
   double g2 = 0.0, u2 = 0.0;
   if (upd) {
-    g2 = sum_parts<kThreads>(P.rnpart, P.n_row_ctas, 2, scr);
-    u2 = sum_parts<kThreads>(P.rnpart + 1, P.n_row_ctas, 2, scr);
+    double v2[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < P.n_row_ctas; i += kThreads) {
+      v2[0] += __ldcg(P.rnpart + 2 * i); v2[1] += __ldcg(P.rnpart + 2 * i + 1);
+    }
+    block_sum_vec<2>(v2, scr2);
+    g2 = v2[0]; u2 = v2[1];
   }
   if (threadIdx.x != 0) return;
   if (D.boundary) {
@@ -266,6 +357,17 @@ int launch_blocknorm(const Params& P, int dtype, cudaStream_t st) {
   if (dtype == GMF_F64) k_blocknorm<double><<<(unsigned)P.R, kThreads, 0, st>>>(P);
   else k_blocknorm<float><<<(unsigned)P.R, kThreads, 0, st>>>(P);
   GMF_LAUNCH_CHECK("k_blocknorm");
+  return GMF_OK;
+}
+
+int launch_cache_fill(const Params& P, int dtype, cudaStream_t st) {
+  const int64_t work = P.nslots > P.m * P.nkb ? P.nslots : P.m * P.nkb;
+  unsigned b = (unsigned)((work + kThreads - 1) / kThreads);
+  if (b > 4 * kSMs) b = 4 * kSMs;
+  if (b < 1) b = 1;
+  if (dtype == GMF_F64) k_cache_fill<double><<<b, kThreads, 0, st>>>(P);
+  else k_cache_fill<float><<<b, kThreads, 0, st>>>(P);
+  GMF_LAUNCH_CHECK("k_cache_fill");
   return GMF_OK;
 }
 

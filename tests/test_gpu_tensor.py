@@ -214,3 +214,37 @@ def test_streaming_run_equals_resident_run_bitwise():
             fit.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-4)])
+def test_per_step_path_matches_persistent(monkeypatch, dtype, tol):
+    """The per-step kernels (k_obj / k_grad / k_colrec / k_apply -- the path
+    every rank of a multi-rank fit runs) reproduce the persistent k_fit: same
+    objective trace and final factors, with the per-step objective read from
+    the row-slot / padded-column caches that k_apply keeps current."""
+    from paper_2412_20509_b200.engine import DeviceFit, Schedule
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    y, x, z, off, st = _problem(13, 500, 150, 6, 2, 1, "nb", True)
+    data = gk.ResponseMatrix(csr=dense_to_csr(y), shape=y.shape)
+    covs = gk.CovariateSet(x=x, z=z, n=500, m=150)
+    cfg = gk.SgdConfig(max_epochs=40, mb_rows=90, mb_cols=150, tol=1e-30, seed=4)
+    sch = Schedule(500, 150, cfg)
+    out = []
+    for per_step in (False, True):
+        if per_step:
+            monkeypatch.setenv("GMF_NO_PERSISTENT", "1")
+        fit = DeviceFit(data, covs, gk.NegBinomial(2.0), gk.Log(), gk.PenaltyConfig(), cfg, st,
+                        schedule=sch, offset=off, dtype=dtype, est_alpha=True)
+        try:
+            fit.reset()
+            fit.run(40)
+            status = fit.status()
+            out.append((fit.trace(int(status.trace_len))[0],
+                        fit.theta_row.cpu().numpy().copy(), fit.theta_col.cpu().numpy().copy()))
+        finally:
+            fit.close()
+        monkeypatch.delenv("GMF_NO_PERSISTENT", raising=False)
+    assert len(out[0][0]) == len(out[1][0]) > 3
+    assert np.allclose(out[0][0], out[1][0], rtol=tol, atol=0)
+    for a, b in zip(out[0][1:], out[1][1:]):
+        assert normwise(b, a) < tol
