@@ -321,6 +321,7 @@ def main():
         oc = per[:, 5:7] / nst    # objective sub-phase clocks per step
         phases["objective_subphases_us(mean over CTAs)"] = {
             "loop": float(oc[:, 0].mean() / 1965.0), "block_reduce": float(oc[:, 1].mean() / 1965.0)}
+        phases["p2_totals_us(mean over CTAs, SM clocks)"] = float((per[:, 7] / nst).mean() / 1965.0)
         kc = per[:, 8:16] / nst   # K1 sub-phase clocks per step (tensor path)
         if kc.any():
             names_k = ["col_operands", "staging_wait", "y_a1_gemm1", "d2_readout_b3", "barrier",

@@ -290,6 +290,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
   const int64_t o_gbar = take(16);
+  const int64_t o_tot = take(64);                               // phase-2 totals (last arriver)
   const int64_t o_ready = take(8);                              // streaming ready counter
   const int64_t E1 = bufs->n_eval > 0 ? bufs->n_eval : 1;
   const int64_t o_esr = take(E1 * 8);                          // eval rows, sorted
@@ -317,6 +318,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.rnpart = (double*)(base + o_rnp);
   P.cnpart = (double*)(base + o_cnp);
   P.gbar = (unsigned int*)(base + o_gbar);
+  P.totals = (double*)(base + o_tot);
   P.ready = (const unsigned long long*)(base + o_ready);
   P.blocksum = (double*)(base + o_bs);
   P.snap_ver = (long long*)(base + o_lm);

@@ -106,6 +106,7 @@ struct Params {
   void* colpart;       // [CT][RS][TC][2 Kc]            T
   double* nbpart;      // [CT * RS][2]
   unsigned int* tickets;   // [CT] col tiles, [CT] grad-global, [CT+1] obj, [CT+2] apply
+  double* totals;          // [7] phase-2 totals, reduced once by the barrier's last arriver
   unsigned int* gbar;      // software grid barrier of the tensor-core fit kernel: count, generation, abort
   double* rec;         // rank record: REC_HDR doubles + [jmax][2 Kc] T
   int64_t rec_stride;  // bytes between gathered records
@@ -181,7 +182,7 @@ GMF_D double block_sum_all(double v, double* scr) {
   return s;
 }
 
-// block-wide sums of N values at once, broadcast to every thread; xor
+// block-wide sums of N values at once (blocks of kThreads), broadcast to every thread; xor
 // butterflies give bitwise-identical lane results (a+b == b+a), then a fixed
 // warp order (scr >= N * warps doubles)
 template <int N>
@@ -198,12 +199,17 @@ GMF_D void block_sum_vec(double (&v)[N], double* scr) {
     for (int i = 0; i < N; ++i) scr[wid * N + i] = v[i];
   }
   __syncthreads();
+  // warps outer, values inner: N independent add chains (same order per value)
+  double s[N];
   #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scr[w * N + i];
-    v[i] = s;
+  for (int i = 0; i < N; ++i) s[i] = 0.0;
+  #pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    #pragma unroll
+    for (int i = 0; i < N; ++i) s[i] += scr[w * N + i];
   }
+  #pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = s[i];
   __syncthreads();
 }
 

@@ -240,7 +240,16 @@ GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long t
 // delaying the arriving thread's fence.
 struct SoftArrival { unsigned int gen; int last; };
 
-GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, SoftArrival& a) {
+GMF_D void soft_grid_release(unsigned int* gb) {   // one thread of the last arriver
+  atomicExch(gb, 0u);
+  __threadfence();
+  atomicAdd(gb + 1, 1u);
+}
+
+// hold: the last arriver does not open the barrier; it sees every other
+// CTA's released writes (fence after its counting atomic), does work the
+// whole grid needs once, and opens the barrier with soft_grid_release
+GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, SoftArrival& a, bool hold = false) {
   __shared__ SoftArrival s_a;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -249,9 +258,8 @@ GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, SoftArrival& a) {
     __threadfence();   // release this CTA's writes
     r.last = atomicAdd(gb, 1u) == G - 1;
     if (r.last) {
-      atomicExch(gb, 0u);
-      __threadfence();
-      atomicAdd(gb + 1, 1u);
+      if (hold) __threadfence();   // acquire side of the other CTAs' releases
+      else soft_grid_release(gb);
     }
     s_a = r;
   }
@@ -278,6 +286,10 @@ GMF_D bool soft_grid_wait(unsigned int* gb, const SoftArrival& a, unsigned long 
   return ok != 0;
 }
 
+#ifndef GMF_TOTALS_HOLD
+#define GMF_TOTALS_HOLD 1   // the barrier's last arriver reduces the phase-2 totals once
+#endif
+
 constexpr unsigned long long kProbeTimeoutNs = 50ull * 1000 * 1000;        // residency probe
 constexpr unsigned long long kBarrierTimeoutNs = 10ull * 1000 * 1000 * 1000;  // hang guard
 
@@ -293,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
 k_fit(Params P, long long n_steps) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double scr[8 * (kThreads / 32)];
+  __shared__ double s_tot[8];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_bar[2];
   constexpr int TC = Tile<T>::TC;
@@ -432,8 +445,59 @@ k_fit(Params P, long long n_steps) {
     // coordinates (theta, EMA state) and the block's snapshot version.  The
     // tensor-core kernel's split barrier arrives first, so these loads do not
     // hold up the arriving thread's release fence.
+    // totals: deviance, ||B||^2, ||V||^2, ||Gamma||^2, ||U||^2, NB moment
+    // sums (one merged reduction of the per-CTA partials, fixed order)
+    auto phase2_totals = [&](double (&v7)[7]) {
+      #pragma unroll
+      for (int k = 0; k < 7; ++k) v7[k] = 0.0;
+      {   // two slots per thread per pass, every load of a pass in flight together
+        const bool tb = boundary, tn = run_grad && P.est_alpha;
+        const int64_t nmax = (int64_t)G > P.R ? (int64_t)G : P.R;
+        for (int64_t i = threadIdx.x; i < nmax; i += 2 * kThreads) {
+          double l[2][7];
+          #pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int64_t ii = i + u * kThreads;
+            const bool ig = ii < G, ir = ii < P.R;
+            const int64_t ic = ig ? ii : 0, irc = ir ? ii : 0;
+            const double o0 = __ldcg(P.objpart + OBJ_W * ic);
+            const double c0 = __ldcg(P.cnpart + 2 * ic), c1 = __ldcg(P.cnpart + 2 * ic + 1);
+            const double b0 = __ldcg(P.blocksum + 2 * irc), b1 = __ldcg(P.blocksum + 2 * irc + 1);
+            const double n0 = __ldcg(P.nbpart + 2 * ic), n1 = __ldcg(P.nbpart + 2 * ic + 1);
+            l[u][0] = tb && ig ? o0 : 0.0;
+            l[u][1] = tb && ig ? c0 : 0.0;
+            l[u][2] = tb && ig ? c1 : 0.0;
+            l[u][3] = tb && ir ? b0 : 0.0;
+            l[u][4] = tb && ir ? b1 : 0.0;
+            l[u][5] = tn && ig ? n0 : 0.0;
+            l[u][6] = tn && ig ? n1 : 0.0;
+          }
+          #pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            #pragma unroll
+            for (int k = 0; k < 7; ++k) v7[k] += l[u][k];
+          }
+        }
+      }
+      block_sum_vec<7>(v7, scr);
+    };
     SoftArrival arr;
-    if constexpr (TCM) soft_grid_arrive(P.gbar, (unsigned int)G, arr);
+    if constexpr (TCM) {
+      // the last CTA to arrive reduces the totals once for the grid, then
+      // opens the barrier; the others read 7 doubles after their wait
+      soft_grid_arrive(P.gbar, (unsigned int)G, arr, GMF_TOTALS_HOLD != 0);
+      if (GMF_TOTALS_HOLD && arr.last) {
+        double t7[7];
+        phase2_totals(t7);
+        if (threadIdx.x == 0) {
+          #pragma unroll
+          for (int k = 0; k < 7; ++k) { s_tot[k] = t7[k]; P.totals[k] = t7[k]; }
+          __threadfence();
+          soft_grid_release(P.gbar);
+        }
+        __syncthreads();
+      }
+    }
     const long long sv = blk >= 0 ? __ldcg(P.snap_ver + blk) : 0;
     const int64_t rI0 = blk >= 0 ? P.rbp[blk] : 0;
     const int64_t nIK = blk >= 0 ? (P.rbp[blk + 1] - rI0) * Kr : 0;
@@ -466,25 +530,25 @@ k_fit(Params P, long long n_steps) {
     // ------------------------- phase 2 -------------------------
     // totals, redundantly in every CTA: deviance, ||B||^2, ||V||^2,
     // ||Gamma||^2, ||U||^2, NB moment sums (one merged reduction)
-    double v7[7] = {0, 0, 0, 0, 0, 0, 0};
-    if (boundary) {
-      for (int i = threadIdx.x; i < G; i += kThreads) {
-        v7[0] += __ldcg(P.objpart + OBJ_W * i);
-        v7[1] += __ldcg(P.cnpart + 2 * i);
-        v7[2] += __ldcg(P.cnpart + 2 * i + 1);
+    const long long ct0 = profc ? clock64() : 0;
+    double v7[7];
+    if constexpr (TCM && !GMF_TOTALS_HOLD) {
+      phase2_totals(v7);
+    } else if constexpr (TCM) {
+      if (arr.last) {
+        #pragma unroll
+        for (int k = 0; k < 7; ++k) v7[k] = s_tot[k];
+      } else {
+        if (threadIdx.x < 7) s_tot[threadIdx.x] = __ldcg(P.totals + threadIdx.x);
+        __syncthreads();
+        #pragma unroll
+        for (int k = 0; k < 7; ++k) v7[k] = s_tot[k];
       }
-      for (int64_t r = threadIdx.x; r < P.R; r += kThreads) {
-        v7[3] += __ldcg(P.blocksum + 2 * r);
-        v7[4] += __ldcg(P.blocksum + 2 * r + 1);
-      }
+    } else {
+      phase2_totals(v7);
     }
-    if (run_grad && P.est_alpha) {
-      for (int i = threadIdx.x; i < G; i += kThreads) {
-        v7[5] += __ldcg(P.nbpart + 2 * i);
-        v7[6] += __ldcg(P.nbpart + 2 * i + 1);
-      }
-    }
-    block_sum_vec<7>(v7, scr);
+    if (profc && threadIdx.x == 0)   // phase-2 totals (SM clocks)
+      atomicAdd(P.prof + 16 + 16 * blockIdx.x + 7, (unsigned long long)(clock64() - ct0));
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 6, t_b - t_a); }
     const Decision D = decide_from(P, C, v7[0], v7[3], v7[4], v7[1], v7[2]);
     const bool upd = !D.stop;
@@ -560,60 +624,65 @@ k_fit(Params P, long long n_steps) {
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 7, t_b - t_a); }
-    // columns of block J: a group of 8 lanes per coordinate splits the K1 row
-    // splits (all loads in flight), fixed xor-butterfly order inside the
-    // group; the group's first lane snapshots and updates
+    // columns of block J.  A task is CG whole columns of one K1 column tile:
+    // their partials are CG * 2Kc contiguous values per row split, so the
+    // CTA's lanes read them coalesced (lane -> value, S lane groups -> row
+    // splits, all of a thread's loads in flight), reduce across the S groups
+    // in shared memory (K1's, idle in phase 2) in a fixed order, and the
+    // first CG * Kc threads update one coordinate each
     if (upd) {
       const int64_t j0 = j0s, nJ = nJs;
       const double s_col = s_col_pre;
       const T* cpart = tptr<T>(P.colpart);
       const int64_t rstride = (int64_t)TC * kk;
-      const int sub = lane & 7;
-      const int64_t gg = gtid >> 3, ng = gstride >> 3;
-      const int64_t ne = nJ * Kc;
-      const int64_t rounds = (ne + ng - 1) / ng;   // uniform trip count (shuffles)
-      for (int64_t rd = 0; rd < rounds; ++rd) {
-        const int64_t e = gg + rd * ng;
-        const bool live = e < ne;
-        const int64_t ee = live ? e : 0;
-        const uint32_t uee = (uint32_t)ee, pos32 = uee / (uint32_t)Kc;   // ne < 2^31
-        const int64_t pos = pos32;
-        const int k = (int)(uee - pos32 * (uint32_t)Kc);
-        const T* base = cpart + ((pos / TC) * RS * TC + (pos % TC)) * kk + k;
-        constexpr int MAXU = 16;   // 128 row splits per pass
-        T g = T(0), h = T(0);
-        for (int r0 = 0; r0 < RS; r0 += 8 * MAXU) {
-          T gv[MAXU], hv[MAXU];
-          #pragma unroll
-          for (int u = 0; u < MAXU; ++u) {   // clamped addresses: all loads in flight
-            const int r = r0 + sub + 8 * u;
-            const int rc = r < RS ? r : 0;
-            const T gx = ldcg_t<T>(base + rc * rstride);
-            const T hx = ldcg_t<T>(base + rc * rstride + Kc);
-            gv[u] = r < RS ? gx : T(0);
-            hv[u] = r < RS ? hx : T(0);
+      int CG = 1;
+      while (2 * CG * kk <= 64 && 2 * CG <= TC) CG *= 2;   // divides TC (a power of two)
+      const int EQ = CG * kk, S = kThreads / EQ;
+      const int qv = threadIdx.x % EQ, sg = threadIdx.x / EQ;
+      T* red = reinterpret_cast<T*>(smem);
+      const int64_t ntask = (nJ + CG - 1) / CG;
+      constexpr int MAXU = 16;
+      for (int64_t task = blockIdx.x; task < ntask; task += G) {
+        const int64_t pos0 = task * CG;
+        if (sg < S) {
+          const T* base = cpart + ((pos0 / TC) * RS * TC + (pos0 % TC)) * kk + qv;
+          T acc = T(0);
+          for (int r0 = sg; r0 < RS; r0 += S * MAXU) {
+            T v[MAXU];
+            #pragma unroll
+            for (int u = 0; u < MAXU; ++u) {
+              const int r = r0 + u * S;
+              v[u] = r < RS ? ldcg_t<T>(base + r * rstride) : T(0);
+            }
+            #pragma unroll
+            for (int u = 0; u < MAXU; ++u) acc += v[u];
           }
-          #pragma unroll
-          for (int u = 0; u < MAXU; ++u) { g += gv[u]; h += hv[u]; }
+          red[sg * EQ + qv] = acc;
         }
-        #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          g += __shfl_xor_sync(0xffffffffu, g, o);
-          h += __shfl_xor_sync(0xffffffffu, h, o);
-        }
-        if (live && sub == 0) {
-          const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
-          T* th = tptr<T>(P.th_col) + j * Kc + k;
-          if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
-          const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k,
-                                      tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
-                                      k < P.p ? P.lam_b : P.lam_v, rho, at);
-          tptr<T>(P.vpad)[j * NK + k] = nvv;   // the objective's padded copy of [b | v | z]
-          if constexpr (TCM) {
-            if (P.colimg_on) tc::colimg_write<NK>(P, j, k, (float)nvv);
+        __syncthreads();
+        if (threadIdx.x < CG * Kc) {
+          const int c = threadIdx.x / Kc, k = threadIdx.x - c * Kc;
+          const int64_t pos = pos0 + c;
+          if (pos < nJ) {
+            T g = T(0), h = T(0);
+            for (int ss = 0; ss < S; ++ss) {
+              g += red[ss * EQ + c * kk + k];
+              h += red[ss * EQ + c * kk + Kc + k];
+            }
+            const int64_t j = P.col_identity ? pos : (int64_t)P.cidx[j0 + pos];
+            T* th = tptr<T>(P.th_col) + j * Kc + k;
+            if (D.snap) tptr<T>(P.sn_col)[j * Kc + k] = *th;
+            const T nvv = ema_update<T>(P, th, tptr<T>(P.gb_col) + j * Kc + k,
+                                        tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
+                                        k < P.p ? P.lam_b : P.lam_v, rho, at);
+            tptr<T>(P.vpad)[j * NK + k] = nvv;   // the objective's padded copy of [b | v | z]
+            if constexpr (TCM) {
+              if (P.colimg_on) tc::colimg_write<NK>(P, j, k, (float)nvv);
+            }
+            nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
           }
-          nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
         }
+        __syncthreads();
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 8, t_b - t_a); }
