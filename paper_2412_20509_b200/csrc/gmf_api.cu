@@ -289,7 +289,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ft = take(64);
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
-  const int64_t o_gbar = take(16);
+  const int64_t o_gbar = take(32);
   const int64_t o_tot = take(64);                               // phase-2 totals (last arriver)
   const int64_t o_ready = take(8);                              // streaming ready counter
   const int64_t E1 = bufs->n_eval > 0 ? bufs->n_eval : 1;
@@ -439,7 +439,7 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
     GMF_CUDA(cudaMemsetAsync(P.hb_col, 0, cb, st));
   }
   GMF_CUDA(cudaMemsetAsync((void*)P.ready, 0, 8, st));
-  GMF_CUDA(cudaMemsetAsync((void*)P.gbar, 0, 16, st));
+  GMF_CUDA(cudaMemsetAsync((void*)P.gbar, 0, 32, st));
   int rc = launch_blocknorm(P, h->desc.dtype, st);
   if (!rc) rc = launch_cache_fill(P, h->desc.dtype, st);   // the per-step path's objective caches
   if (rc) return rc;

@@ -206,63 +206,79 @@ GMF_D unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   return v;
 }
 
-GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned long long timeout_ns) {
+// Barrier state (P.gbar, zeroed at every launch): u32 [1] generation,
+// [2] abort flag, u64 at [4] arrivals (monotonic: the k-th barrier of a
+// launch completes at G * k arrivals, so no reset RMW is needed).  Every CTA
+// counts its barriers in `gen`.  Release: fence.acq_rel + the counting
+// atomic; the completing arrival opens the barrier with one generation
+// increment after its own fence; waiters spin on relaxed loads (an acquire
+// load per iteration would invalidate the SM's L1 every time) and fence once.
+GMF_D void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+GMF_D unsigned long long* gbar_count(unsigned int* gb) {
+  return reinterpret_cast<unsigned long long*>(gb + 4);
+}
+
+GMF_D bool soft_spin(unsigned int* gb, unsigned int gen, unsigned long long timeout_ns) {
+  const unsigned long long t0 = gtimer();
+  while (ld_relaxed_u32(gb + 1) == gen) {
+    if (ld_relaxed_u32(gb + 2)) return false;
+    if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); return false; }
+  }
+  return true;
+}
+
+GMF_D bool soft_grid_sync(unsigned int* gb, unsigned int G, unsigned int& gen,
+                          unsigned long long timeout_ns) {
   __shared__ int ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     int res = 1;
-    const unsigned int gen = ld_relaxed_u32(gb + 1);
-    __threadfence();   // release this CTA's writes
-    if (atomicAdd(gb, 1u) == G - 1) {
-      atomicExch(gb, 0u);
-      __threadfence();
+    fence_acq_rel_gpu();   // release this CTA's writes
+    const unsigned long long target = (unsigned long long)G * (gen + 1);
+    if (atomicAdd(gbar_count(gb), 1ull) == target - 1) {
+      fence_acq_rel_gpu();   // everyone's writes (acquire) -> the opening (release)
       atomicAdd(gb + 1, 1u);
     } else {
-      // spin on relaxed loads (an acquire load per iteration would invalidate
-      // the SM's L1 every time); one acquire after the wait
-      const unsigned long long t0 = gtimer();
-      while (ld_relaxed_u32(gb + 1) == gen) {
-        if (ld_relaxed_u32(gb + 2)) { res = 0; break; }
-        if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); res = 0; break; }
-      }
+      res = soft_spin(gb, gen, timeout_ns) ? 1 : 0;
+      fence_acq_rel_gpu();   // acquire: later loads see other CTAs' writes
     }
-    (void)ld_acquire_u32(gb + 1);   // acquire: later loads see other CTAs' writes
-    __threadfence();
     ok = res;
   }
+  ++gen;
   __syncthreads();
   return ok != 0;
 }
 
 // Split form: arrive (release this CTA's writes, count in) and wait (spin,
 // acquire).  Loads issued between the two -- inputs of the next phase that
-// the current phase does not write -- overlap the barrier instead of
-// delaying the arriving thread's fence.
+// the current phase does not write -- overlap the barrier.
 struct SoftArrival { unsigned int gen; int last; };
 
 GMF_D void soft_grid_release(unsigned int* gb) {   // one thread of the last arriver
-  atomicExch(gb, 0u);
-  __threadfence();
+  fence_acq_rel_gpu();
   atomicAdd(gb + 1, 1u);
 }
 
 // hold: the last arriver does not open the barrier; it sees every other
 // CTA's released writes (fence after its counting atomic), does work the
 // whole grid needs once, and opens the barrier with soft_grid_release
-GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, SoftArrival& a, bool hold = false) {
+GMF_D void soft_grid_arrive(unsigned int* gb, unsigned int G, unsigned int& gen, SoftArrival& a,
+                            bool hold = false) {
   __shared__ SoftArrival s_a;
   __syncthreads();
   if (threadIdx.x == 0) {
     SoftArrival r;
-    r.gen = ld_relaxed_u32(gb + 1);
-    __threadfence();   // release this CTA's writes
-    r.last = atomicAdd(gb, 1u) == G - 1;
+    r.gen = gen;
+    fence_acq_rel_gpu();   // release this CTA's writes
+    const unsigned long long target = (unsigned long long)G * (gen + 1);
+    r.last = atomicAdd(gbar_count(gb), 1ull) == target - 1;
     if (r.last) {
-      if (hold) __threadfence();   // acquire side of the other CTAs' releases
+      if (hold) fence_acq_rel_gpu();   // acquire side of the other CTAs' releases
       else soft_grid_release(gb);
     }
     s_a = r;
   }
+  ++gen;
   __syncthreads();
   a = s_a;
 }
@@ -272,14 +288,9 @@ GMF_D bool soft_grid_wait(unsigned int* gb, const SoftArrival& a, unsigned long 
   if (threadIdx.x == 0) {
     int res = 1;
     if (!a.last) {
-      const unsigned long long t0 = gtimer();
-      while (ld_relaxed_u32(gb + 1) == a.gen) {
-        if (ld_relaxed_u32(gb + 2)) { res = 0; break; }
-        if (gtimer() - t0 > timeout_ns) { atomicExch(gb + 2, 1u); res = 0; break; }
-      }
+      res = soft_spin(gb, a.gen, timeout_ns) ? 1 : 0;
+      fence_acq_rel_gpu();   // acquire
     }
-    (void)ld_acquire_u32(gb + 1);   // acquire: later loads see other CTAs' writes
-    __threadfence();
     ok = res;
   }
   __syncthreads();
@@ -313,9 +324,10 @@ k_fit(Params P, long long n_steps) {
   if (C.stopped) return;
   tc::Ctx tcx;
   const int G = gridDim.x;
+  unsigned int bgen = 0;   // software barriers passed by this CTA (P.gbar zeroed per launch)
   auto gsync = [&](unsigned long long timeout) -> bool {
     if constexpr (TCM) {
-      return soft_grid_sync(P.gbar, (unsigned int)G, timeout);
+      return soft_grid_sync(P.gbar, (unsigned int)G, bgen, timeout);
     } else {
       (void)timeout;
       cg::this_grid().sync();
@@ -485,15 +497,14 @@ k_fit(Params P, long long n_steps) {
     if constexpr (TCM) {
       // the last CTA to arrive reduces the totals once for the grid, then
       // opens the barrier; the others read 7 doubles after their wait
-      soft_grid_arrive(P.gbar, (unsigned int)G, arr, GMF_TOTALS_HOLD != 0);
+      soft_grid_arrive(P.gbar, (unsigned int)G, bgen, arr, GMF_TOTALS_HOLD != 0);
       if (GMF_TOTALS_HOLD && arr.last) {
         double t7[7];
         phase2_totals(t7);
         if (threadIdx.x == 0) {
           #pragma unroll
           for (int k = 0; k < 7; ++k) { s_tot[k] = t7[k]; P.totals[k] = t7[k]; }
-          __threadfence();
-          soft_grid_release(P.gbar);
+          soft_grid_release(P.gbar);   // fence, then open
         }
         __syncthreads();
       }
@@ -863,7 +874,7 @@ int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, 
   Q.colimg_on = P.tcm && P.colimg != nullptr;   // images maintained by k_fit's own updates
   void* args[] = {(void*)&Q, (void*)&n_steps};
   if (P.tcm) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
-    GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 4 * sizeof(unsigned int), st));
+    GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 32, st));
     GMF_CUDA(cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
   } else {
     GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
