@@ -225,6 +225,14 @@ GMF_D double sum_parts(const double* parts, int64_t n, int64_t stride, double* s
 // ---------------------------------------------------------------------------
 // tracker decision (optim.py:301-338), from objective totals
 // ---------------------------------------------------------------------------
+// a mod b for a, b >= 0 through the 32-bit path whenever both fit (a 64-bit
+// remainder by a runtime divisor is a long software sequence)
+GMF_D long long mod_nn(long long a, long long b) {
+  if ((((unsigned long long)a | (unsigned long long)b) >> 32) == 0)
+    return (long long)((unsigned int)a % (unsigned int)b);
+  return a % b;
+}
+
 struct Decision {
   double obj;
   int boundary, snap, stop, conv, div, div_init, streak;
@@ -234,7 +242,7 @@ GMF_D Decision decide_from(const Params& P, const Ctrl& C, double dev, double ng
                            double nb, double nv) {
   Decision D;
   D.obj = 0.0;
-  D.boundary = (C.t % P.S) == 0;
+  D.boundary = mod_nn(C.t, P.S) == 0;
   D.snap = 0; D.stop = 0; D.conv = C.converged; D.div = 0; D.div_init = 0; D.streak = C.streak;
   if (D.boundary) {
     D.obj = P.escale * dev / (2.0 * P.phi) +
@@ -245,7 +253,7 @@ GMF_D Decision decide_from(const Params& P, const Ctrl& C, double dev, double ng
     } else if (!isfinite(D.obj)) {
       D.div = 1; D.stop = 1;
     } else {
-      if ((C.trace_len + 1) % P.snap_stride == 0) D.snap = 1;
+      if (mod_nn(C.trace_len + 1, P.snap_stride) == 0) D.snap = 1;
       const double rel = fabs(D.obj - C.last_obj) / (fabs(C.last_obj) + 1e-12);
       D.streak = rel < P.tol ? D.streak + 1 : 0;
       if (D.streak >= 2) { D.conv = 1; D.stop = 1; }

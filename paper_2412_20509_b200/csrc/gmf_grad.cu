@@ -404,10 +404,10 @@ k_fit(Params P, long long n_steps) {
   for (long long it = 0; it < n_steps; ++it) {
     const long long t = C.t;
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 0] = gtimer(); }
-    const bool boundary = (t % P.S) == 0;
+    const long long sidx = mod_nn(t, P.S);
+    const bool boundary = sidx == 0;
     const bool run_grad = t < P.max_steps;
     const long long blk = run_grad ? (long long)P.bseq[t] : -1;
-    const long long sidx = t % P.S;
     // ------------------------- phase 1 -------------------------
     if (blockIdx.x == 0 && prev_blk >= 0) {   // row norms of the block updated last step
       double v[2] = {0.0, 0.0};
@@ -631,7 +631,8 @@ k_fit(Params P, long long n_steps) {
           const int32_t sl = u < 2 ? prs[u] : P.rslot[i];
           if (sl >= 0) tptr<T>(P.ecache)[(int64_t)sl * (NK + 4) + apos] = nvv;
         }
-        nrm[k < P.q ? 0 : 1] += (double)nvv * (double)nvv;
+        const double sq = (double)nvv * (double)nvv;   // register selects, no local array
+        if (k < P.q) nrm[0] += sq; else nrm[1] += sq;
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 7, t_b - t_a); }
@@ -690,7 +691,8 @@ k_fit(Params P, long long n_steps) {
             if constexpr (TCM) {
               if (P.colimg_on) tc::colimg_write<NK>(P, j, k, (float)nvv);
             }
-            nrm[k < P.p ? 2 : 3] += (double)nvv * (double)nvv;
+            const double sq = (double)nvv * (double)nvv;
+            if (k < P.p) nrm[2] += sq; else nrm[3] += sq;
           }
         }
         __syncthreads();
@@ -705,7 +707,8 @@ k_fit(Params P, long long n_steps) {
         if (upd && P.cbof[j] == sidx) continue;
         const T x = tc[e];
         if (D.snap) tptr<T>(P.sn_col)[e] = x;
-        nrm[(int)(e % Kc) < P.p ? 2 : 3] += (double)x * (double)x;
+        const double sq = (double)x * (double)x;
+        if ((int)(e - j * Kc) < P.p) nrm[2] += sq; else nrm[3] += sq;
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 9, t_b - t_a); }
