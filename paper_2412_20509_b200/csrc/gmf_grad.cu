@@ -408,6 +408,8 @@ k_fit(Params P, long long n_steps) {
     const bool boundary = sidx == 0;
     const bool run_grad = t < P.max_steps;
     const long long blk = run_grad ? (long long)P.bseq[t] : -1;
+    const unsigned long long rdy_pre =
+        (P.stream_mode && threadIdx.x == 0) ? ld_relaxed_u64(P.ready) : 0ull;
     // ------------------------- phase 1 -------------------------
     if (blockIdx.x == 0 && prev_blk >= 0) {   // row norms of the block updated last step
       double v[2] = {0.0, 0.0};
@@ -435,12 +437,17 @@ k_fit(Params P, long long n_steps) {
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
     if (P.stream_mode && run_grad) {
       // streaming: this step's row block is being uploaded; wait for its flag
+      // (read at the start of the step, so a block that arrived long ago
+      // costs no round trip here)
       if (threadIdx.x == 0) {
-        const unsigned long long want = (unsigned long long)t + 1, t0 = gtimer();
-        while (ld_relaxed_u64(P.ready) < want) {
-          if (gtimer() - t0 > kBarrierTimeoutNs) { atomicExch(P.gbar + 2, 1u); break; }
+        const unsigned long long want = (unsigned long long)t + 1;
+        if (rdy_pre < want) {
+          const unsigned long long t0 = gtimer();
+          while (ld_relaxed_u64(P.ready) < want) {
+            if (gtimer() - t0 > kBarrierTimeoutNs) { atomicExch(P.gbar + 2, 1u); break; }
+          }
         }
-        (void)ld_acquire_u32(P.gbar + 1);   // acquire: the uploaded block is visible
+        fence_acq_rel_gpu();   // acquire: the uploaded block is visible
       }
       __syncthreads();
     }
@@ -730,14 +737,21 @@ k_fit(Params P, long long n_steps) {
       }
       if (cow) P.snap_ver[blk] = per_now;
       *P.ctrl = N;
-      if (P.host_status) reinterpret_cast<Ctrl*>(P.host_status)[it] = N;   // per-step D2H
     }
     C = N;
     prev_blk = upd ? blk : -1;
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 3, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 4] = gtimer(); }
-    if (D.stop) break;
+    // per-step status word to pinned host memory, written after the barrier:
+    // a system-memory store ahead of a barrier's gpu-scope fence would hold
+    // that fence for a PCIe round trip
+    const bool host_w = P.host_status && blockIdx.x == 0 && threadIdx.x == 0;
+    if (D.stop) {
+      if (host_w) reinterpret_cast<Ctrl*>(P.host_status)[it] = N;
+      break;
+    }
     if (!gsync(kBarrierTimeoutNs)) break;
+    if (host_w) reinterpret_cast<Ctrl*>(P.host_status)[it] = N;
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 4, t_b - t_a); t_a = t_b; atomicAdd(P.prof + 5, 1ull); }
   }
   if (blockIdx.x == 0 && prev_blk >= 0) {
