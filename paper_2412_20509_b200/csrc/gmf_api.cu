@@ -22,7 +22,7 @@ int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, 
 int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int launch_cache_fill(const Params& P, int dtype, cudaStream_t st);
-int tile_cols(int dtype);
+int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm);
 int launch_obj(const Params& P, int dtype, cudaStream_t st);
@@ -135,7 +135,13 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int Kr = q + d, Kc = p + d, KA = p + q + d;
   h->NK = grad_bucket(KA);
   if (h->NK < 0) {
-    set_error("p+q+d = %d exceeds the fused kernel's 32-feature limit", KA);
+    set_error("p+q+d = %d exceeds the fused kernel's 64-feature limit", KA);
+    delete h;
+    return GMF_ERR_UNSUPPORTED;
+  }
+  if (h->NK > 32 && desc->dtype == GMF_F64) {
+    set_error("p+q+d = %d > 32 is supported in fp32 only (the fp64 K1 tile does not fit in "
+              "shared memory at that width)", KA);
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }
@@ -207,7 +213,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   }
   P.tcm = tc_ok && cfg->k1_impl != GMF_K1_CUDA_CORES;
 
-  const int TC = tile_cols(desc->dtype);
+  const int TC = tile_cols(desc->dtype, h->NK);
   P.TC = TC;
   P.CT = (int)((jmax + TC - 1) / TC);
   const int64_t nchunks = (nstar_max + TR - 1) / TR;

@@ -15,6 +15,11 @@ constexpr int OBJ_W = 3;                  // objective partial: (deviance, ||B||
 // threads), 64 for fp64 (4 row groups; register/smem budget)
 template <typename T> struct Tile { static constexpr int TC = 128; };
 template <> struct Tile<double> { static constexpr int TC = 64; };
+// the 64-feature bucket (K in (32, 64], fp32 only) halves the CUDA-core K1's
+// column tile so its shared memory fits
+template <typename T, int NK> struct TileK {
+  static constexpr int TC = NK > 32 ? Tile<T>::TC / 2 : Tile<T>::TC;
+};
 
 // rank record header slots (doubles)
 enum { R_DEV = 0, R_NGAM = 1, R_NU = 2, R_NB = 3, R_NV = 4, R_NBNUM = 5, R_NBDEN = 6 };

@@ -30,7 +30,7 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   __shared__ double scr[kThreads / 32];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_bar[2];
-  constexpr int TC = Tile<T>::TC;
+  constexpr int TC = TileK<T, NK>::TC;
   const Ctrl* C = P.ctrl;
   long long blk, s;
   double alpha;
@@ -319,7 +319,7 @@ k_fit(Params P, long long n_steps) {
   __shared__ double s_tot[8];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_bar[2];
-  constexpr int TC = Tile<T>::TC;
+  constexpr int TC = TileK<T, NK>::TC;
   Ctrl C = *P.ctrl;
   if (C.stopped) return;
   tc::Ctx tcx;
@@ -783,6 +783,10 @@ static void* pick(int NK, bool fit) {
     case 16: return fit ? Inst<T, FAM, 16, TCM>::fit() : Inst<T, FAM, 16, TCM>::grad();
     case 24: return fit ? Inst<T, FAM, 24, TCM>::fit() : Inst<T, FAM, 24, TCM>::grad();
     case 32: return fit ? Inst<T, FAM, 32, TCM>::fit() : Inst<T, FAM, 32, TCM>::grad();
+    case 64:   // K = p+q+d in (32, 64]: fp32 CUDA-core K1 only (c5's rank 50)
+      if constexpr (!TCM && sizeof(T) == 4)
+        return fit ? Inst<T, FAM, 64, false>::fit() : Inst<T, FAM, 64, false>::grad();
+      return nullptr;
     default: return nullptr;
   }
 }
@@ -805,16 +809,20 @@ int grad_bucket(int KA) {
   if (KA <= 16) return 16;
   if (KA <= 24) return 24;
   if (KA <= 32) return 32;
+  if (KA <= 64) return 64;
   return -1;
 }
 
-int tile_cols(int dtype) { return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC; }
+int tile_cols(int dtype, int NK) {
+  if (NK > 32) return dtype == GMF_F64 ? TileK<double, 64>::TC : TileK<float, 64>::TC;
+  return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC;
+}
 
 int64_t colimg_bytes_total(int NK, int CT) { return (int64_t)CT * tc::colimg_bytes(NK); }
 
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm) {
   if (tcm) return tc::smem_layout(NK).total;
-  return grad_smem(tile_cols(dtype), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
+  return grad_smem(tile_cols(dtype, NK), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
 }
 
 // opt in to >48 KB dynamic shared memory (outside any graph capture) and

@@ -13,10 +13,10 @@ constexpr int kCrossRows = 64;
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
 k_cross(int64_t rows, const T* __restrict__ A, int64_t lda, int a0, int a, const T* __restrict__ B,
-        int64_t ldb, int b0, int b, double* part, unsigned int* ticket, double* out) {
+        int64_t ldb, int b0, int b, int tr, double* part, unsigned int* ticket, double* out) {
   extern __shared__ double sm[];
-  double* As = sm;                       // [kCrossRows][a]
-  double* Bs = sm + kCrossRows * a;      // [kCrossRows][b]
+  double* As = sm;                       // [tr][a]  (tr <= kCrossRows rows per tile)
+  double* Bs = sm + tr * a;              // [tr][b]
   const int nout = a * b;
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per;
@@ -24,8 +24,8 @@ k_cross(int64_t rows, const T* __restrict__ A, int64_t lda, int a0, int a, const
   double acc[16];
   #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-  for (int64_t r0 = lo; r0 < hi; r0 += kCrossRows) {
-    const int nr = (int)(hi - r0 < kCrossRows ? hi - r0 : kCrossRows);
+  for (int64_t r0 = lo; r0 < hi; r0 += tr) {
+    const int nr = (int)(hi - r0 < tr ? hi - r0 : tr);
     __syncthreads();
     for (int e = threadIdx.x; e < nr * a; e += kThreads)
       As[e] = (double)A[(r0 + e / a) * lda + a0 + e % a];
@@ -100,14 +100,17 @@ int gmf_cross_rows(int dtype, int64_t rows, const void* A, int64_t lda, int32_t 
   double* part = (double*)work;
   unsigned int* ticket = (unsigned int*)((char*)work + (int64_t)kCrossCtas * a * b * 8);
   GMF_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
-  const size_t sm = (size_t)kCrossRows * (a + b) * 8;
-  if (sm > 48 * 1024) { set_error("cross_rows: too wide"); return GMF_ERR_UNSUPPORTED; }
+  // rows per shared-memory tile: up to kCrossRows within the 48 KB default
+  int tr = (48 * 1024) / ((a + b) * 8);
+  tr = tr > kCrossRows ? kCrossRows : tr;
+  if (tr < 1) { set_error("cross_rows: too wide"); return GMF_ERR_UNSUPPORTED; }
+  const size_t sm = (size_t)tr * (a + b) * 8;
   if (dtype == GMF_F64)
     k_cross<double><<<kCrossCtas, kThreads, sm, st>>>(rows, (const double*)A, lda, a0, a,
-        (const double*)B, ldb, b0, b, part, ticket, out);
+        (const double*)B, ldb, b0, b, tr, part, ticket, out);
   else
     k_cross<float><<<kCrossCtas, kThreads, sm, st>>>(rows, (const float*)A, lda, a0, a,
-        (const float*)B, ldb, b0, b, part, ticket, out);
+        (const float*)B, ldb, b0, b, tr, part, ticket, out);
   GMF_LAUNCH_CHECK("k_cross");
   return GMF_OK;
 }

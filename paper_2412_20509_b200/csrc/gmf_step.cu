@@ -51,31 +51,33 @@ __global__ void __launch_bounds__(kThreads) k_cache_fill(Params P) {
 }
 
 // deviance of entry en from the caches: eta = a_slot . c_j (16-byte loads,
-// all in flight; nkb <= 32)
+// all in flight; nkb <= 64 in passes of 32)
 template <typename T>
 GMF_D double entry_dev_cached(const Params& P, int4 en, double alpha) {
   using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   constexpr int VN = 16 / sizeof(T);
-  constexpr int MAXV = 32 / VN;
+  constexpr int MAXV = 32 / VN;   // 32 features per pass (nkb <= 64: two passes)
   const int nv = P.nkb / VN;
   const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + (int64_t)en.w * (P.nkb + 4));
   const V* c = reinterpret_cast<const V*>(tptr<T>(P.vpad) + (int64_t)en.y * P.nkb);
-  V av[MAXV], cv[MAXV];
-  #pragma unroll
-  for (int u = 0; u < MAXV; ++u) {
-    const int uu = u < nv ? u : 0;
-    av[u] = a[uu];
-    cv[u] = __ldcg(c + uu);
-  }
   const T off = tptr<T>(P.ecache)[(int64_t)en.w * (P.nkb + 4) + P.nkb];
   double eta = (double)off;
-  #pragma unroll
-  for (int u = 0; u < MAXV; ++u) {
-    if (u < nv) {
-      const T* ap = reinterpret_cast<const T*>(&av[u]);
-      const T* cp = reinterpret_cast<const T*>(&cv[u]);
-      #pragma unroll
-      for (int k = 0; k < VN; ++k) eta += (double)ap[k] * (double)cp[k];
+  for (int v0 = 0; v0 < nv; v0 += MAXV) {
+    V av[MAXV], cv[MAXV];
+    #pragma unroll
+    for (int u = 0; u < MAXV; ++u) {   // loads all in flight (clamped index)
+      const int uu = v0 + u < nv ? v0 + u : 0;
+      av[u] = a[uu];
+      cv[u] = __ldcg(c + uu);
+    }
+    #pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+      if (v0 + u < nv) {
+        const T* ap = reinterpret_cast<const T*>(&av[u]);
+        const T* cp = reinterpret_cast<const T*>(&cv[u]);
+        #pragma unroll
+        for (int k = 0; k < VN; ++k) eta += (double)ap[k] * (double)cp[k];
+      }
     }
   }
   const double wv = P.has_w ? (double)tptr<T>(P.w)[(int64_t)en.x * P.m + en.y] : 1.0;

@@ -124,3 +124,55 @@ def test_fit_with_ragged_blocks_matches_oracle(dtype, tol):
     assert normwise(rep.objective_trace, orep.objective_trace) < tol
     assert normwise(rep.nb_shape_trace, orep.nb_shape_trace) < tol
     assert normwise(final.u @ final.v.T, ofinal.u @ ofinal.v.T) < tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4)])
+def test_rank50_gradient_uses_64_feature_bucket(dtype, tol):
+    """c5's largest rank: K = p + q + d = 52 > 32 runs the fp32 CUDA-core K1
+    in the 64-feature bucket (64-column tiles; the tensor path is limited to
+    q+d, p+d <= 16)."""
+    rng = np.random.default_rng(6)
+    n, m, d = 300, 180, 50
+    st = _state(rng, n, m, d, 1, 1)
+    st.u *= 0.3
+    st.v *= 0.3
+    x = np.ones((n, 1))
+    z = np.ones((m, 1))
+    y = rng.poisson(2.0, (n, m)).astype(float)
+    errs = _check(y, st, x, z, None, np.arange(20, 260), np.arange(m), "nb", dtype, "auto", True)
+    assert max(errs.values()) < tol, errs
+
+
+def test_rank50_fp64_is_rejected_cleanly():
+    """fp64 at K > 32 does not fit the CUDA-core K1 tile: UnsupportedError."""
+    from paper_2412_20509_b200 import _lib
+    rng = np.random.default_rng(8)
+    n, m, d = 40, 30, 40
+    st = _state(rng, n, m, d, 1, 0)
+    y = rng.poisson(2.0, (n, m)).astype(float)
+    with pytest.raises(_lib.UnsupportedError):
+        gk.minibatch_gradients(st, gk.ResponseMatrix(y), gk.CovariateSet(x=np.ones((n, 1)), n=n, m=m),
+                               gk.Poisson(), gk.Log(), gk.PenaltyConfig(),
+                               gk.Minibatch(np.arange(n), np.arange(m)), dtype="f64")
+
+
+def test_rank50_fit_matches_oracle():
+    """A short fp32 fit at rank 50 (64-feature bucket, persistent kernel and
+    cached objective) follows the oracle's trace within the fp32 bounds."""
+    rng = np.random.default_rng(7)
+    n, m, d = 160, 90, 50
+    st = _state(rng, n, m, d, 1, 0)
+    st.u *= 0.2
+    st.v *= 0.2
+    x = np.ones((n, 1))
+    y = rng.poisson(2.0, (n, m)).astype(float)
+    cfg = gk.SgdConfig(max_epochs=5, mb_rows=40, mb_cols=m, tol=1e-30, seed=3)
+    final, rep = gk.fit_asgd(gk.ResponseMatrix(y), gk.CovariateSet(x=x, n=n, m=m), gk.Poisson(),
+                             gk.Log(), gk.PenaltyConfig(), cfg, st, dtype="f32")
+    pb = orc.OProblem(y, x, np.zeros((m, 0)))
+    ost = orc.OState(st.b, st.gamma, st.u, st.v, 1.0, 2.0)
+    ocfg = orc.OConfig(max_epochs=5, mb_rows=40, mb_cols=m, tol=1e-30, seed=3)
+    ofinal, orep = orc.fit_asgd(pb, orc.POISSON, orc.LOG, (0.0, 0.0, 1.0, 0.0), ocfg, ost)
+    assert len(rep.objective_trace) == len(orep.objective_trace)
+    assert normwise(rep.objective_trace, orep.objective_trace) < 1e-4
+    assert normwise(final.u @ final.v.T, ofinal.u @ ofinal.v.T) < 1e-3
