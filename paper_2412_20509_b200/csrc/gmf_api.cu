@@ -22,6 +22,7 @@ int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, 
 int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int launch_cache_fill(const Params& P, int dtype, cudaStream_t st);
+int launch_tile_index(const Params& P, int32_t* tidx, unsigned int* unsorted, cudaStream_t st);
 int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
 int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm);
@@ -306,6 +307,9 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_esl = take(E1 * 4);                          // cache slot per entry
   const int64_t o_ecache = take(E1 * (h->NK + 4) * h->tsz);    // objective row cache (<= E slots)
   const int64_t o_vpad = take(desc->m * h->NK * h->tsz);       // padded column features
+  // K1's tile index for CSR rows too dense to stage (J = all columns)
+  const bool want_tidx = desc->y_format != GMF_Y_DENSE_I32 && col_identity && desc->n > 0;
+  const int64_t o_tidx = take(want_tidx ? desc->n * (P.CT + 1) * 4 + 16 : 16);
   const bool want_img = P.tcm && col_identity;
   const int64_t o_cimg = take(want_img ? colimg_bytes_total(h->NK, P.CT) : 16);
   cudaError_t e = cudaMalloc(&h->ws, off);
@@ -374,6 +378,17 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     P.ecol = (const int32_t*)(base + o_esc);
   }
   if (bufs->n_eval <= 0 && desc->n > 0) GMF_CUDA(cudaMemset(base + o_rsl, 0xFF, desc->n * 4));   // no slots
+  P.tidx = nullptr;
+  if (want_tidx) {
+    int32_t* ti = (int32_t*)(base + o_tidx);
+    unsigned int* flag = (unsigned int*)(base + o_tidx + desc->n * (P.CT + 1) * 4);
+    GMF_CUDA(cudaMemset(flag, 0, 4));
+    rc = launch_tile_index(P, ti, flag, 0);
+    if (rc) { gmf_destroy(h); return rc; }
+    unsigned int unsorted = 1;
+    GMF_CUDA(cudaMemcpy(&unsorted, flag, 4, cudaMemcpyDeviceToHost));
+    if (!unsorted) P.tidx = ti;   // columns not increasing in some row: full-row scans
+  }
   P.ep = (const int4*)(base + o_ep);
   if (bufs->n_eval > 0) {   // tracked sample packed with its Y, once per fit
     rc = launch_eval_pack(P, (int4*)(base + o_ep), 0);

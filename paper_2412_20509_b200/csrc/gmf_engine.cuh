@@ -94,6 +94,8 @@ struct Params {
   // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;
   // each step's status word is written to mapped pinned host memory
   int stream_mode;
+  const int32_t* tidx;     // [n][CT+1] per-row start of each column tile's nonzeros (CSR,
+                           // J = all columns, rows sorted by column), else null
   // tensor-core K1 column operands (R | B1h | B1l per column tile, bf16, in the
   // shared-memory byte layout), kept current by the persistent kernel's column
   // updates when every step uses all columns; colimg_on only inside k_fit

@@ -384,10 +384,17 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
             if (pp >= 0 && cl >= 0 && cl < TC) ytile[rr * TC + cl] = stg_val(pack, w, pack ? 0 : val_b[e]);
           }
         }
-      } else {   // row range too long or chunk too dense: direct loads
+      } else {   // row range too long or chunk too dense: direct loads (this tile's range)
+        const bool tix = P.tidx != nullptr && !P.stream_mode;
         for (int rr = tid >> 5; rr < rows; rr += kThreads / 32) {
           const int64_t i = i0 + rr;
-          for (int64_t k = P.rp[i] + (tid & 31); k < P.rp[i + 1]; k += 32) {
+          int64_t k0 = P.rp[i], k1 = P.rp[i + 1];
+          if (tix) {
+            const int32_t* tr = P.tidx + i * (P.CT + 1) + ct;
+            k1 = k0 + tr[1];
+            k0 += tr[0];
+          }
+          for (int64_t k = k0 + (tid & 31); k < k1; k += 32) {
             const int col = csr_col_at(P, k);
             const int64_t pp = P.col_identity ? col : ((P.cbof[col] == s) ? (int64_t)P.cpos[col] : -1);
             const int64_t cl = pp - cbase;

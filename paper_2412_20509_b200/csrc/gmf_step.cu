@@ -362,6 +362,42 @@ int launch_blocknorm(const Params& P, int dtype, cudaStream_t st) {
   return GMF_OK;
 }
 
+// Per-row tile index of a column-sorted CSR (J = all columns): thread per
+// (row, tile boundary ct): the number of the row's nonzeros with column
+// < ct * TC (lower bound); the ct = 0 thread also checks that the row's
+// columns increase, else flags the index unusable.
+__global__ void __launch_bounds__(kThreads) k_tile_index(Params P, int32_t* tidx,
+                                                           unsigned int* unsorted) {
+  const int CT1 = P.CT + 1;
+  const int64_t total = P.n * CT1;
+  for (int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = g / CT1;
+    const int ct = (int)(g - i * CT1);
+    const int64_t lo = P.rp[i], hi = P.rp[i + 1];
+    const int64_t bound = (int64_t)ct * P.TC;
+    int64_t a = lo, b = hi;   // first k in [lo, hi) with col >= bound
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (csr_col_at(P, mid) < bound) a = mid + 1; else b = mid;
+    }
+    tidx[g] = (int32_t)((ct == P.CT ? hi : a) - lo);
+    if (ct == 0)
+      for (int64_t k = lo + 1; k < hi; ++k)
+        if (csr_col_at(P, k) <= csr_col_at(P, k - 1)) { atomicOr(unsorted, 1u); break; }
+  }
+}
+
+int launch_tile_index(const Params& P, int32_t* tidx, unsigned int* unsorted, cudaStream_t st) {
+  const int64_t total = P.n * (P.CT + 1);
+  unsigned b = (unsigned)((total + kThreads - 1) / kThreads);
+  if (b > 8 * kSMs) b = 8 * kSMs;
+  if (b < 1) b = 1;
+  k_tile_index<<<b, kThreads, 0, st>>>(P, tidx, unsorted);
+  GMF_LAUNCH_CHECK("k_tile_index");
+  return GMF_OK;
+}
+
 int launch_cache_fill(const Params& P, int dtype, cudaStream_t st) {
   const int64_t work = P.nslots > P.m * P.nkb ? P.nslots : P.m * P.nkb;
   unsigned b = (unsigned)((work + kThreads - 1) / kThreads);
