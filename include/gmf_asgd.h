@@ -97,7 +97,8 @@ typedef struct gmf_handle gmf_handle;
 typedef struct gmf_desc {
   int64_t n;            /* rows held by this rank (block-major order)          */
   int64_t m;            /* columns                                             */
-  int32_t p, q, d;      /* row design X (n x p), column design Z (m x q), rank */
+  int32_t p, q, d;      /* row design X (n x p), column design Z (m x q), rank;
+                           p+q+d <= 64 (fp64: <= 32)                           */
   int32_t dtype;        /* GMF_F32 | GMF_F64: parameters and block arithmetic  */
   int32_t family, link; /* fused path: (POISSON|NEG_BINOMIAL, LOG)             */
   int32_t y_format;     /* gmf_yfmt                                            */
