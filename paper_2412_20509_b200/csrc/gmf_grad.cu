@@ -20,11 +20,16 @@ namespace cg = cooperative_groups;
 
 namespace gmf {
 
-template <typename T> struct MinBlocks { static constexpr int v = 2; };
-template <> struct MinBlocks<double> { static constexpr int v = 1; };
+// CTAs per SM the register allocation targets: two for fp32 (the tensor-core
+// K1 and the narrow CUDA-core buckets), one for fp64 and for the 64-feature
+// bucket, whose shared-memory tile allows one CTA per SM anyway (so it may
+// use up to 255 registers instead of spilling at 128)
+template <typename T, int NK> struct MinBlocks {
+  static constexpr int v = (sizeof(T) == 8 || NK > 32) ? 1 : 2;
+};
 
 template <typename T, int FAM, int NK, bool TCM>
-__global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
+__global__ void __launch_bounds__(kThreads, MinBlocks<T, NK>::v)
 k_grad(Params P, long long xb, long long xs, double xalpha) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double scr[kThreads / 32];
@@ -312,7 +317,7 @@ GMF_D T warp_sum(T v) {
 }
 
 template <typename T, int FAM, int NK, bool TCM>
-__global__ void __launch_bounds__(kThreads, MinBlocks<T>::v)
+__global__ void __launch_bounds__(kThreads, MinBlocks<T, NK>::v)
 k_fit(Params P, long long n_steps) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double scr[8 * (kThreads / 32)];
