@@ -12,6 +12,7 @@
  *                             kernels/_ref.py:65-88 (same contract)
  *     gmf_deviance_from_mu <- kernels/_ref.py:91-108 deviance_from_mu(fcode, y, mu,
  *                             w, alpha) -> float; kernels/__init__.py:80-90
+ *     gmf_score_pairs      <- metrics.py:35-55 rel_log_rmse / rel_deviance sums
  *
  *   Level 2 (fit engine behind optim.fit_asgd, optim.py:383-489):
  *     gmf_create/gmf_destroy  own the device workspace of one fit (optim.py:409-414)
@@ -25,6 +26,11 @@
  *     gmf_run                 n x (local + apply), captured in a CUDA graph
  *     gmf_status/gmf_read_*   FitReport fields (optim.py:109-127)
  *     gmf_objective_full      model.py:268-276 penalized_objective (deviance part)
+ *     gmf_loglik_full         select.py:81-96 information_criteria: deviance and the
+ *                             NB dispersion constant (select.py:57-78) in one pass
+ *     gmf_entries_eval        select.py:141-145 _mu_at at held-out entries, fused
+ *                             with metrics.py:35-55 (cv_rank_select scoring,
+ *                             select.py:201-213)
  *   Level 3 (identify.project_constraints (A)+(B1), identify.py:59-110):
  *     gmf_cross_rows          Z = A' B over rows (Gram / cross products), fp64
  *     gmf_rows_affine         Y <- beta Y + A M, row-local apply of a small matrix
@@ -89,6 +95,13 @@ int64_t gmf_reduce_work_bytes(int64_t n);
 int gmf_deviance_from_mu(int fcode, int dtype, const void* y, const void* mu,
                          const void* w, int64_t n, double alpha, double* dev_sum,
                          void* work, void* stream);
+
+/* sums4 (device, 4 doubles) = [sum D(y, mu), sum D(y, ybar), sum log^2((1+y)/(1+mu)),
+ * sum log^2((1+y)/(1+ybar))] over n pairs (unit weights), fixed-order reduction;
+ * `work` is device scratch of gmf_score_work_bytes() bytes. */
+int64_t gmf_score_work_bytes(void);
+int gmf_score_pairs(int fcode, int dtype, const void* y, const void* mu, int64_t n, double ybar,
+                    double alpha, double* sums4, void* work, void* stream);
 
 /* ---------------------------------------------------------------- level 2 */
 
@@ -252,6 +265,18 @@ int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stre
 /* Deviance half of penalized_objective over ALL local entries at the current
  * state: *dev_sum (device double) = sum_ij w_ij D(y_ij, mu_ij). */
 int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream);
+
+/* Same pass plus the NB dispersion constant: out2 (device, 2 doubles) =
+ * [sum_ij w D(y, mu), -2 sum_ij w (sat_ij + y log y)] at the handle's nb shape
+ * (second entry 0 for Poisson).  AIC/BIC follow on the host (select.py:81-96). */
+int gmf_loglik_full(gmf_handle* h, double* out2, void* stream);
+
+/* mu = exp(eta) at n listed entries (rows: the handle's local row numbers,
+ * int64; cols: int32; device arrays).  mu_out (device, n doubles) may be NULL;
+ * with y (device, n doubles) and sums4 (device, 4 doubles) non-NULL the
+ * entries are scored as gmf_score_pairs does, against the constant ybar. */
+int gmf_entries_eval(gmf_handle* h, const int64_t* rows, const int32_t* cols, const double* y,
+                     int64_t n, double ybar, double* mu_out, double* sums4, void* stream);
 
 /* ---------------------------------------------------------------- level 3 */
 

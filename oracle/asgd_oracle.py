@@ -234,6 +234,65 @@ def penalized_objective(st, pb, fcode, lcode, lam):
     return dev / (2.0 * st.phi) + penalty_value(st, lam)
 
 
+# ---------------------------------------------------------------------------
+# model selection and held-out metrics (gmfkit/select.py, gmfkit/metrics.py)
+# ---------------------------------------------------------------------------
+
+def dispersion_constant(fcode, y, w, phi, alpha):
+    """phi/alpha part of -2 log-likelihood beyond D/phi -- select.py:57-79."""
+    from scipy.special import gammaln
+    if fcode in (GAUSSIAN, INV_GAUSSIAN):
+        return float(y.size * np.log(phi))
+    if fcode == GAMMA:
+        shape = w / phi
+        return float(2.0 * np.sum(gammaln(shape) - shape * np.log(shape) + shape))
+    if fcode == NEG_BINOMIAL:
+        a = alpha
+        sat = (gammaln(y + a) - gammaln(a) - gammaln(y + 1.0)
+               - (y + a) * np.log(y + a) + a * np.log(a))
+        ylogy = np.where(y > 0, y * np.log(np.where(y > 0, y, 1.0)), 0.0)
+        return float(-2.0 * np.sum(w * (sat + ylogy)))
+    return 0.0
+
+
+def information_criteria(st, pb, fcode, lcode, alpha):
+    """(AIC, BIC) = D/phi + c(phi) + (2 | log n_obs) k -- select.py:81-96
+    (fully observed; k = pm + qn + d(n+m) + 1, model.py:279-283)."""
+    mu = mean_of_eta(lcode, linear_predictor(st, pb))
+    y, w = pb.y.ravel(), pb.weights().ravel()
+    dev = float(np.sum(w * unit_deviance(fcode, y, mu.ravel(), alpha))) / st.phi
+    dev += dispersion_constant(fcode, y, w, st.phi, alpha)
+    n, m = pb.y.shape
+    k = pb.x.shape[1] * m + pb.z.shape[1] * n + st.u.shape[1] * (n + m) + 1
+    return dev + 2.0 * k, dev + k * np.log(n * m)
+
+
+def mu_at(st, pb, lcode, rows, cols):
+    """g^{-1}(eta) at listed entries -- select.py:141-145 (+ offset shim)."""
+    eta = np.einsum("ik,ik->i", st.u[rows], st.v[cols])
+    if pb.x.shape[1]:
+        eta = eta + np.einsum("ik,ik->i", pb.x[rows], st.b[cols])
+    if pb.z.shape[1]:
+        eta = eta + np.einsum("ik,ik->i", st.gamma[rows], pb.z[cols])
+    if pb.offset is not None:
+        eta = eta + pb.offset[rows]
+    return mean_of_eta(lcode, eta)
+
+
+def rel_log_rmse(y, mu, ybar):
+    """metrics.py:35-45."""
+    num = np.sum(np.log((1.0 + y) / (1.0 + mu)) ** 2)
+    den = np.sum(np.log((1.0 + y) / (1.0 + ybar)) ** 2)
+    return float(num / den)
+
+
+def rel_deviance(fcode, y, mu, ybar, alpha):
+    """metrics.py:48-55 (unit weights)."""
+    num = np.sum(unit_deviance(fcode, y, mu, alpha))
+    den = np.sum(unit_deviance(fcode, y, np.full_like(y, float(ybar)), alpha))
+    return float(num / den)
+
+
 def penalty_vectors(p, q, d, lam):
     """Per-coordinate ridge weights [Gamma,U] and [B,V] -- gradients.py:91-99."""
     lb, lg, lu, lv = lam

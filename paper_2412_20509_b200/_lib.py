@@ -115,6 +115,10 @@ SIGNATURES = {
     "gmf_stream_signal": (C.c_int, [_P, _i64, _P]),
     "gmf_launch_count": (_i64, [_P]),
     "gmf_objective_full": (C.c_int, [_P, _P, _P]),
+    "gmf_loglik_full": (C.c_int, [_P, _P, _P]),
+    "gmf_entries_eval": (C.c_int, [_P, _P, _P, _P, _i64, _d, _P, _P, _P]),
+    "gmf_score_work_bytes": (_i64, []),
+    "gmf_score_pairs": (C.c_int, [C.c_int, C.c_int, _P, _P, _i64, _d, _d, _P, _P, _P]),
     "gmf_cross_work_bytes": (_i64, [_i32, _i32]),
     "gmf_cross_rows": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _P, _i64, _i32, _i32,
                                  _P, _P, _P]),

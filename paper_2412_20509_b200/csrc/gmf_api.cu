@@ -32,8 +32,11 @@ int launch_blocknorm(const Params& P, int dtype, cudaStream_t st);
 int launch_gradout(const Params& P, int dtype, long long blk, long long sidx, int64_t nI,
                    int64_t nJ, void* g_row, void* h_row, void* g_col, void* h_col,
                    double* nb_sums, cudaStream_t st);
-int launch_objfull(const Params& P, int dtype, double alpha, double* part, unsigned int* ticket,
-                   double* out, cudaStream_t st);
+int launch_objfull(const Params& P, int dtype, double alpha, int with_const, double* part,
+                   unsigned int* ticket, double* out, cudaStream_t st);
+int launch_entries(const Params& P, int dtype, double alpha, const int64_t* rows,
+                   const int32_t* cols, const double* y, int64_t n, double ybar, double* mu_out,
+                   double* part, unsigned int* ticket, double* out, cudaStream_t st);
 }  // namespace gmf
 
 using namespace gmf;
@@ -292,7 +295,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_lm = take(R * 8);
   const int64_t o_rho = take(ms * 8);
   const int64_t o_alp = take(ms * 8);
-  const int64_t o_fp = take(2 * kSMs * 8);
+  const int64_t o_fp = take(4 * 2 * kSMs * 8);   // k_objfull / k_entries partials
   const int64_t o_ft = take(64);
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);
@@ -703,8 +706,39 @@ int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
   int rc = gmf_status_read(h, &s, stream);
   if (rc) return rc;
   h->launches += 1;
-  return launch_objfull(h->P, h->desc.dtype, s.nb_shape, h->full_part, h->full_ticket, dev_sum,
+  return launch_objfull(h->P, h->desc.dtype, s.nb_shape, 0, h->full_part, h->full_ticket, dev_sum,
                         (cudaStream_t)stream);
+}
+
+int gmf_loglik_full(gmf_handle* h, double* out2, void* stream) {
+  if (!h || !out2) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  gmf_status s;
+  int rc = gmf_status_read(h, &s, stream);
+  if (rc) return rc;
+  const int nb = h->desc.family == GMF_NEG_BINOMIAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!nb) GMF_CUDA(cudaMemsetAsync(out2 + 1, 0, sizeof(double), st));
+  h->launches += 1;
+  return launch_objfull(h->P, h->desc.dtype, s.nb_shape, nb, h->full_part, h->full_ticket, out2,
+                        st);
+}
+
+int gmf_entries_eval(gmf_handle* h, const int64_t* rows, const int32_t* cols, const double* y,
+                     int64_t n, double ybar, double* mu_out, double* sums4, void* stream) {
+  if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
+  if (n < 0 || (n > 0 && (!rows || !cols))) { set_error("entries: null rows/cols"); return GMF_ERR_CONFIG; }
+  if (sums4 && !y) { set_error("entries: sums need y"); return GMF_ERR_CONFIG; }
+  gmf_status s;
+  int rc = gmf_status_read(h, &s, stream);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    if (sums4) GMF_CUDA(cudaMemsetAsync(sums4, 0, 4 * sizeof(double), st));
+    return GMF_OK;
+  }
+  h->launches += 1;
+  return launch_entries(h->P, h->desc.dtype, s.nb_shape, rows, cols, y, n, ybar, mu_out,
+                        h->full_part, h->full_ticket, sums4, st);
 }
 
 void* gmf_stream_ready_ptr(gmf_handle* h) { return h ? (void*)h->P.ready : nullptr; }

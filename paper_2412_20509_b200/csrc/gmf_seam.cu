@@ -117,6 +117,38 @@ __global__ void k_deviance(int fcode, const T* __restrict__ y, const T* __restri
   }
 }
 
+// metrics.py:35-55 (rel_log_rmse, rel_deviance) on device arrays: out =
+// [sum D(y, mu), sum D(y, ybar), sum log^2((1+y)/(1+mu)), sum log^2((1+y)/(1+ybar))]
+template <typename T>
+__global__ void k_score_pairs(int fcode, const T* __restrict__ y, const T* __restrict__ mu,
+                              int64_t n, double ybar, double alpha, double* part,
+                              unsigned int* ticket, double* out) {
+  __shared__ double scratch[kThreads / 32];
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double yi = (double)y[i], mi = (double)mu[i];
+    s[0] += unit_deviance(fcode, yi, mi, alpha);
+    s[1] += unit_deviance(fcode, yi, ybar, alpha);
+    const double a = log((1.0 + yi) / (1.0 + mi)), b = log((1.0 + yi) / (1.0 + ybar));
+    s[2] += a * a;
+    s[3] += b * b;
+  }
+  for (int c = 0; c < 4; ++c) {
+    const double t = block_sum<kThreads>(s[c], scratch);
+    if (threadIdx.x == 0) part[c * gridDim.x + blockIdx.x] = t;
+  }
+  if (last_block_ticket(ticket, gridDim.x)) {
+    if (threadIdx.x < 4) {
+      double tot = 0.0;
+      for (unsigned int b = 0; b < gridDim.x; ++b) tot += ld_cg(part + threadIdx.x * gridDim.x + b);
+      out[threadIdx.x] = tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
 static int blocks_for(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   if (b < 1) b = 1;
@@ -193,6 +225,29 @@ int gmf_deviance_from_mu(int fcode, int dtype, const void* y, const void* mu, co
     k_deviance<float><<<nb, kThreads, 0, s>>>(fcode, (const float*)y, (const float*)mu,
         (const float*)w, n, alpha, part, ticket, dev_sum);
   GMF_LAUNCH_CHECK("gmf_deviance_from_mu");
+  return GMF_OK;
+}
+
+int64_t gmf_score_work_bytes(void) { return (int64_t)4 * kSeamBlocks * 8 + 64; }
+
+int gmf_score_pairs(int fcode, int dtype, const void* y, const void* mu, int64_t n, double ybar,
+                    double alpha, double* sums4, void* work, void* stream) {
+  if (fcode < 0 || fcode > GMF_NEG_BINOMIAL) { set_error("unknown family code %d", fcode); return GMF_ERR_DOMAIN; }
+  if (!dtype_ok(dtype)) return GMF_ERR_CONFIG;
+  if (!work || !sums4) { set_error("score_pairs: null work/out"); return GMF_ERR_CONFIG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = (double*)work;
+  unsigned int* ticket = (unsigned int*)((char*)work + (int64_t)4 * kSeamBlocks * 8);
+  GMF_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
+  int nb = blocks_for(n);
+  if (nb > kSeamBlocks) nb = kSeamBlocks;
+  if (dtype == GMF_F64)
+    k_score_pairs<double><<<nb, kThreads, 0, s>>>(fcode, (const double*)y, (const double*)mu, n,
+                                                  ybar, alpha, part, ticket, sums4);
+  else
+    k_score_pairs<float><<<nb, kThreads, 0, s>>>(fcode, (const float*)y, (const float*)mu, n,
+                                                 ybar, alpha, part, ticket, sums4);
+  GMF_LAUNCH_CHECK("gmf_score_pairs");
   return GMF_OK;
 }
 

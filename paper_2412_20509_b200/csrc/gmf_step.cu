@@ -296,22 +296,35 @@ __global__ void __launch_bounds__(kThreads) k_gradout(Params P, long long blk, l
   }
 }
 
-// full deviance over all local entries (model.py:268-276): warp per row
+// NB part of -2 log-likelihood beyond D/phi for one entry with y > 0
+// (select.py:57-78 _dispersion_constant: sat + y log y; zeros contribute 0)
+GMF_D double nb_loglik_term(double y, double a) {
+  const double sat = lgamma(y + a) - lgamma(a) - lgamma(y + 1.0) - (y + a) * log(y + a) +
+                     a * log(a);
+  return sat + y * log(y);
+}
+
+// full deviance over all local entries (model.py:268-276): warp per row.
+// With `with_const` (NB only) the same pass over Y also sums the dispersion
+// constant of select.py:71-78 -> out[1] = -2 sum w (sat + y log y).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, double* part,
-                                                      unsigned int* ticket, double* out) {
+__global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, int with_const,
+                                                      double* part, unsigned int* ticket,
+                                                      double* out) {
   __shared__ double scr[kThreads / 32];
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)kThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
   const T* wg = tptr<T>(P.w);
-  double s = 0.0;
+  double s = 0.0, c = 0.0;
   for (int64_t i = gw; i < P.n; i += nw) {
     if (P.yfmt == GMF_Y_DENSE_I32) {
       for (int64_t j = lane; j < P.m; j += 32) {
         const double mu = exp(eta_at<T>(P, i, j));
         const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-        s += w * unit_deviance(P.fam, (double)P.y[i * P.m + j], mu, alpha);
+        const double y = (double)P.y[i * P.m + j];
+        s += w * unit_deviance(P.fam, y, mu, alpha);
+        if (with_const && y > 0.0) c += w * nb_loglik_term(y, alpha);
       }
     } else {
       // zeros everywhere, corrected at the stored nonzeros
@@ -320,19 +333,74 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, do
       for (int64_t k = P.rp[i] + lane; k < P.rp[i + 1]; k += 32) {
         const int64_t j = csr_col_at(P, k);
         const double mu = exp(eta_at<T>(P, i, j));
-        s += unit_deviance(P.fam, (double)csr_val_at(P, k), mu, alpha) - unit_deviance(P.fam, 0.0, mu, alpha);
+        const double y = (double)csr_val_at(P, k);
+        s += unit_deviance(P.fam, y, mu, alpha) - unit_deviance(P.fam, 0.0, mu, alpha);
+        if (with_const && y > 0.0) c += nb_loglik_term(y, alpha);
       }
     }
   }
   s = block_sum<kThreads>(s, scr);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (with_const) {
+    c = block_sum<kThreads>(c, scr);
+    if (threadIdx.x == 0) part[gridDim.x + blockIdx.x] = c;
+  }
   if (last_block_ticket(ticket, gridDim.x)) {
     const double tot = sum_parts<kThreads>(part, gridDim.x, 1, scr);
+    __syncthreads();
+    const double ctot = with_const ? sum_parts<kThreads>(part + gridDim.x, gridDim.x, 1, scr) : 0.0;
     if (threadIdx.x == 0) {
-      *out = tot;
+      out[0] = tot;
+      if (with_const) out[1] = -2.0 * ctot;
       *ticket = 0u;
     }
   }
+}
+
+// Held-out scoring at listed entries (select.py:141-145 _mu_at, then
+// metrics.py:35-55): mu = exp(eta) at (rows[k], cols[k]) -- rows in the
+// handle's local (block-major) numbering -- optionally stored, and with y
+// the four sums of rel_deviance / rel_log_rmse (unit prior weights):
+// out = [sum D(y, mu), sum D(y, ybar), sum log^2((1+y)/(1+mu)), sum log^2((1+y)/(1+ybar))].
+GMF_D void score_entry(int fam, double y, double mu, double ybar, double alpha, double* s) {
+  s[0] += unit_deviance(fam, y, mu, alpha);
+  s[1] += unit_deviance(fam, y, ybar, alpha);
+  const double a = log((1.0 + y) / (1.0 + mu)), b = log((1.0 + y) / (1.0 + ybar));
+  s[2] += a * a;
+  s[3] += b * b;
+}
+
+template <int NT>
+GMF_D void publish4(const double* s, double* part, unsigned int* ticket, double* out, double* scr) {
+  for (int c = 0; c < 4; ++c) {
+    const double t = block_sum<NT>(s[c], scr);
+    if (threadIdx.x == 0) part[c * gridDim.x + blockIdx.x] = t;
+  }
+  if (last_block_ticket(ticket, gridDim.x)) {
+    for (int c = 0; c < 4; ++c) {
+      __syncthreads();
+      const double tot = sum_parts<NT>(part + c * gridDim.x, gridDim.x, 1, scr);
+      if (threadIdx.x == 0) out[c] = tot;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_entries(Params P, double alpha, const int64_t* rows,
+                                                      const int32_t* cols, const double* y,
+                                                      int64_t n, double ybar, double* mu_out,
+                                                      double* part, unsigned int* ticket,
+                                                      double* out) {
+  __shared__ double scr[kThreads / 32];
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t k = blockIdx.x * (int64_t)kThreads + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * kThreads) {
+    const double mu = exp(eta_at<T>(P, rows[k], cols[k]));
+    if (mu_out) mu_out[k] = mu;
+    if (out) score_entry(P.fam, y[k], mu, ybar, alpha, s);
+  }
+  if (out) publish4<kThreads>(s, part, ticket, out, scr);
 }
 
 // ---------------------------------------------------------------------------
@@ -433,12 +501,30 @@ int launch_gradout(const Params& P, int dtype, long long blk, long long sidx, in
   return GMF_OK;
 }
 
-int launch_objfull(const Params& P, int dtype, double alpha, double* part, unsigned int* ticket,
-                   double* out, cudaStream_t st) {
+int launch_objfull(const Params& P, int dtype, double alpha, int with_const, double* part,
+                   unsigned int* ticket, double* out, cudaStream_t st) {
   const int grid = 2 * kSMs;
-  if (dtype == GMF_F64) k_objfull<double><<<grid, kThreads, 0, st>>>(P, alpha, part, ticket, out);
-  else k_objfull<float><<<grid, kThreads, 0, st>>>(P, alpha, part, ticket, out);
+  if (dtype == GMF_F64)
+    k_objfull<double><<<grid, kThreads, 0, st>>>(P, alpha, with_const, part, ticket, out);
+  else
+    k_objfull<float><<<grid, kThreads, 0, st>>>(P, alpha, with_const, part, ticket, out);
   GMF_LAUNCH_CHECK("k_objfull");
+  return GMF_OK;
+}
+
+int launch_entries(const Params& P, int dtype, double alpha, const int64_t* rows,
+                   const int32_t* cols, const double* y, int64_t n, double ybar, double* mu_out,
+                   double* part, unsigned int* ticket, double* out, cudaStream_t st) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b > 2 * kSMs) b = 2 * kSMs;
+  if (b < 1) b = 1;
+  if (dtype == GMF_F64)
+    k_entries<double><<<(unsigned)b, kThreads, 0, st>>>(P, alpha, rows, cols, y, n, ybar, mu_out,
+                                                         part, ticket, out);
+  else
+    k_entries<float><<<(unsigned)b, kThreads, 0, st>>>(P, alpha, rows, cols, y, n, ybar, mu_out,
+                                                        part, ticket, out);
+  GMF_LAUNCH_CHECK("k_entries");
   return GMF_OK;
 }
 

@@ -372,6 +372,14 @@ class DeviceFit:
                    "gmf_objective_full")
         return float(out.item())
 
+    def loglik_full(self):
+        """(sum w D over all local entries, NB dispersion constant) in one pass."""
+        out = self.torch.zeros(2, device=self.device, dtype=self.torch.float64)
+        _lib.check(self.lib.gmf_loglik_full(self.h, _lib.ptr(out), self.stream()),
+                   "gmf_loglik_full")
+        dev, const = out.cpu().numpy()
+        return float(dev), float(const)
+
     def snapshot_rows(self):
         """Local rows of the divergence snapshot (copy-on-write reconstruction:
         blocks saved during the current snapshot period come from snap_row,

@@ -325,10 +325,52 @@ def make_weighted():
     return out
 
 
+def make_select():
+    """information_criteria / _mu_at / rel_deviance / rel_log_rmse of the
+    reference (select.py:57-96, 141-145; metrics.py:35-55)."""
+    import gmfkit.select as gsel
+    import gmfkit.metrics as gmet
+    rng = np.random.default_rng(61)
+    out = {}
+    cases = [("pois", gk.Poisson(), 1.3, False, 2, 1), ("nb", gk.NegBinomial(1.7), 1.0, False, 2, 1),
+             ("nbw", gk.NegBinomial(0.6), 1.0, True, 1, 0), ("nb50", gk.NegBinomial(50.0), 1.0, False, 1, 1)]
+    for k, (key, fam, phi, weighted, p, q) in enumerate(cases):
+        n, m, d = 60, 24, 3
+        y, x, z, off, init = _nb_problem(n, m, p, q, d, 62 + k, False)
+        w = rng.uniform(0.5, 2.0, (n, m)) if weighted else None
+        data = gk.ResponseMatrix(y.astype(float), weights=w)
+        covs = gk.CovariateSet(x=x, z=z)
+        st = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], phi,
+                                   getattr(fam, "nb_shape", 1.0))
+        aic, bic = gsel.information_criteria(st, data, covs, fam, gk.Log())
+        rows = rng.integers(0, n, 50)
+        cols = rng.integers(0, m, 50)
+        ybar = float(np.mean(y))
+        mu_t = gsel._mu_at(st, covs, gk.Log(), rows, cols)
+        yt = y[rows, cols].astype(float)
+        out[f"{key}|y"] = y
+        out[f"{key}|x"] = covs.x
+        out[f"{key}|z"] = covs.z
+        if w is not None:
+            out[f"{key}|w"] = w
+        out.update(_state_arrays(f"{key}|st", st))
+        out[f"{key}|alpha"] = np.float64(getattr(fam, "nb_shape", 1.0))
+        out[f"{key}|aic"] = np.float64(aic)
+        out[f"{key}|bic"] = np.float64(bic)
+        out[f"{key}|rows"] = rows
+        out[f"{key}|cols"] = cols
+        out[f"{key}|ybar"] = np.float64(ybar)
+        out[f"{key}|mu_test"] = mu_t
+        out[f"{key}|rel_dev"] = np.float64(gmet.rel_deviance(yt, mu_t, ybar, fam))
+        out[f"{key}|rel_lrmse"] = np.float64(gmet.rel_log_rmse(yt, mu_t, ybar))
+    return out
+
+
 def main():
     makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
-              "project": make_project, "weighted": make_weighted}
+              "project": make_project, "weighted": make_weighted,
+              "select": make_select}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
