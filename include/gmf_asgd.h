@@ -31,6 +31,11 @@
  *     gmf_entries_eval        select.py:141-145 _mu_at at held-out entries, fused
  *                             with metrics.py:35-55 (cv_rank_select scoring,
  *                             select.py:201-213)
+ *   Initialization (initialization.py:143-169 init_ols_svd, 62-82 randomized_svd):
+ *     gmf_csr_spmm            S P for the log-transformed counts' sparse part
+ *                             (S' Q through the CSC); the residual's low-rank
+ *                             part is applied by the host (no n x m residual)
+ *     gmf_init_moments        _nb_shape_moment sums (initialization.py:93-100)
  *   Level 3 (identify.project_constraints (A)+(B1), identify.py:59-110):
  *     gmf_cross_rows          Z = A' B over rows (Gram / cross products), fp64
  *     gmf_rows_affine         Y <- beta Y + A M, row-local apply of a small matrix
@@ -294,6 +299,26 @@ int gmf_cross_rows(int dtype, int64_t rows, const void* A, int64_t lda, int32_t 
 int gmf_rows_affine(int dtype, int64_t rows, void* Y, int64_t ldy, int32_t y0, int32_t c,
                     double beta, const void* A, int64_t lda, int32_t a0, int32_t a,
                     const double* M, void* stream);
+
+/* ------------------------------------------------------- initialization */
+
+/* out (nrows x r doubles, row-major) = S P with s_k = log(val_k + eps) - log(eps)
+ * at the stored entries of a CSR (ptr int64, col/val int32; pass a CSC to get
+ * S' Q); P is (ncols x r) row-major doubles.  Rows longer than 2048 nonzeros
+ * are split into segments whose partials are summed in fixed order in `work`
+ * (gmf_spmm_work_bytes bytes; may be NULL when that is 0). */
+int64_t gmf_spmm_work_bytes(int64_t nrows, int64_t max_row_nnz, int32_t r);
+int gmf_csr_spmm(int64_t nrows, const int64_t* ptr, const int32_t* col, const int32_t* val,
+                 int64_t max_row_nnz, double eps, const double* P, int32_t r, double* out,
+                 void* work, void* stream);
+
+/* out2 (device) = [sum mu0^2, sum ((y - mu0)^2 - mu0)] over all n x m entries,
+ * mu0 = exp(clip(x_i b_j + gamma_i z_j, eta_lo, eta_hi)); fp64, fixed order. */
+int64_t gmf_moments_work_bytes(void);
+int gmf_init_moments(int64_t n, int64_t m, const int64_t* ptr, const int32_t* col,
+                     const int32_t* val, const double* x, const double* b, int32_t p,
+                     const double* gamma, const double* z, int32_t q, double eta_lo,
+                     double eta_hi, double* out2, void* work, void* stream);
 
 const char* gmf_last_error(void);
 const char* gmf_version(void);

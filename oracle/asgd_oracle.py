@@ -293,6 +293,57 @@ def rel_deviance(fcode, y, mu, ybar, alpha):
     return float(num / den)
 
 
+# ---------------------------------------------------------------------------
+# OLS-SVD initialization (gmfkit/initialization.py:62-82, 93-100, 143-169)
+# ---------------------------------------------------------------------------
+
+def randomized_svd(a, k, oversample=10, n_power=2, seed=0):
+    """Truncated SVD by a randomized range finder -- initialization.py:62-82."""
+    n, m = a.shape
+    k = min(k, min(n, m))
+    if k == 0:
+        return np.zeros((n, 0)), np.zeros(0), np.zeros((m, 0))
+    if k + oversample >= min(n, m):
+        u, s, vt = np.linalg.svd(a, full_matrices=False)
+        return u[:, :k], s[:k], vt[:k].T
+    rng = np.random.default_rng(seed)
+    probe = rng.standard_normal((m, k + oversample))
+    sketch = a @ probe
+    for _ in range(n_power):
+        q, _ = np.linalg.qr(sketch)
+        sketch = a @ (a.T @ q)
+    q, _ = np.linalg.qr(sketch)
+    u_small, s, vt = np.linalg.svd(q.T @ a, full_matrices=False)
+    return (q @ u_small)[:, :k], s[:k], vt[:k].T
+
+
+def _ols(y, design, offset=None, damping=1e-8):
+    """Single Gaussian/identity Fisher step from zero = damped least squares,
+    per column of y -- glm.py:36-64 via initialization.py:136-140."""
+    p = design.shape[1]
+    if p == 0:
+        return np.zeros((y.shape[1], 0))
+    r = y if offset is None else y - offset
+    return np.linalg.solve(design.T @ design + damping * np.eye(p), design.T @ r).T
+
+
+def init_ols_svd(pb: OProblem, d, fcode, eps=0.1, seed=0):
+    """Fully observed, unit-weight, log-link init_ols_svd -- initialization.py:143-169."""
+    y_eps = np.log(pb.y + eps)
+    b = _ols(y_eps, pb.x)
+    offset = pb.x @ b.T
+    gamma = _ols(y_eps.T, pb.z, offset.T)
+    eta0 = offset + (gamma @ pb.z.T if pb.z.shape[1] else 0.0)
+    left, sing, right = randomized_svd(y_eps - eta0, d, seed=seed)
+    mu0 = np.exp(np.clip(eta0, -700.0, 700.0))
+    nb = 1.0
+    if fcode == NEG_BINOMIAL:
+        num = float(np.sum(mu0 ** 2))
+        den = float(np.sum((pb.y - mu0) ** 2 - mu0))
+        nb = 1e8 if den <= 0 else float(np.clip(num / den, 1e-4, 1e8))
+    return OState(b, gamma, left * sing, right, 1.0, nb)
+
+
 def penalty_vectors(p, q, d, lam):
     """Per-coordinate ridge weights [Gamma,U] and [B,V] -- gradients.py:91-99."""
     lb, lg, lu, lv = lam

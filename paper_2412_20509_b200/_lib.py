@@ -124,6 +124,11 @@ SIGNATURES = {
                                  _P, _P, _P]),
     "gmf_rows_affine": (C.c_int, [C.c_int, _i64, _P, _i64, _i32, _i32, _d, _P, _i64, _i32, _i32,
                                   _P, _P]),
+    "gmf_spmm_work_bytes": (_i64, [_i64, _i64, _i32]),
+    "gmf_csr_spmm": (C.c_int, [_i64, _P, _P, _P, _i64, _d, _P, _i32, _P, _P, _P]),
+    "gmf_moments_work_bytes": (_i64, []),
+    "gmf_init_moments": (C.c_int, [_i64, _i64, _P, _P, _P, _P, _P, _i32, _P, _P, _i32, _d, _d,
+                                   _P, _P, _P]),
     "gmf_last_error": (C.c_char_p, []),
     "gmf_version": (C.c_char_p, []),
 }

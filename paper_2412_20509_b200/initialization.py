@@ -1,0 +1,227 @@
+"""OLS-SVD starting values on the GPU (gmfkit/initialization.py:143-169).
+
+The reference builds the dense n x m link-transformed response, its OLS
+residual and a randomized SVD of it (initialization.py:62-82) -- 5.2 GB of
+fp64 per copy at 1.3M x 500.  Here nothing n x m is materialised.  With a
+fully observed count matrix and the log link,
+
+    Y_eps = log(Y + eps) = log(eps) 1 1' + S,   S sparse like Y,
+    A     = Y_eps - X B' - Gamma Z' = S + L R',
+    L = [1 | X | Gamma],  R = [log(eps) 1 | -B | -Z],
+
+so every product of the initialization is one sparse product with S
+(``gmf_csr_spmm`` over the CSR for S P, over the CSC for S' Q) plus
+rank-(1+p+q) corrections.  The OLS stages solve the reference's damped normal
+equations (glm.py:36-64 with the Gaussian/identity single Fisher step:
+(D'D + 1e-8 I) c = D'(y - offset)); the range finder replays the reference's
+probe (numpy ``default_rng(seed).standard_normal``) so the sketched subspace
+is the reference's; the NB shape moment (initialization.py:93-100) is one
+pass over all entries (``gmf_init_moments``).  Dense QR/SVD of the
+(k + 10)-column sketches run in cuSOLVER through torch (library calls on
+tall-skinny matrices).
+
+Scope: Poisson / negative binomial with the log link, fully observed
+responses, unit prior weights (the fit's own device scope).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import _counts_int32
+from .exceptions import ConfigError
+from .model import CovariateSet, FactorizationState, ResponseMatrix
+
+__all__ = ["InitMethod", "init_ols_svd", "randomized_svd_sparse"]
+
+_LINK_EPS = {"log": 0.1, "logit": 0.01, "inverse": 0.1, "inverse_squared": 0.1}
+_DAMPING = 1e-8            # glm.py:68 fit_glm_batched default
+_ETA_CLIP_LOG = (-700.0, 700.0)   # initialization.py:217-220
+
+
+@dataclass
+class InitMethod:
+    """Residual kind and g_eps perturbation (initialization.py:29-45)."""
+
+    residual_kind: str = "deviance"
+    link_epsilon: float | None = None
+
+    def __post_init__(self):
+        if self.residual_kind not in ("deviance", "pearson"):
+            raise ConfigError("residual_kind must be 'deviance' or 'pearson'")
+        if self.link_epsilon is not None and self.link_epsilon <= 0:
+            raise ConfigError("link_epsilon must be positive")
+
+    def eps_for(self, lnk) -> float:
+        if self.link_epsilon is not None:
+            return self.link_epsilon
+        return _LINK_EPS.get(lnk.kind, 0.1)
+
+
+class _SparseCounts:
+    """Y on the device as CSR and CSC (int64 pointers, int32 indices/counts)."""
+
+    def __init__(self, data: ResponseMatrix, dev):
+        import torch
+        n, m = data.shape
+        if data.csr is not None:
+            indptr, indices, vals = data.csr
+        else:
+            r, c = np.nonzero(data.values)
+            indptr = np.zeros(n + 1, np.int64)
+            np.cumsum(np.bincount(r, minlength=n), out=indptr[1:])
+            indices, vals = c.astype(np.int32), data.values[r, c]
+        counts = _counts_int32(np.asarray(vals), "response")
+        self.n, self.m = n, m
+        self.ptr = torch.from_numpy(np.asarray(indptr, np.int64)).to(dev)
+        self.col = torch.from_numpy(np.asarray(indices, np.int32)).to(dev)
+        self.val = torch.from_numpy(counts).to(dev)
+        lens = self.ptr[1:] - self.ptr[:-1]
+        self.max_row = int(lens.max().item()) if n else 0
+        # CSC by a stable sort on the column index (row order kept within a column)
+        order = torch.argsort(self.col.long(), stable=True)
+        rows = torch.repeat_interleave(torch.arange(n, device=dev, dtype=torch.int32), lens)
+        self.cptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+        self.cptr[1:] = torch.cumsum(torch.bincount(self.col.long(), minlength=m), 0)
+        self.crow = rows[order].contiguous()
+        self.cval = self.val[order].contiguous()
+        clens = self.cptr[1:] - self.cptr[:-1]
+        self.max_col = int(clens.max().item()) if m else 0
+
+    def _spmm(self, transpose, P, eps):
+        import torch
+        lib = _lib.lib()
+        P = P.contiguous()
+        r = P.shape[1]
+        nrows = self.m if transpose else self.n
+        ptr, idx, val, mx = ((self.cptr, self.crow, self.cval, self.max_col) if transpose
+                             else (self.ptr, self.col, self.val, self.max_row))
+        out = torch.empty((nrows, r), dtype=torch.float64, device=P.device)
+        wb = int(lib.gmf_spmm_work_bytes(nrows, mx, r))
+        work = torch.empty(max(wb, 1), dtype=torch.uint8, device=P.device)
+        stream = torch.cuda.current_stream(P.device).cuda_stream
+        _lib.check(lib.gmf_csr_spmm(nrows, _lib.ptr(ptr), _lib.ptr(idx), _lib.ptr(val), mx,
+                                    float(eps), _lib.ptr(P), r, _lib.ptr(out), _lib.ptr(work),
+                                    stream), "gmf_csr_spmm")
+        return out
+
+    def s_mul(self, P, eps):
+        """S P, P (m x r)."""
+        return self._spmm(False, P, eps)
+
+    def st_mul(self, Q, eps):
+        """S' Q, Q (n x r)."""
+        return self._spmm(True, Q, eps)
+
+    def dense_s(self, eps):
+        import torch
+        out = torch.zeros((self.n, self.m), dtype=torch.float64, device=self.ptr.device)
+        rows = torch.repeat_interleave(torch.arange(self.n, device=out.device),
+                                       self.ptr[1:] - self.ptr[:-1])
+        out[rows, self.col.long()] = torch.log(self.val.double() + eps) - math.log(eps)
+        return out
+
+
+def _damped_solve(design, rhs):
+    """(D'D + 1e-8 I)^{-1} rhs (glm.py:49-53, Gaussian/identity Fisher step)."""
+    import torch
+    p = design.shape[1]
+    G = design.T @ design + _DAMPING * torch.eye(p, dtype=torch.float64, device=design.device)
+    return torch.linalg.solve(G, rhs)
+
+
+def randomized_svd_sparse(Y: _SparseCounts, eps, L, R, k, oversample=10, n_power=2, seed=0):
+    """randomized_svd (initialization.py:62-82) of A = S + L R' on the GPU."""
+    import torch
+    n, m = Y.n, Y.m
+    dev = L.device
+    k = min(k, min(n, m))
+    if k == 0:
+        z = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)
+        return z(n, 0), z(0), z(m, 0)
+    if k + oversample >= min(n, m):
+        A = Y.dense_s(eps) + L @ R.T
+        u, s, vt = torch.linalg.svd(A, full_matrices=False)
+        return u[:, :k], s[:k], vt[:k].T
+    rng = np.random.default_rng(seed)
+    probe = torch.from_numpy(rng.standard_normal((m, k + oversample))).to(dev)
+    a_mul = lambda P: Y.s_mul(P, eps) + L @ (R.T @ P)
+    at_mul = lambda Q: Y.st_mul(Q, eps) + R @ (L.T @ Q)
+    sketch = a_mul(probe)
+    for _ in range(n_power):
+        q, _ = torch.linalg.qr(sketch)
+        sketch = a_mul(at_mul(q))
+    q, _ = torch.linalg.qr(sketch)
+    u_small, s, vt = torch.linalg.svd(at_mul(q).T, full_matrices=False)
+    return (q @ u_small)[:, :k], s[:k], vt[:k].T
+
+
+def init_ols_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
+                 method: InitMethod | None = None, seed: int = 0, return_info: bool = False,
+                 *, device=None):
+    """Least-squares initialization on the link-transformed response
+    (initialization.py:143-169), computed on the GPU; returns a host state."""
+    import torch
+    method = method or InitMethod()
+    n, m = data.shape
+    if d > min(n, m):
+        raise ConfigError("rank d cannot exceed min(n, m)")
+    if fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log":
+        raise _lib.UnsupportedError(
+            f"device initialization implements poisson/neg_binomial with log link, "
+            f"got {fam.kind}+{lnk.kind}")
+    if not data.fully_observed or data.weights is not None:
+        raise _lib.UnsupportedError("device initialization needs a fully observed, unweighted "
+                                    "response")
+    _lib.require_cuda()
+    _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       int(str(device).split(":")[-1]))
+    eps = method.eps_for(lnk)
+    leps = math.log(eps)
+    Y = _SparseCounts(data, dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    X = torch.from_numpy(np.ascontiguousarray(covs.x, dtype=float)).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(covs.z, dtype=float)).to(dev)
+    p, q = X.shape[1], Z.shape[1]
+    ones_n, ones_m = torch.ones((n, 1), **f64), torch.ones((m, 1), **f64)
+
+    # B stage: columns regress y_eps on X (initialization.py:154)
+    if p:
+        rhs = leps * X.sum(0)[:, None] * ones_m.T + Y.st_mul(X, eps).T      # X' Y_eps
+        B = _damped_solve(X, rhs).T.contiguous()
+    else:
+        B = torch.zeros((m, 0), **f64)
+    # Gamma stage: rows regress y_eps - X B' on Z (initialization.py:155-156)
+    if q:
+        rhs = leps * Z.sum(0)[None, :] + Y.s_mul(Z, eps) - X @ (B.T @ Z)    # rows of Z'(y_eps - off)
+        Gm = _damped_solve(Z, rhs.T).T.contiguous()
+    else:
+        Gm = torch.zeros((n, 0), **f64)
+
+    # residual SVD (initialization.py:159-162)
+    L = torch.cat([ones_n, X, Gm], 1)
+    R = torch.cat([leps * ones_m, -B, -Z], 1)
+    left, sing, right = randomized_svd_sparse(Y, eps, L, R, d, seed=seed)
+    U = left * sing
+    V = right
+
+    nb_shape = 1.0
+    if fam.kind == "neg_binomial":    # initialization.py:93-100 at mu0 (164-166)
+        lib = _lib.lib()
+        out = torch.zeros(2, **f64)
+        work = torch.empty(int(lib.gmf_moments_work_bytes()), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(lib.gmf_init_moments(n, m, _lib.ptr(Y.ptr), _lib.ptr(Y.col), _lib.ptr(Y.val),
+                                        _lib.ptr(X), _lib.ptr(B), p, _lib.ptr(Gm), _lib.ptr(Z), q,
+                                        _ETA_CLIP_LOG[0], _ETA_CLIP_LOG[1], _lib.ptr(out),
+                                        _lib.ptr(work), stream), "gmf_init_moments")
+        num, den = (float(v) for v in out.cpu().numpy())
+        nb_shape = 1e8 if den <= 0 else float(np.clip(num / den, 1e-4, 1e8))
+    host = lambda t: t.cpu().numpy()
+    state = FactorizationState(host(B), host(Gm), host(U), host(V), 1.0, nb_shape)
+    info = {"method": "ols_svd"}
+    return (state, info) if return_info else state

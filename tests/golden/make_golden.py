@@ -366,11 +366,37 @@ def make_select():
     return out
 
 
+def make_init():
+    """init_ols_svd of the reference (initialization.py:143-169), Poisson and
+    NB, randomized range finder and the exact-SVD fallback."""
+    out = {}
+    cases = [("pois", gk.Poisson(), 300, 80, 1, 1, 4), ("nb", gk.NegBinomial(2.0), 400, 60, 2, 1, 5),
+             ("small", gk.NegBinomial(1.0), 30, 12, 1, 0, 3), ("noz", gk.Poisson(), 200, 50, 0, 0, 2)]
+    for k, (key, fam, n, m, p, q, d) in enumerate(cases):
+        y, x, z, off, init = _nb_problem(n, m, max(p, 1), q, d, 81 + k, False)
+        x = x[:, :p]
+        data = gk.ResponseMatrix(y.astype(float))
+        covs = gk.CovariateSet(x=x, z=z)
+        st = gk.init_ols_svd(data, covs, fam, gk.Log(), d, seed=3)
+        out[f"{key}|y"] = y
+        out[f"{key}|x"] = x
+        out[f"{key}|z"] = z
+        out[f"{key}|d"] = np.int64(d)
+        out[f"{key}|nbfam"] = np.int64(fam.kind == "neg_binomial")
+        out[f"{key}|b"] = st.b
+        out[f"{key}|gamma"] = st.gamma
+        out[f"{key}|uv"] = st.u @ st.v.T
+        out[f"{key}|s"] = np.linalg.norm(st.u, axis=0)
+        out[f"{key}|nb_shape"] = np.float64(st.nb_shape)
+        out[f"{key}|phi"] = np.float64(st.phi)
+    return out
+
+
 def main():
     makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
-              "select": make_select}
+              "select": make_select, "init": make_init}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
