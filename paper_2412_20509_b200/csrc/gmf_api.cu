@@ -295,7 +295,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_lm = take(R * 8);
   const int64_t o_rho = take(ms * 8);
   const int64_t o_alp = take(ms * 8);
-  const int64_t o_fp = take(4 * 2 * kSMs * 8);   // k_objfull / k_entries partials
+  const int64_t o_fp = take(2 * 8 * kSMs * 8);   // k_objfull (2 x 8 kSMs) / k_entries (4 x 2 kSMs) partials
   const int64_t o_ft = take(64);
   const int64_t o_ep = take((bufs->n_eval > 0 ? bufs->n_eval : 1) * 16);
   const int64_t o_cnp = take(cta_max * 2 * 8);

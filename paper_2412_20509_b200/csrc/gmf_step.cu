@@ -304,6 +304,17 @@ GMF_D double nb_loglik_term(double y, double a) {
   return sat + y * log(y);
 }
 
+// unit deviance at eta: fp64 on the fp64 path; on the fp32 path the fp32
+// transcendentals of the tracked objective (gmf_common.cuh unit_deviance_f),
+// accumulated in fp64 by the caller
+template <typename T>
+GMF_D double dev_at(int fam, double y, double eta, double alpha) {
+  if constexpr (std::is_same<T, float>::value)
+    return (double)unit_deviance_f(fam, (float)y, __expf((float)eta), (float)alpha);
+  else
+    return unit_deviance(fam, y, exp(eta), alpha);
+}
+
 // full deviance over all local entries (model.py:268-276): warp per row.
 // With `with_const` (NB only) the same pass over Y also sums the dispersion
 // constant of select.py:71-78 -> out[1] = -2 sum w (sat + y log y).
@@ -320,21 +331,20 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
   for (int64_t i = gw; i < P.n; i += nw) {
     if (P.yfmt == GMF_Y_DENSE_I32) {
       for (int64_t j = lane; j < P.m; j += 32) {
-        const double mu = exp(eta_at<T>(P, i, j));
         const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
         const double y = (double)P.y[i * P.m + j];
-        s += w * unit_deviance(P.fam, y, mu, alpha);
+        s += w * dev_at<T>(P.fam, y, eta_at<T>(P, i, j), alpha);
         if (with_const && y > 0.0) c += w * nb_loglik_term(y, alpha);
       }
     } else {
       // zeros everywhere, corrected at the stored nonzeros
       for (int64_t j = lane; j < P.m; j += 32)
-        s += unit_deviance(P.fam, 0.0, exp(eta_at<T>(P, i, j)), alpha);
+        s += dev_at<T>(P.fam, 0.0, eta_at<T>(P, i, j), alpha);
       for (int64_t k = P.rp[i] + lane; k < P.rp[i + 1]; k += 32) {
         const int64_t j = csr_col_at(P, k);
-        const double mu = exp(eta_at<T>(P, i, j));
+        const double eta = eta_at<T>(P, i, j);
         const double y = (double)csr_val_at(P, k);
-        s += unit_deviance(P.fam, y, mu, alpha) - unit_deviance(P.fam, 0.0, mu, alpha);
+        s += dev_at<T>(P.fam, y, eta, alpha) - dev_at<T>(P.fam, 0.0, eta, alpha);
         if (with_const && y > 0.0) c += nb_loglik_term(y, alpha);
       }
     }
@@ -503,7 +513,7 @@ int launch_gradout(const Params& P, int dtype, long long blk, long long sidx, in
 
 int launch_objfull(const Params& P, int dtype, double alpha, int with_const, double* part,
                    unsigned int* ticket, double* out, cudaStream_t st) {
-  const int grid = 2 * kSMs;
+  const int grid = 8 * kSMs;   // 64 warps per SM to hide the fp64 latency chains
   if (dtype == GMF_F64)
     k_objfull<double><<<grid, kThreads, 0, st>>>(P, alpha, with_const, part, ticket, out);
   else
