@@ -47,6 +47,8 @@ def _args():
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", type=int, default=0)
+    ap.add_argument("--no-aux", action="store_true",
+                    help="skip the model-selection / initialization legs (SURVEY 8f)")
     ap.add_argument("--k1-impl", default="auto", choices=["auto", "tensor", "cuda_cores"])
     return ap.parse_args()
 
@@ -213,6 +215,46 @@ def run_reference(args):
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _aux_legs(wl, data, covs, st, fam, dev, reps=3):
+    """SURVEY 8f rows on the same workload: the one-pass log-likelihood behind
+    information_criteria (k_objfull + NB constant, all n*m entries) and
+    init_ols_svd (sparse products, no n x m residual).  CUDA events for the
+    kernel, wall clock for the init call (it includes the CSR upload)."""
+    import torch
+    import paper_2412_20509_b200 as gk
+    from paper_2412_20509_b200 import _lib
+    from paper_2412_20509_b200.initialization import init_ols_svd
+    from paper_2412_20509_b200.select import _state_fit
+    sp = wl.spec
+    fit = _state_fit(st, data, covs, fam, gk.Log(), wl.offset, sp.dtype, dev.index)
+    try:
+        res = torch.zeros(2, dtype=torch.float64, device=dev)
+        call = lambda: _lib.check(fit.lib.gmf_loglik_full(fit.h, _lib.ptr(res), fit.stream()),
+                                  "gmf_loglik_full")
+        call()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream(dev))
+        for _ in range(reps):
+            call()
+        e1.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        ll_ms = e0.elapsed_time(e1) / reps
+    finally:
+        fit.close()
+    init_ols_svd(data, covs, fam, gk.Log(), sp.d, seed=0)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    init_ols_svd(data, covs, fam, gk.Log(), sp.d, seed=0)
+    torch.cuda.synchronize(dev)
+    init_s = time.perf_counter() - t0
+    return {"loglik_full": {"kernel": "k_objfull (deviance + NB dispersion constant, all n*m "
+                                      "entries; information_criteria)",
+                            "ms": ll_ms, "entries_per_s": sp.n * sp.m / (ll_ms * 1e-3)},
+            "init_ols_svd": {"s": init_s, "path": "gmf_csr_spmm / gmf_init_moments + cuSOLVER "
+                                                  "sketches; host CSR upload included"}}
 
 
 def _workload_desc(name):
@@ -464,6 +506,12 @@ def main():
         cpu = _cpu_baseline(wl, max(4, args.cpu_steps))
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
     fit.close()
+    aux = None
+    if rank == 0 and world == 1 and not args.no_aux:
+        try:
+            aux = _aux_legs(wl, data, covs, st, fam, dev)
+        except Exception as err:   # reported, never fatal to the headline line
+            aux = {"error": f"{type(err).__name__}: {err}"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -479,7 +527,7 @@ def main():
                        "parallelism": f"rows of each block split x{world}" if world > 1 else "1 GPU",
                        "geometry": geometry, "k1_impl": fit.k1_impl, "y_storage": fit.y_format},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(timed_launches), "clocks": clocks,
+            "gpu_launches": int(timed_launches), "clocks": clocks, "aux": aux,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
