@@ -201,8 +201,9 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
         if rank is None:
             raise ConfigError("pass init_state or rank")
         raise _lib.UnsupportedError(
-            "initialization (init_glm_svd, initialization.py:172-214) is not part of the "
-            "device path; pass init_state")
+            "the reference's default initialization (init_glm_svd, initialization.py:172-214) "
+            "is not on the device path; pass init_state (e.g. from "
+            "paper_2412_20509_b200.initialization.init_ols_svd)")
     init_state.check_shapes(data, covs)
     est_phi, est_alpha = _resolve_dispersion(fam, dispersion)
     if est_phi:
