@@ -315,6 +315,22 @@ GMF_D double dev_at(int fam, double y, double eta, double alpha) {
     return unit_deviance(fam, y, exp(eta), alpha);
 }
 
+// D(0, mu) -- the all-zero grid of a CSR pass.  NB: -2 alpha log1p(-mu / (mu + alpha))
+// = 2 alpha log1p(mu / alpha) (no division; also exact where mu >> alpha);
+// Poisson: 2 mu.
+template <typename T>
+GMF_D double dev0_at(int fam, double eta, double alpha, double inv_alpha) {
+  if constexpr (std::is_same<T, float>::value) {
+    const float mu = __expf((float)eta);
+    if (fam == GMF_NEG_BINOMIAL) return (double)(2.f * (float)alpha * log1pf(mu * (float)inv_alpha));
+    return (double)(2.f * mu);
+  } else {
+    const double mu = exp(eta);
+    if (fam == GMF_NEG_BINOMIAL) return 2.0 * alpha * log1p(mu * inv_alpha);
+    return 2.0 * mu;
+  }
+}
+
 // full deviance over all local entries (model.py:268-276), tiled: a CTA
 // takes 32 rows x 64 columns at a time with the rows' [u | x | gamma] and
 // the columns' [v | b | z] staged in shared memory as fp64 (stride S = K | 1
@@ -348,6 +364,7 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
   const T* og = tptr<T>(P.off);
   const T* wg = tptr<T>(P.w);
   const bool dense = P.yfmt == GMF_Y_DENSE_I32;
+  const double inv_alpha = 1.0 / alpha;
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;   // rows rg + 8r, columns lane, lane + 32
   double s = 0.0, c = 0.0;
   const int64_t ntiles = (P.n + kFullRows - 1) / kFullRows;
@@ -408,7 +425,7 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
             s += w * dev_at<T>(P.fam, y, eta, alpha);
             if (with_const && y > 0.0) c += w * nb_loglik_term(y, alpha);
           } else {
-            s += dev_at<T>(P.fam, 0.0, eta, alpha);
+            s += dev0_at<T>(P.fam, eta, alpha, inv_alpha);
           }
         }
       }
@@ -429,7 +446,7 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
         for (int kk = 0; kk < q; ++kk) eta = fma(R[d + p + kk], (double)zg[j * q + kk], eta);
         eta += offs[a];
         const double y = (double)csr_val_at(P, k);
-        s += dev_at<T>(P.fam, y, eta, alpha) - dev_at<T>(P.fam, 0.0, eta, alpha);
+        s += dev_at<T>(P.fam, y, eta, alpha) - dev0_at<T>(P.fam, eta, alpha, inv_alpha);
         if (with_const && y > 0.0) c += nb_loglik_term(y, alpha);
       }
     }

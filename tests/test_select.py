@@ -193,3 +193,42 @@ def test_gpu_information_criteria_c3_scale_against_oracle():
     oaic, obic = orc.information_criteria(ost, orc.OProblem(y.astype(float), x, z),
                                           orc.NEG_BINOMIAL, orc.LOG, alpha)
     assert _rel(aic, oaic) < 1e-10 and _rel(bic, obic) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-4)])
+def test_gpu_selection_with_offset_against_oracle(dtype, tol):
+    """c4-style model (intercept-only X, per-row log-library offset, CSR),
+    the SURVEY §8c offset shim on both sides; large counts with a small NB
+    shape stress the zero-grid identity D(0, mu) = 2 alpha log1p(mu / alpha)."""
+    _need_gpu()
+    import scipy.sparse as sp
+    import paper_2412_20509_b200 as gk
+    from paper_2412_20509_b200 import select
+    rng = np.random.default_rng(17)
+    n, m, d, alpha = 3_000, 500, 10, 0.4
+    x = np.ones((n, 1))
+    off = rng.normal(0, 0.7, n)
+    u, v = rng.normal(0, 0.3, (n, d)), rng.normal(0, 0.3, (m, d))
+    b = rng.normal(-1.0, 1.0, (m, 1))
+    eta = u @ v.T + x @ b.T + off[:, None]
+    y = rng.poisson(rng.gamma(alpha, np.exp(eta) / alpha)).astype(np.int32)
+    st = gk.FactorizationState(b, np.zeros((n, 0)), u, v, 1.0, alpha)
+    covs = gk.CovariateSet(x=x, m=m)
+    data = gk.ResponseMatrix(csr=sp.csr_matrix(y), shape=(n, m))
+    fam = gk.NegBinomial(alpha)
+    pb = orc.OProblem(y.astype(float), x, np.zeros((m, 0)), offset=off)
+    ost = orc.OState(b, np.zeros((n, 0)), u, v, 1.0, alpha)
+    aic, bic = select.information_criteria(st, data, covs, fam, gk.Log(), offset=off, dtype=dtype)
+    oaic, obic = orc.information_criteria(ost, pb, orc.NEG_BINOMIAL, orc.LOG, alpha)
+    assert _rel(aic, oaic) < tol and _rel(bic, obic) < tol
+    rows, cols = rng.integers(0, n, 20_000), rng.integers(0, m, 20_000)
+    mu_o = orc.mu_at(ost, pb, orc.LOG, rows, cols)
+    mu_g = select.mu_at(st, covs, gk.Log(), rows, cols, offset=off, dtype=dtype)
+    assert np.max(np.abs(mu_g - mu_o)) / np.max(mu_o) < tol
+    yt = y[rows, cols].astype(float)
+    ybar = float(y.mean())
+    res = select.heldout_scores(st, covs, fam, gk.Log(), rows, cols, yt, ybar, offset=off,
+                                dtype=dtype)
+    assert _rel(res.rel_deviance, orc.rel_deviance(orc.NEG_BINOMIAL, yt, mu_o, ybar, alpha)) < tol
+    assert _rel(res.rel_log_rmse, orc.rel_log_rmse(yt, mu_o, ybar)) < tol

@@ -58,8 +58,9 @@ def main():
     ll_bytes = nnz * 4 + (sp.n + 1) * 8 + sp.n * e * (sp.d + sp.p + 1) + sp.m * e * (sp.d + sp.p)
     out["loglik_full"] = {"ms": ms, "entries_per_s": sp.n * sp.m / (ms * 1e-3),
                           "algorithmic_bytes": ll_bytes, "GB_s": ll_bytes / (ms * 1e-3) / 1e9,
-                          "note": "fp64 exp + log1p per entry over all n*m entries (zeros "
-                                  "analytic) plus lgamma at the nonzeros: FP64-pipe bound"}
+                          "note": "predictor + exp/log1p per entry over all n*m entries "
+                                  "(fp32 transcendentals on the f32 path, fp64 on f64), lgamma "
+                                  "at the nonzeros; instruction-issue bound (ncu)"}
     rng = np.random.default_rng(0)
     nt = 1_000_000
     rows, cols = rng.integers(0, sp.n, nt), rng.integers(0, sp.m, nt)
