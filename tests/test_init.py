@@ -122,3 +122,25 @@ def test_init_rejects_out_of_scope():
         InitMethod(residual_kind="bogus")
     with pytest.raises(NotImplementedError):
         init_ols_svd(gk.ResponseMatrix(y), covs, gk.Gaussian(), gk.Identity(), 1)
+
+
+@pytest.mark.gpu
+def test_gpu_init_wide_sketch_against_oracle():
+    """d = 25: the sketch has k + 10 = 35 > 32 columns, so every sparse
+    product takes two lane passes; Poisson, dense input, q = 1."""
+    _need_gpu()
+    import paper_2412_20509_b200 as gk
+    from paper_2412_20509_b200.initialization import init_ols_svd
+    rng = np.random.default_rng(23)
+    n, m, d = 3_000, 200, 25
+    x = np.ones((n, 1))
+    z = rng.normal(0, 1, (m, 1))
+    eta = rng.normal(0, 0.3, (n, 4)) @ rng.normal(0, 0.3, (m, 4)).T + rng.normal(0.2, 0.5, m)
+    y = rng.poisson(np.exp(eta)).astype(np.int32)
+    st = init_ols_svd(gk.ResponseMatrix(y.astype(float)), gk.CovariateSet(x=x, z=z),
+                      gk.Poisson(), gk.Log(), d, seed=5)
+    ost = orc.init_ols_svd(orc.OProblem(y.astype(float), x, z), d, orc.POISSON, seed=5)
+    assert _nrm(st.b, ost.b) < 1e-10
+    assert _nrm(st.gamma, ost.gamma) < 1e-10
+    assert _nrm(st.u @ st.v.T, ost.u @ ost.v.T) < 1e-8
+    assert st.nb_shape == 1.0
