@@ -36,6 +36,8 @@
  *                             (S' Q through the CSC); the residual's low-rank
  *                             part is applied by the host (no n x m residual)
  *     gmf_init_moments        _nb_shape_moment sums (initialization.py:93-100)
+ *   File formats (io.py:104-109 read_matrix_market, densifying):
+ *     gmf_mm_header/gmf_mm_read_csr  coordinate MatrixMarket -> CSR counts (host)
  *   Level 3 (identify.project_constraints (A)+(B1), identify.py:59-110):
  *     gmf_cross_rows          Z = A' B over rows (Gram / cross products), fp64
  *     gmf_rows_affine         Y <- beta Y + A M, row-local apply of a small matrix
@@ -319,6 +321,17 @@ int gmf_init_moments(int64_t n, int64_t m, const int64_t* ptr, const int32_t* co
                      const int32_t* val, const double* x, const double* b, int32_t p,
                      const double* gamma, const double* z, int32_t q, double eta_lo,
                      double eta_hi, double* out2, void* work, void* stream);
+
+/* --------------------------------------------------------- file formats */
+
+/* Coordinate MatrixMarket -> CSR (host memory, caller-owned).  gmf_mm_header
+ * gives n, m and an upper bound on the stored entries; gmf_mm_read_csr fills
+ * indptr (n+1 int64), indices / counts (cap int32 each; rows column-sorted,
+ * duplicates summed, zeros dropped) and *nnz_out.  integer / real (integral)
+ * / pattern fields, general / symmetric. */
+int gmf_mm_header(const char* path, int64_t* n, int64_t* m, int64_t* max_nnz);
+int gmf_mm_read_csr(const char* path, int64_t cap, int64_t* indptr, int32_t* indices,
+                    int32_t* counts, int64_t* nnz_out);
 
 const char* gmf_last_error(void);
 const char* gmf_version(void);

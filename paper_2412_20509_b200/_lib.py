@@ -129,6 +129,9 @@ SIGNATURES = {
     "gmf_moments_work_bytes": (_i64, []),
     "gmf_init_moments": (C.c_int, [_i64, _i64, _P, _P, _P, _P, _P, _i32, _P, _P, _i32, _d, _d,
                                    _P, _P, _P]),
+    "gmf_mm_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int64)]),
+    "gmf_mm_read_csr": (C.c_int, [C.c_char_p, _i64, _P, _P, _P, C.POINTER(C.c_int64)]),
     "gmf_last_error": (C.c_char_p, []),
     "gmf_version": (C.c_char_p, []),
 }

@@ -392,11 +392,33 @@ def make_init():
     return out
 
 
+def make_mm():
+    """MatrixMarket files and the reference's dense reads of them
+    (io.py:96-109); the files themselves are fixtures under golden/mm/."""
+    import gmfkit.io as gio
+    d = os.path.join(HERE, "mm")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(91)
+    y = rng.poisson(rng.gamma(0.5, 2.0, (50, 20))).astype(float)
+    y[3] = 0.0                                         # an empty row
+    gio.write_matrix_market(os.path.join(d, "counts.mtx"), y)
+    with open(os.path.join(d, "sym_pattern.mtx"), "w") as fh:
+        fh.write("%%MatrixMarket matrix coordinate pattern symmetric\n% a comment\n"
+                 "5 5 4\n1 1\n3 1\n5 2\n4 4\n")
+    with open(os.path.join(d, "dups.mtx"), "w") as fh:
+        fh.write("%%MatrixMarket matrix coordinate integer general\n%\n% comments\n"
+                 "4 6 7\n2 3 4\n1 6 1\n2 3 5\n4 1 0\n\n4 2 7\n3 5 2\n1 1 3\n")
+    out = {}
+    for name in ("counts", "sym_pattern", "dups"):
+        out[name] = gio.read_matrix_market(os.path.join(d, f"{name}.mtx"))
+    return out
+
+
 def main():
     makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
-              "select": make_select, "init": make_init}
+              "select": make_select, "init": make_init, "mm": make_mm}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
