@@ -1,4 +1,4 @@
-"""(A) + (B1)/(B2) identifiability projection on the device
+"""(A) + (B1)/(B2)/(B3) identifiability projection on the device
 (gmfkit/identify.py:59-138).
 
 O(n d^2) work -- Gram matrices and design cross products over the n rows,
@@ -103,8 +103,6 @@ def project_on_device(dev: _Dev, n, m, mode="B1"):
     mode = mode.upper()
     if mode not in ("B1", "B2", "B3"):
         raise ConfigError(f"unknown identifiability mode {mode!r}")
-    if mode == "B3":
-        raise _lib.UnsupportedError("B3 normalization is not implemented on the device path")
     p, q, d = dev.p, dev.q, dev.d
     info = {"mode": mode, "effective_rank": d, "rank_deficient": False}
     tr, tc, x, z = dev.theta_row, dev.theta_col, dev.x, dev.z
@@ -126,6 +124,9 @@ def project_on_device(dev: _Dev, n, m, mode="B1"):
         dev.affine(tc, p, d, 1.0, z, 0, q, -dv)                          # V -= Z D
         dev.affine(tr, 0, q, 1.0, tr, q, d, dv.T)                        # Gamma += U D'
     if d == 0:
+        return info
+    if mode == "B3":
+        _b3(dev, info)
         return info
     # ---- B1/B2 thin-QR SVD of U V' (identify.py:40-45, 93-110) ----
     v = tc[:, p:].double().cpu().numpy()
@@ -160,6 +161,38 @@ def project_on_device(dev: _Dev, n, m, mode="B1"):
     dev.affine(tr, q, d, 0.0, tr, q, d, Mu)
     tc[:, p:] = dev.torch.as_tensor(v_new, device=dev.device, dtype=dev.tdt)
     return info
+
+
+def _b3(dev: _Dev, info):
+    """B3 (identify.py:111-135): whiten U's column covariance, then rotate so
+    V's leading d x d block is lower triangular with a positive diagonal.
+    Column sums and the Gram matrix of U come from the device (fixed-order
+    fp64); the d x d algebra and V (m x d) are host work; U is updated by one
+    row-local affine map U <- U S^{-1/2} Q diag(signs)."""
+    torch, tr, tc, p, q, d = dev.torch, dev.theta_row, dev.theta_col, dev.p, dev.q, dev.d
+    rows = tr.shape[0]
+    ones = torch.ones((rows, 1), device=dev.device, dtype=dev.tdt)
+    mean = dev.cross(ones, 0, 1, tr, q, d) / rows                      # (1, d)
+    G = dev.cross(tr, q, d, tr, q, d)
+    S = (G - rows * mean.T @ mean) / rows
+    S = 0.5 * (S + S.T)
+    try:
+        evals, evecs = np.linalg.eigh(S)
+    except np.linalg.LinAlgError:
+        raise SingularSystemError("whitening of U failed") from None
+    if evals.min() <= rows * np.finfo(float).eps * max(evals.max(), 1.0):
+        info["rank_deficient"] = True
+        info["effective_rank"] = int(np.sum(evals > 0))
+        raise SingularSystemError("U has a degenerate column covariance; B3 whitening undefined")
+    s_inv_half = evecs @ np.diag(evals ** -0.5) @ evecs.T
+    s_half = evecs @ np.diag(evals ** 0.5) @ evecs.T
+    v = tc[:, p:].double().cpu().numpy() @ s_half
+    q_rot, r = np.linalg.qr(v.T)
+    v_new = r.T
+    signs = np.sign(np.diag(v_new[:d, :d]))
+    signs[signs == 0] = 1.0
+    dev.affine(tr, q, d, 0.0, tr, q, d, (s_inv_half @ q_rot) * signs)
+    tc[:, p:] = torch.as_tensor(v_new * signs, device=dev.device, dtype=dev.tdt)
 
 
 def project_constraints(state, covs, mode="B1", return_info=False, dtype="f64", device=None):
@@ -203,8 +236,18 @@ def check_constraints(state, covs, mode="B1") -> dict:
         a, b, nm = vtv, utu, ("v_orthonormality", "u_off_diagonal")
     elif mode == "B2":
         a, b, nm = utu, vtv, ("u_orthonormality", "v_off_diagonal")
+    elif mode == "B3":
+        n = state.n
+        mean = state.u.mean(axis=0, keepdims=True)
+        rep["u_standardized"] = mx((utu - n * mean.T @ mean) / n - np.eye(d))
+        top = state.v[:d, :d]
+        rep["v_upper_triangle"] = mx(top[np.triu_indices(d, k=1)]) if d > 1 else 0.0
+        rep["v_diag_positive"] = float(max(0.0, -np.min(np.diag(top))))
+        rep["normalization"] = max(rep["u_standardized"], rep["v_upper_triangle"],
+                                   rep["v_diag_positive"])
+        return rep
     else:
-        raise ConfigError(f"unsupported identifiability mode {mode!r}")
+        raise ConfigError(f"unknown identifiability mode {mode!r}")
     rep[nm[0]] = mx(a - np.eye(d))
     rep[nm[1]] = mx(b[off])
     rep["sigma_sorted"] = float(max(0.0, np.max(np.diff(np.diag(b)), initial=0.0)))

@@ -414,11 +414,31 @@ def make_mm():
     return out
 
 
+def make_project_b23():
+    """project_constraints in the B2 and B3 modes (identify.py:59-138)."""
+    rng = np.random.default_rng(43)
+    out = {}
+    for k in range(3):
+        n, m, d, p, q = 40 + 7 * k, 12, 3, 2, 1
+        x = np.hstack([np.ones((n, 1)), rng.normal(size=(n, p - 1))])
+        z = np.ones((m, q)) if k != 1 else rng.normal(size=(m, q))
+        covs = gk.CovariateSet(x=x, z=z)
+        st = gk.FactorizationState(b=rng.normal(size=(m, p)), gamma=rng.normal(size=(n, q)),
+                                   u=rng.normal(size=(n, d)), v=rng.normal(size=(m, d)))
+        out.update({f"{k}|x": x, f"{k}|z": z})
+        out.update(_state_arrays(f"{k}|in", st))
+        for mode in ("B2", "B3"):
+            pr = gk.project_constraints(st, covs, mode)
+            out.update(_state_arrays(f"{k}|{mode}", pr))
+    return out
+
+
 def main():
     makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
-              "select": make_select, "init": make_init, "mm": make_mm}
+              "select": make_select, "init": make_init, "mm": make_mm,
+              "project_b23": make_project_b23}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()

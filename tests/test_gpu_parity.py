@@ -332,3 +332,21 @@ def test_c4_full_size_block_gradient_against_oracle():
     assert normwise(out1[1], ref.h_row) < 1e-4
     assert normwise(out1[2], ref_gc) < 1e-4
     assert normwise(out1[3], ref_hc) < 1e-4
+
+
+@pytest.mark.parametrize("mode", ["B2", "B3"])
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-9), ("f32", 1e-4)])
+def test_projection_b2_b3_match_reference(mode, dtype, tol):
+    """B2 and B3 normalizations (identify.py:93-135) on the device against the
+    reference's own projections (tests/golden/project_b23.npz)."""
+    g = golden("project_b23")
+    for k in range(3):
+        st = _state(g, f"{k}|in")
+        covs = gk.CovariateSet(x=g[f"{k}|x"], z=g[f"{k}|z"])
+        out = gk.project_constraints(st, covs, mode, dtype=dtype)
+        ref = _state(g, f"{k}|{mode}")
+        for blk in ("b", "gamma", "u", "v"):
+            assert normwise(getattr(out, blk), getattr(ref, blk)) < tol, (k, mode, blk)
+        if dtype == "f64":
+            rep = gk.check_constraints(out, covs, mode)
+            assert rep["normalization"] < 1e-8 and max(rep.values()) < 1e-8, rep
