@@ -15,12 +15,14 @@
 // malformed file, GMF_ERR_DOMAIN for a negative / non-integral / > 2^31-1
 // value, GMF_ERR_UNSUPPORTED for `array` or complex/hermitian files.
 #include <algorithm>
+#include <chrono>
 #include <cerrno>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gmf_common.cuh"
@@ -100,6 +102,85 @@ int gmf_mm_header(const char* path, int64_t* n, int64_t* m, int64_t* max_nnz) {
   return GMF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+struct Chunk {
+  std::vector<int32_t> r, c;
+  std::vector<int64_t> v;
+  int err = 0;           // GMF_ERR_* of the first bad line
+  const char* bad = nullptr;
+  int64_t parsed = 0;    // coordinate lines seen
+};
+
+inline bool is_sp(char ch) { return ch == ' ' || ch == '\t' || ch == '\r'; }
+
+// parse one unsigned decimal integer; false if no digits
+inline bool parse_u(const char*& p, const char* e, long long& out) {
+  while (p < e && is_sp(*p)) ++p;
+  const char* s0 = p;
+  long long v = 0;
+  while (p < e && *p >= '0' && *p <= '9' && v < (1LL << 60)) v = v * 10 + (*p++ - '0');
+  out = v;
+  return p > s0;
+}
+
+// entries of [b, e) (whole lines); value: integer fast path, strtod otherwise
+void parse_chunk(const char* b, const char* e, const MMHeader& h, Chunk* c) {
+  const char* p = b;
+  const size_t guess = (size_t)(e - b) / 8 + 16;   // ~8+ bytes per coordinate line
+  c->r.reserve(guess); c->c.reserve(guess); c->v.reserve(guess);
+  while (p < e) {
+    const char* line = p;
+    const char* nl = (const char*)memchr(p, '\n', (size_t)(e - p));
+    const char* le = nl ? nl : e;
+    p = nl ? nl + 1 : e;
+    const char* q = line;
+    while (q < le && is_sp(*q)) ++q;
+    if (q == le || *q == '%') continue;
+    long long i, j, v = 1;
+    if (!parse_u(q, le, i) || !parse_u(q, le, j)) { c->err = GMF_ERR_CONFIG; c->bad = line; return; }
+    if (!h.pattern) {
+      while (q < le && is_sp(*q)) ++q;
+      const char* t = q;
+      bool neg = false;
+      if (q < le && (*q == '-' || *q == '+')) neg = *q++ == '-';
+      long long iv = 0;
+      const char* d0 = q;
+      while (q < le && *q >= '0' && *q <= '9' && iv < (1LL << 60)) iv = iv * 10 + (*q++ - '0');
+      if (q < le && !is_sp(*q)) {       // '.', exponent, ... : full float parse
+        char tmp[64];
+        const size_t len = std::min((size_t)(le - t), sizeof tmp - 1);
+        memcpy(tmp, t, len);
+        tmp[len] = 0;
+        char* endp;
+        const double dv = strtod(tmp, &endp);
+        if (endp == tmp) { c->err = GMF_ERR_CONFIG; c->bad = line; return; }
+        if (!(dv >= 0.0) || dv != std::floor(dv) || dv > 2147483647.0) {
+          c->err = GMF_ERR_DOMAIN; c->bad = line; return;
+        }
+        v = (long long)dv;
+      } else {
+        if (q == d0) { c->err = GMF_ERR_CONFIG; c->bad = line; return; }
+        if (neg && iv != 0) { c->err = GMF_ERR_DOMAIN; c->bad = line; return; }
+        if (iv > 2147483647LL) { c->err = GMF_ERR_DOMAIN; c->bad = line; return; }
+        v = iv;
+      }
+    }
+    if (i < 1 || i > h.n || j < 1 || j > h.m) { c->err = GMF_ERR_CONFIG - 100; c->bad = line; return; }
+    ++c->parsed;
+    c->r.push_back((int32_t)(i - 1)); c->c.push_back((int32_t)(j - 1)); c->v.push_back(v);
+    if (h.symmetric && i != j) {
+      c->r.push_back((int32_t)(j - 1)); c->c.push_back((int32_t)(i - 1)); c->v.push_back(v);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int gmf_mm_read_csr(const char* path, int64_t cap, int64_t* indptr, int32_t* indices,
                     int32_t* counts, int64_t* nnz_out) {
   if (!path || !indptr || !nnz_out || (cap > 0 && (!indices || !counts))) {
@@ -113,7 +194,7 @@ int gmf_mm_read_csr(const char* path, int64_t cap, int64_t* indptr, int32_t* ind
   if (rc) { fclose(f); return rc; }
   if (h.n > INT32_MAX || h.m > INT32_MAX) {
     fclose(f);
-    gmf::set_error("%s: dimensions exceed int32 column indices", path);
+    gmf::set_error("%s: dimensions exceed int32 indices", path);
     return GMF_ERR_UNSUPPORTED;
   }
   const int64_t need = h.symmetric ? 2 * h.entries : h.entries;
@@ -123,97 +204,188 @@ int gmf_mm_read_csr(const char* path, int64_t cap, int64_t* indptr, int32_t* ind
                    (long long)need);
     return GMF_ERR_CONFIG;
   }
-  // pass 1: coordinates into (row, col, value) triplets
-  std::vector<int32_t> ri, ci;
-  std::vector<double> vv;
-  ri.reserve(need); ci.reserve(need); vv.reserve(need);
-  char buf[4096];
-  int64_t got = 0;
-  while (got < h.entries && fgets(buf, sizeof buf, f)) {
-    ++h.line;
-    char* p = buf;
-    while (*p == ' ' || *p == '\t') ++p;
-    if (*p == '%' || *p == '\n' || *p == '\r' || *p == 0) continue;
-    char* end;
-    errno = 0;
-    const long long i = strtoll(p, &end, 10);
-    if (end == p) goto malformed;
-    p = end;
-    {
-      const long long j = strtoll(p, &end, 10);
-      if (end == p) goto malformed;
-      p = end;
-      double v = 1.0;
-      if (!h.pattern) {
-        v = strtod(p, &end);
-        if (end == p) goto malformed;
-      }
-      if (i < 1 || i > h.n || j < 1 || j > h.m) {
-        fclose(f);
-        gmf::set_error("%s: line %lld: index (%lld, %lld) out of range", path, (long long)h.line, i, j);
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  const bool verbose = getenv("GMF_VERBOSE") != nullptr;
+  auto lap = [&](const char* what) {
+    if (verbose)
+      fprintf(stderr, "[gmf] mm_read_csr %s: %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(clk::now() - t_start).count());
+  };
+  // the data section in memory, split at line boundaries across threads
+  fseek(f, 0, SEEK_END);
+  const long fend = ftell(f);
+  fseek(f, h.data_offset, SEEK_SET);
+  std::string buf((size_t)(fend - h.data_offset), '\0');
+  const size_t got_bytes = buf.empty() ? 0 : fread(&buf[0], 1, buf.size(), f);
+  fclose(f);
+  buf.resize(got_bytes);
+  lap("read");
+  const char* b = buf.data();
+  const char* e = b + buf.size();
+  unsigned T = std::thread::hardware_concurrency();
+  T = T < 1 ? 1 : (T > 32 ? 32 : T);
+  if (buf.size() < ((size_t)1 << 20)) T = 1;
+  std::vector<const char*> cut(T + 1, e);
+  cut[0] = b;
+  for (unsigned t = 1; t < T; ++t) {
+    const char* x = b + buf.size() * t / T;
+    if (x < cut[t - 1]) x = cut[t - 1];
+    const char* nl = (const char*)memchr(x, '\n', (size_t)(e - x));
+    cut[t] = nl ? nl + 1 : e;
+  }
+  std::vector<Chunk> ch(T);
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(parse_chunk, cut[t], cut[t + 1], std::cref(h), &ch[t]);
+    parse_chunk(cut[0], cut[1], h, &ch[0]);
+    for (auto& x : th) x.join();
+  }
+  lap("parse");
+  int64_t lines = 0;
+  for (unsigned t = 0; t < T; ++t) {
+    if (ch[t].err) {
+      const int64_t ln = h.line + 1 + std::count(b, ch[t].bad, '\n');
+      if (ch[t].err == GMF_ERR_CONFIG - 100) {
+        gmf::set_error("%s: line %lld: index out of range", path, (long long)ln);
         return GMF_ERR_CONFIG;
       }
-      if (!(v >= 0.0) || v != std::floor(v) || v > 2147483647.0) {
-        fclose(f);
-        gmf::set_error("%s: line %lld: value %g is not a count (nonnegative integer < 2^31)", path,
-                       (long long)h.line, v);
+      if (ch[t].err == GMF_ERR_DOMAIN) {
+        gmf::set_error("%s: line %lld: value is not a count (nonnegative integer < 2^31)", path,
+                       (long long)ln);
         return GMF_ERR_DOMAIN;
       }
-      ri.push_back((int32_t)(i - 1)); ci.push_back((int32_t)(j - 1)); vv.push_back(v);
-      if (h.symmetric && i != j) {
-        ri.push_back((int32_t)(j - 1)); ci.push_back((int32_t)(i - 1)); vv.push_back(v);
-      }
-      ++got;
-      continue;
+      gmf::set_error("%s: line %lld: expected 'row col%s'", path, (long long)ln,
+                     h.pattern ? "" : " value");
+      return GMF_ERR_CONFIG;
     }
-  malformed:
-    fclose(f);
-    gmf::set_error("%s: line %lld: expected 'row col%s'", path, (long long)h.line,
-                   h.pattern ? "" : " value");
-    return GMF_ERR_CONFIG;
+    lines += ch[t].parsed;
   }
-  fclose(f);
-  if (got < h.entries) {
+  if (lines != h.entries) {
     gmf::set_error("%s: %lld entries declared, %lld found", path, (long long)h.entries,
-                   (long long)got);
+                   (long long)lines);
     return GMF_ERR_CONFIG;
   }
-  // pass 2: counting sort by row, then each row sorted by column with
-  // duplicates summed (scipy coo -> dense adds them) and zeros dropped
-  const int64_t t = (int64_t)ri.size();
+  // CSR by two stable counting sorts -- by column, then by row -- so every
+  // row comes out column-sorted with duplicates adjacent (file order among
+  // equal coordinates); duplicates are summed (scipy coo -> dense adds them)
+  // and zeros dropped.  O(nnz + n + m), no per-row sorting.
+  // Fast path: files written row by row (scipy's mmwrite of a dense or CSR
+  // matrix, most count-matrix exports) are already grouped by row; then only
+  // rows whose columns are out of order are sorted, locally.
+  bool row_sorted = true;
+  {
+    int32_t prev = 0;
+    for (auto& c : ch) {
+      for (int32_t r : c.r) {
+        if (r < prev) { row_sorted = false; break; }
+        prev = r;
+      }
+      if (!row_sorted) break;
+    }
+  }
+  if (row_sorted && !h.symmetric) {
+    std::vector<int32_t> cc;
+    std::vector<int64_t> vv, rowp(h.n + 1, 0);
+    for (auto& c : ch)
+      for (int32_t r : c.r) ++rowp[r + 1];
+    for (int64_t r = 0; r < h.n; ++r) rowp[r + 1] += rowp[r];
+    cc.reserve(rowp[h.n]);
+    vv.reserve(rowp[h.n]);
+    for (auto& c : ch) {
+      cc.insert(cc.end(), c.c.begin(), c.c.end());
+      vv.insert(vv.end(), c.v.begin(), c.v.end());
+    }
+    lap("scatter");
+    std::vector<std::pair<int32_t, int64_t>> row;
+    int64_t w = 0;
+    indptr[0] = 0;
+    for (int64_t r = 0; r < h.n; ++r) {
+      const int64_t lo = rowp[r], hi = rowp[r + 1];
+      bool sorted = true;
+      for (int64_t k = lo + 1; k < hi && sorted; ++k) sorted = cc[k] > cc[k - 1];
+      if (!sorted) {
+        row.clear();
+        for (int64_t k = lo; k < hi; ++k) row.emplace_back(cc[k], vv[k]);
+        std::stable_sort(row.begin(), row.end(),
+                         [](const std::pair<int32_t, int64_t>& a,
+                            const std::pair<int32_t, int64_t>& x) { return a.first < x.first; });
+        for (int64_t k = lo; k < hi; ++k) { cc[k] = row[k - lo].first; vv[k] = row[k - lo].second; }
+      }
+      for (int64_t k = lo; k < hi;) {
+        int64_t e2 = k, sum = 0;
+        while (e2 < hi && cc[e2] == cc[k]) sum += vv[e2++];
+        if (sum > 2147483647LL) {
+          gmf::set_error("%s: summed duplicate entry exceeds int32", path);
+          return GMF_ERR_DOMAIN;
+        }
+        if (sum != 0) {
+          indices[w] = cc[k];
+          counts[w] = (int32_t)sum;
+          ++w;
+        }
+        k = e2;
+      }
+      indptr[r + 1] = w;
+    }
+    *nnz_out = w;
+    lap("rows (row-sorted input)");
+    return GMF_OK;
+  }
+  std::vector<int64_t> cstart(h.m + 1, 0);
+  for (auto& c : ch)
+    for (int32_t j : c.c) ++cstart[j + 1];
+  for (int64_t j = 0; j < h.m; ++j) cstart[j + 1] += cstart[j];
+  const int64_t t_all = cstart[h.m];
+  std::vector<int32_t> r1(t_all), c1(t_all);
+  std::vector<int64_t> v1(t_all);
+  for (auto& c : ch) {
+    for (size_t k = 0; k < c.c.size(); ++k) {
+      const int64_t at = cstart[c.c[k]]++;
+      r1[at] = c.r[k];
+      c1[at] = c.c[k];
+      v1[at] = c.v[k];
+    }
+    std::vector<int32_t>().swap(c.r);
+    std::vector<int32_t>().swap(c.c);
+    std::vector<int64_t>().swap(c.v);
+  }
   std::vector<int64_t> start(h.n + 1, 0);
-  for (int64_t k = 0; k < t; ++k) ++start[ri[k] + 1];
+  for (int64_t k = 0; k < t_all; ++k) ++start[r1[k] + 1];
   for (int64_t r = 0; r < h.n; ++r) start[r + 1] += start[r];
-  std::vector<int64_t> fill(start.begin(), start.end() - 1), order(t);
-  for (int64_t k = 0; k < t; ++k) order[fill[ri[k]]++] = k;
+  std::vector<int32_t> cc(t_all);
+  std::vector<int64_t> vv(t_all);
+  {
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t k = 0; k < t_all; ++k) {
+      const int64_t at = fill[r1[k]]++;
+      cc[at] = c1[k];
+      vv[at] = v1[k];
+    }
+  }
+  lap("scatter");
   int64_t w = 0;
   indptr[0] = 0;
-  std::vector<std::pair<int32_t, double>> row;
   for (int64_t r = 0; r < h.n; ++r) {
-    row.clear();
-    for (int64_t k = start[r]; k < start[r + 1]; ++k) row.emplace_back(ci[order[k]], vv[order[k]]);
-    std::stable_sort(row.begin(), row.end(),
-                     [](const std::pair<int32_t, double>& a, const std::pair<int32_t, double>& b) {
-                       return a.first < b.first;
-                     });
-    for (size_t k = 0; k < row.size();) {
-      size_t e = k;
-      double sum = 0.0;
-      while (e < row.size() && row[e].first == row[k].first) sum += row[e++].second;
-      if (sum > 2147483647.0) {
+    const int64_t lo = start[r], hi = start[r + 1];
+    for (int64_t k = lo; k < hi;) {
+      int64_t e2 = k, sum = 0;
+      while (e2 < hi && cc[e2] == cc[k]) sum += vv[e2++];
+      if (sum > 2147483647LL) {
         gmf::set_error("%s: summed duplicate entry exceeds int32", path);
         return GMF_ERR_DOMAIN;
       }
-      if (sum != 0.0) {
-        indices[w] = row[k].first;
+      if (sum != 0) {
+        indices[w] = cc[k];
         counts[w] = (int32_t)sum;
         ++w;
       }
-      k = e;
+      k = e2;
     }
     indptr[r + 1] = w;
   }
   *nnz_out = w;
+  lap("rows");
   return GMF_OK;
 }
 
