@@ -143,12 +143,6 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }
-  if (h->NK > 32 && desc->dtype == GMF_F64) {
-    set_error("p+q+d = %d > 32 is supported in fp32 only (the fp64 K1 tile does not fit in "
-              "shared memory at that width)", KA);
-    delete h;
-    return GMF_ERR_UNSUPPORTED;
-  }
   h->tsz = desc->dtype == GMF_F64 ? 8 : 4;
   const int64_t R = bufs->n_row_blocks, S = bufs->n_col_blocks;
   h->rbp_host.resize(R + 1);
@@ -236,6 +230,16 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
 
   // persistent kernel geometry: every co-resident CTA, a multiple of CT
   int fit_bps = 0;
+  int smem_optin = 0;
+  GMF_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device));
+  const int64_t k1_smem = grad_smem_bytes(desc->dtype, h->NK, P.has_w, Kr, Kc, P.tcm);
+  if (k1_smem > smem_optin) {
+    set_error("the K1 tile for p+q+d = %d (%s%s) needs %lld B of shared memory, the device "
+              "allows %d", KA, desc->dtype == GMF_F64 ? "fp64" : "fp32",
+              P.has_w ? ", prior weights" : "", (long long)k1_smem, smem_optin);
+    delete h;
+    return GMF_ERR_UNSUPPORTED;
+  }
   rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, 0, &fit_bps);
   if (rc) { delete h; return rc; }
   {
@@ -245,7 +249,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     GMF_CUDA(cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, desc->device));
     const int grid0 = P.CT > 0 ? (fit_bps * n_sm0 / P.CT) * P.CT : 0;   // = fit_grid below
     const int64_t cap = grid0 > 0 ? (bufs->n_eval + grid0 - 1) / grid0 : 0;
-    if (cap > 0 && cap <= 1024) {
+    if (cap > 0 && cap <= 1024 && k1_smem + cap * 16 <= smem_optin) {
       int bps2 = 0;
       rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm,
                         (int)(cap * 16), &bps2);

@@ -788,8 +788,8 @@ static void* pick(int NK, bool fit) {
     case 16: return fit ? Inst<T, FAM, 16, TCM>::fit() : Inst<T, FAM, 16, TCM>::grad();
     case 24: return fit ? Inst<T, FAM, 24, TCM>::fit() : Inst<T, FAM, 24, TCM>::grad();
     case 32: return fit ? Inst<T, FAM, 32, TCM>::fit() : Inst<T, FAM, 32, TCM>::grad();
-    case 64:   // K = p+q+d in (32, 64]: fp32 CUDA-core K1 only (c5's rank 50)
-      if constexpr (!TCM && sizeof(T) == 4)
+    case 64:   // K = p+q+d in (32, 64]: CUDA-core K1 only (c5's rank 50)
+      if constexpr (!TCM)
         return fit ? Inst<T, FAM, 64, false>::fit() : Inst<T, FAM, 64, false>::grad();
       return nullptr;
     default: return nullptr;

@@ -115,7 +115,10 @@ GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
   auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
   s.rd = o; o = al(o + (int64_t)2 * TC * NK * tsz);
   s.P = o; o = al(o + (int64_t)2 * TC * (TR + 1) * tsz);
-  const int64_t red = (int64_t)NQ * 2 * Kr * (TR + 1) * tsz;
+  // fp64 at K > 32: the row-side reduction runs in two passes over halves of
+  // the Kr features so its buffer (and the tile) fits in shared memory
+  const int KrR = (tsz == 8 && NK > 32) ? (Kr + 1) / 2 : Kr;
+  const int64_t red = (int64_t)NQ * 2 * KrR * (TR + 1) * tsz;
   const int64_t cp = (int64_t)TC * (2 * Kc + 1) * tsz;
   s.red = o; o = al(o + red);   // (column partials reuse the P region at the end)
   (void)cp;
@@ -437,20 +440,28 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         for (int k = 0; k < NK; ++k) acc[k] = fma(pv, rd[k], acc[k]);
       }
     }
+    constexpr bool kSplit = sizeof(T) == 8 && NK > 32;
+    const int KrR = kSplit ? (Kr + 1) / 2 : Kr;
     #pragma unroll
-    for (int k = 0; k < NK; ++k)
-      if (k < Kr) red_s[((pq * 2 + ph) * Kr + k) * (TR + 1) + pr] = acc[k];
-    __syncthreads();
-    {
+    for (int pass = 0; pass < (kSplit ? 2 : 1); ++pass) {
+      const int k0 = pass * KrR, k1 = min(Kr, k0 + KrR);
+      if (pass) __syncthreads();   // previous pass's readers are done with red_s
+      #pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (k >= k0 && k < k1) red_s[((pq * 2 + ph) * KrR + (k - k0)) * (TR + 1) + pr] = acc[k];
+      __syncthreads();
       // o = rr * rkk + hk walked incrementally (no runtime division per element)
       T* outp = tptr<T>(P.rowpart) + ((int64_t)ct * P.nstar_max + rowbase) * rkk;
       int rr = o_rr0, hk = o_hk0;
       for (int o = tid; o < rows * rkk; o += kThreads) {
         const int h = hk >= Kr ? 1 : 0, k = hk - h * Kr;
-        T sum = T(0);
-        #pragma unroll
-        for (int qq = 0; qq < NQ; ++qq) sum += red_s[((qq * 2 + h) * Kr + k) * (TR + 1) + rr];
-        outp[o] = sum;
+        if (!kSplit || (k >= k0 && k < k1)) {
+          T sum = T(0);
+          #pragma unroll
+          for (int qq = 0; qq < NQ; ++qq)
+            sum += red_s[((qq * 2 + h) * KrR + (k - k0)) * (TR + 1) + rr];
+          outp[o] = sum;
+        }
         rr += o_dq;
         hk += o_dr;
         if (hk >= rkk) { hk -= rkk; ++rr; }

@@ -126,10 +126,11 @@ def test_fit_with_ragged_blocks_matches_oracle(dtype, tol):
     assert normwise(final.u @ final.v.T, ofinal.u @ ofinal.v.T) < tol
 
 
-@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4)])
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("f64", 1e-10)])
 def test_rank50_gradient_uses_64_feature_bucket(dtype, tol):
-    """c5's largest rank: K = p + q + d = 52 > 32 runs the fp32 CUDA-core K1
-    in the 64-feature bucket (64-column tiles; the tensor path is limited to
+    """c5's largest rank: K = p + q + d = 52 > 32 runs the CUDA-core K1 in the
+    64-feature bucket (fp32: 64-column tiles; fp64: 32-column tiles with the
+    row-side reduction in two feature halves; the tensor path is limited to
     q+d, p+d <= 16)."""
     rng = np.random.default_rng(6)
     n, m, d = 300, 180, 50
@@ -143,17 +144,48 @@ def test_rank50_gradient_uses_64_feature_bucket(dtype, tol):
     assert max(errs.values()) < tol, errs
 
 
-def test_rank50_fp64_is_rejected_cleanly():
-    """fp64 at K > 32 does not fit the CUDA-core K1 tile: UnsupportedError."""
+def test_oversize_k1_tile_is_rejected_cleanly():
+    """fp64 with prior weights at K = 64: the K1 tile exceeds the 227 KB of
+    shared memory a CTA may use -> UnsupportedError, not a CUDA error."""
     from paper_2412_20509_b200 import _lib
     rng = np.random.default_rng(8)
-    n, m, d = 40, 30, 40
-    st = _state(rng, n, m, d, 1, 0)
+    n, m, d = 80, 40, 62
+    st = _state(rng, n, m, d, 1, 1)
     y = rng.poisson(2.0, (n, m)).astype(float)
+    w = rng.uniform(0.5, 2.0, (n, m))
     with pytest.raises(_lib.UnsupportedError):
-        gk.minibatch_gradients(st, gk.ResponseMatrix(y), gk.CovariateSet(x=np.ones((n, 1)), n=n, m=m),
+        gk.minibatch_gradients(st, gk.ResponseMatrix(y, weights=w),
+                               gk.CovariateSet(x=np.ones((n, 1)), z=np.ones((m, 1))),
                                gk.Poisson(), gk.Log(), gk.PenaltyConfig(),
                                gk.Minibatch(np.arange(n), np.arange(m)), dtype="f64")
+
+
+@pytest.mark.parametrize("y_format", ["dense", "csr"])
+def test_rank50_fp64_fit_matches_oracle(y_format):
+    """fp64 at rank 50 (persistent kernel, split row reduction) follows the
+    oracle's fit at fp64 tolerance, dense and CSR."""
+    rng = np.random.default_rng(17)
+    n, m, d = 160, 90, 50
+    st = _state(rng, n, m, d, 1, 0)
+    st.u *= 0.2
+    st.v *= 0.2
+    x = np.ones((n, 1))
+    y = rng.poisson(2.0, (n, m)).astype(float)
+    cfg = gk.SgdConfig(max_epochs=5, mb_rows=40, mb_cols=m, tol=1e-30, seed=3)
+    if y_format == "csr":
+        import scipy.sparse as sp
+        data = gk.ResponseMatrix(csr=sp.csr_matrix(y.astype(np.int32)), shape=(n, m))
+    else:
+        data = gk.ResponseMatrix(y)
+    final, rep = gk.fit_asgd(data, gk.CovariateSet(x=x, n=n, m=m), gk.NegBinomial(2.0),
+                             gk.Log(), gk.PenaltyConfig(), cfg, st, dtype="f64")
+    pb = orc.OProblem(y, x, np.zeros((m, 0)))
+    ost = orc.OState(st.b, st.gamma, st.u, st.v, 1.0, 2.0)
+    ocfg = orc.OConfig(max_epochs=5, mb_rows=40, mb_cols=m, tol=1e-30, seed=3)
+    ofinal, orep = orc.fit_asgd(pb, orc.NEG_BINOMIAL, orc.LOG, (0.0, 0.0, 1.0, 0.0), ocfg, ost)
+    assert len(rep.objective_trace) == len(orep.objective_trace)
+    assert normwise(rep.objective_trace, orep.objective_trace) < 1e-10
+    assert normwise(final.u @ final.v.T, ofinal.u @ ofinal.v.T) < 1e-9
 
 
 def test_rank50_fit_matches_oracle():

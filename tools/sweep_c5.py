@@ -12,9 +12,9 @@ then times K steps of one persistent launch with CUDA events, and, as a
 second figure, the block gradient K1 alone (per-step kernel, gmf_time_grad).
 Reported per cell: step and K1 time, entries/s (n* m per step), algorithmic
 bytes per step (bench._step_bytes) and the achieved fraction of
-the measured HBM bandwidth.  fp64 at K = p+q+d > 32 (d = 50) is not
-supported (the fp64 K1 tile does not fit in shared memory) and is reported
-as such.
+the measured HBM bandwidth.  fp64 at K = p+q+d > 32 (d = 50) runs the
+fp64 64-feature bucket (32-column tiles, row-side reduction in two feature
+halves).
 
 usage: python tools/sweep_c5.py [--steps K] [--warmup W] [--quick] > out.jsonl
 """
@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--quick", action="store_true", help="m = 500 only")
+    ap.add_argument("--only-d", type=int, default=None, help="one rank only")
+    ap.add_argument("--only-dtype", default=None, help="f32 or f64 only")
     args = ap.parse_args()
     import torch
     import paper_2412_20509_b200 as gk
@@ -61,12 +63,12 @@ def main():
             print(json.dumps({"gen": {"m": m, "format": fmt, "seconds": round(gen_s, 1),
                                       "zero_frac": round(wl.meta["zero_frac"], 4)}}), flush=True)
             rng = np.random.default_rng(0)
-            for d in (5, 15, 50):
+            for d in ((args.only_d,) if args.only_d else (5, 15, 50)):
                 st = gk.FactorizationState(wl.truth["b"], wl.truth["gamma"],
                                            0.3 * rng.standard_normal((N, d)),
                                            0.3 * rng.standard_normal((m, d)), 1.0, 2.0)
                 for family in ("poisson", "nb"):
-                    for dtype in ("f32", "f64"):
+                    for dtype in ((args.only_dtype,) if args.only_dtype else ("f32", "f64")):
                         for nstar in (256, 4096, 65536):
                             cell = {"nstar": nstar, "m": m, "d": d, "family": family,
                                     "dtype": dtype, "format": fmt}
