@@ -37,6 +37,26 @@ from .model import CovariateSet, FactorizationState, ResponseMatrix
 
 __all__ = ["InitMethod", "init_ols_svd", "randomized_svd_sparse"]
 
+
+class _Laps:
+    """GMF_VERBOSE=1: per-stage wall clock (device synchronised) to stderr."""
+
+    def __init__(self):
+        import os
+        import time
+        self.on = bool(os.environ.get("GMF_VERBOSE"))
+        self.time = time
+        self.t0 = time.perf_counter()
+
+    def __call__(self, what):
+        if self.on:
+            import sys
+            import torch
+            torch.cuda.synchronize()
+            print(f"[gmf] init_ols_svd {what}: {1e3 * (self.time.perf_counter() - self.t0):.1f} ms",
+                  file=sys.stderr)
+
+
 _LINK_EPS = {"log": 0.1, "logit": 0.01, "inverse": 0.1, "inverse_squared": 0.1}
 _DAMPING = 1e-8            # glm.py:68 fit_glm_batched default
 _ETA_CLIP_LOG = (-700.0, 700.0)   # initialization.py:217-220
@@ -182,7 +202,9 @@ def init_ols_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
                        int(str(device).split(":")[-1]))
     eps = method.eps_for(lnk)
     leps = math.log(eps)
+    lap = _Laps()
     Y = _SparseCounts(data, dev)
+    lap("upload + CSC")
     f64 = dict(dtype=torch.float64, device=dev)
     X = torch.from_numpy(np.ascontiguousarray(covs.x, dtype=float)).to(dev)
     Z = torch.from_numpy(np.ascontiguousarray(covs.z, dtype=float)).to(dev)
@@ -202,12 +224,14 @@ def init_ols_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
     else:
         Gm = torch.zeros((n, 0), **f64)
 
+    lap("OLS stages")
     # residual SVD (initialization.py:159-162)
     L = torch.cat([ones_n, X, Gm], 1)
     R = torch.cat([leps * ones_m, -B, -Z], 1)
     left, sing, right = randomized_svd_sparse(Y, eps, L, R, d, seed=seed)
     U = left * sing
     V = right
+    lap("randomized SVD")
 
     nb_shape = 1.0
     if fam.kind == "neg_binomial":    # initialization.py:93-100 at mu0 (164-166)
@@ -221,7 +245,9 @@ def init_ols_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
                                         _lib.ptr(work), stream), "gmf_init_moments")
         num, den = (float(v) for v in out.cpu().numpy())
         nb_shape = 1e8 if den <= 0 else float(np.clip(num / den, 1e-4, 1e8))
+    lap("NB moments")
     host = lambda t: t.cpu().numpy()
     state = FactorizationState(host(B), host(Gm), host(U), host(V), 1.0, nb_shape)
+    lap("download")
     info = {"method": "ols_svd"}
     return (state, info) if return_info else state
