@@ -67,8 +67,21 @@ def _solve(gram, rhs, what):
             f"rank-deficient design while removing the covariate span from {what}") from None
 
 
+def _eig_factor(G, n, m):
+    """R with R'R = G (rows of dropped directions zero) and its pseudo-inverse."""
+    lam, E = np.linalg.eigh(G)
+    lmax = max(lam.max(), 0.0)
+    keep = lam > max(n, m) * np.finfo(float).eps * lmax
+    s = np.zeros_like(lam)
+    s[keep] = np.sqrt(lam[keep])
+    inv = np.zeros_like(lam)
+    inv[keep] = 1.0 / s[keep]
+    return (E * s).T, E * inv
+
+
 def _u_factor(dev: _Dev, n, m):
-    """(M1 applied in place to U, pinv(R)) such that U_cur = Q R after step."""
+    """(R_U, P) with U_orig = Q R_U, where P is the d x d map that, applied to
+    the CURRENT device U, yields Q (CholeskyQR2; eigen fallback)."""
     q, d = dev.q, dev.d
     G = dev.cross(dev.theta_row, q, d, dev.theta_row, q, d)
     G = 0.5 * (G + G.T)
@@ -77,25 +90,20 @@ def _u_factor(dev: _Dev, n, m):
         dg = np.diag(L1)
         if dg.min() <= 1e-7 * dg.max():
             raise np.linalg.LinAlgError
-        # CholeskyQR2: Q1 = U R1^-1 on the device, then R2 from Q1'Q1
-        R1inv = np.linalg.inv(L1.T)
-        dev.affine(dev.theta_row, q, d, 0.0, dev.theta_row, q, d, R1inv)
-        G2 = dev.cross(dev.theta_row, q, d, dev.theta_row, q, d)
-        G2 = 0.5 * (G2 + G2.T)
-        L2 = np.linalg.cholesky(G2)
-        R2 = L2.T
-        return R2 @ L1.T, np.linalg.inv(R2)      # (R_U, pinv applied to current U)
     except np.linalg.LinAlgError:
-        lam, E = np.linalg.eigh(G)
-        lmax = max(lam.max(), 0.0)
-        keep = lam > max(n, m) * np.finfo(float).eps * lmax
-        s = np.zeros_like(lam)
-        s[keep] = np.sqrt(lam[keep])
-        inv = np.zeros_like(lam)
-        inv[keep] = 1.0 / s[keep]
-        R = (E * s).T                     # d x d, rows of dropped directions are 0
-        Rpinv = E * inv                   # d x d pseudo-inverse
-        return R, Rpinv
+        return _eig_factor(G, n, m)       # device U untouched
+    # CholeskyQR2: Q1 = U R1^-1 on the device, then R2 from Q1'Q1
+    R1 = L1.T
+    dev.affine(dev.theta_row, q, d, 0.0, dev.theta_row, q, d, np.linalg.inv(R1))
+    # from here on the device holds Q1: every factor is taken of Q1 itself
+    G2 = dev.cross(dev.theta_row, q, d, dev.theta_row, q, d)
+    G2 = 0.5 * (G2 + G2.T)
+    try:
+        R2 = np.linalg.cholesky(G2).T
+        P2 = np.linalg.inv(R2)
+    except np.linalg.LinAlgError:
+        R2, P2 = _eig_factor(G2, n, m)
+    return R2 @ R1, P2
 
 
 def project_on_device(dev: _Dev, n, m, mode="B1"):

@@ -228,12 +228,7 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
         def host_state(snapshot, nb):
             if world == 1:
                 return fit.download_state(snapshot=snapshot, nb_shape=nb)
-            tr = _gather_rows(fit, fit.snapshot_rows() if snapshot else fit.theta_row, process_group,
-                              exchange)
-            tc = (fit.snap_col if snapshot else fit.theta_col).double().cpu().numpy()
-            p, q = covs.p, covs.q
-            return FactorizationState(tc[:, :p].copy(), tr[:, :q].copy(), tr[:, q:].copy(),
-                                      tc[:, p:].copy(), fit.phi, nb)
+            return _gathered_state(fit, process_group, exchange, nb, snapshot)
 
         if st.diverged:
             snap_nb = float(nb_trace[max(int(st.snapshot_trace_len) - 1, 0)])
@@ -283,6 +278,15 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
         fit.close()
 
 
+def _gathered_state(fit: DeviceFit, group, exchange, nb_shape, snapshot=False):
+    """Host FactorizationState of a row-sharded fit (collective over the group)."""
+    tr = _gather_rows(fit, fit.snapshot_rows() if snapshot else fit.theta_row, group, exchange)
+    tc = (fit.snap_col if snapshot else fit.theta_col).double().cpu().numpy()
+    p, q = fit.p, fit.q
+    return FactorizationState(tc[:, :p].copy(), tr[:, :q].copy(), tr[:, q:].copy(),
+                              tc[:, p:].copy(), fit.phi, nb_shape)
+
+
 def _drive(fit: DeviceFit, callback, group, exchange):
     """Run steps until the device tracker stops (converged / diverged /
     max_epochs); the host only polls the status word between chunks."""
@@ -297,7 +301,8 @@ def _drive(fit: DeviceFit, callback, group, exchange):
             if callback is not None or t % 32 == 0 or t >= total:
                 st = fit.status()
                 if callback is not None and st.t > prev:
-                    callback(int(st.t) - 1, None)
+                    # collective: every rank gathers the live state (optim.py:474-475)
+                    callback(int(st.t) - 1, _gathered_state(fit, group, exchange, st.nb_shape))
                 if st.stopped:
                     return
         return

@@ -169,3 +169,34 @@ def test_packed_csr_round_trip():
     assert np.array_equal(c2, cols) and np.array_equal(v2, counts)
     assert packable(65536, counts) and not packable(65537, counts)
     assert not packable(10, np.array([0, 65536])) and packable(10, np.array([], dtype=int))
+
+
+def test_csr_input_is_canonicalized():
+    """Unsorted rows, duplicate coordinates and explicit zeros are rewritten
+    to the canonical CSR of the dense matrix the reference sees (duplicates
+    summed, as scipy's densify does; io.py:104-109)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(3)
+    n, m, nnz = 40, 17, 300
+    r = rng.integers(0, n, nnz)
+    c = rng.integers(0, m, nnz)
+    v = rng.integers(0, 4, nnz)            # includes explicit zeros
+    coo = sp.coo_matrix((v, (r, c)), shape=(n, m))
+    dense = coo.toarray()
+    # a deliberately non-canonical CSR: rows grouped, columns shuffled inside rows
+    order = np.lexsort((rng.random(nnz), r))
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=indptr[1:])
+    data = gk.ResponseMatrix(csr=(indptr, c[order], v[order]), shape=(n, m))
+    ip, ix, dv = data.csr
+    assert np.all(dv != 0)
+    for i in range(n):
+        cols = ix[ip[i]:ip[i + 1]]
+        assert np.all(np.diff(cols) > 0)
+    back = sp.csr_matrix((dv, ix, ip), shape=(n, m)).toarray()
+    np.testing.assert_array_equal(back, dense)
+    # canonical input passes through unchanged (no copy)
+    canon = sp.csr_matrix(dense)
+    canon.eliminate_zeros()
+    d2 = gk.ResponseMatrix(csr=canon, shape=(n, m))
+    assert d2.csr[1] is not None and np.array_equal(d2.csr[1], canon.indices)
