@@ -22,6 +22,9 @@ Fixtures:
   seam.npz        derivs_from_mu / deviance / mean_of_eta vectors, all families.
   project.npz     (A)+(B1) projections incl. a rank-deficient case.
   weighted.npz    minibatch gradients with non-unit prior weights.
+  c2.npz          BASELINE config 2 at full size (26,472 x 500 NB fp64, k=15,
+                  offset), 20 epochs: traces, final objective, V/B at check
+                  steps, projected V/B and U at a row sample (make_c2).
 """
 from __future__ import annotations
 
@@ -34,6 +37,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
 os.environ.setdefault("GMFKIT_PURE_PYTHON", "1")
 
 import gmfkit as gk                      # noqa: E402
@@ -152,6 +156,52 @@ def make_c1():
                   nb_shape=init.nb_shape)
     cfg = gk.SgdConfig(max_epochs=50, mb_rows=100, mb_cols=100, tol=1e-30, seed=0)
     return _run_fit(y, wl.x, wl.z, init_d, gk.Poisson(), cfg)
+
+
+C2_EPOCHS = 20
+C2_CHECK = (0, 1, 4, 9, 19)
+
+
+from make_golden_checksum import y_checksum  # noqa: E402
+
+
+def make_c2():
+    """BASELINE config 2 at FULL size (26,472 x 500 NB, k=15, fp64, centred
+    log-library offset through the SURVEY 8c shim, mb 2,000 rows x all
+    columns) run by gmfkit itself for C2_EPOCHS epochs (tol 1e-30).  The
+    counts and init are regenerated from the seeded workload generator at
+    test time (checksum stored); the fixture keeps the traces, the final
+    objective, V/B at check steps and the projected state's V, B and U at a
+    fixed row sample."""
+    wl = workloads.generate("c2")
+    y = wl.y_dense
+    init = wl.init_state()
+    cfg = gk.SgdConfig(max_epochs=C2_EPOCHS, mb_rows=2000, mb_cols=500, tol=1e-30, seed=0)
+    data = gk.ResponseMatrix(y.astype(float))
+    covs = gk.CovariateSet(x=wl.x, z=None, n=y.shape[0], m=y.shape[1])
+    st0 = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], 1.0,
+                                init["nb_shape"])
+    steps = {}
+
+    def cb(t, st):
+        if t in C2_CHECK:
+            steps[t] = (st.b.copy(), st.v.copy(), float(st.nb_shape))
+
+    with OffsetShim(wl.offset):
+        final, rep = gk.fit_asgd(data, covs, gk.NegBinomial(init["nb_shape"]), gk.Log(),
+                                 gk.PenaltyConfig(), cfg, st0, callback=cb)
+    rows = np.sort(np.random.default_rng(11).choice(y.shape[0], 600, replace=False))
+    out = {"y_checksum": y_checksum(y), "trace": np.asarray(rep.objective_trace),
+           "nb_trace": np.asarray(rep.nb_shape_trace),
+           "final_objective": np.float64(rep.final_objective),
+           "epochs_run": np.int64(rep.epochs_run),
+           "iterations": np.int64(rep.diagnostics["iterations"]),
+           "final_b": final.b, "final_v": final.v, "final_nb": np.float64(final.nb_shape),
+           "sample_rows": rows, "final_u_rows": final.u[rows],
+           "check_steps": np.asarray(sorted(steps), dtype=np.int64)}
+    for t, (b, v, nb) in steps.items():
+        out[f"step{t}_b"], out[f"step{t}_v"], out[f"step{t}_nb"] = b, v, np.float64(nb)
+    return out
 
 
 def _nb_problem(n, m, p, q, d, seed, offset):
@@ -438,7 +488,7 @@ def main():
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,
-              "project_b23": make_project_b23}
+              "project_b23": make_project_b23, "c2": make_c2}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()

@@ -143,3 +143,46 @@ def test_known_answers():
     # Poisson deviance D(2, 1) = 2(2 ln 2 - 1), tests/test_families.py:42-44
     d = orc.unit_deviance(orc.POISSON, np.array([2.0]), np.array([1.0]), 1.0)[0]
     assert d == pytest.approx(2 * (2 * np.log(2) - 1))
+
+
+def _c2_oracle(callback=None, csr=False):
+    from paper_2412_20509_b200 import workloads
+    wl = workloads.generate("c2")
+    init = wl.init_state()
+    y = wl.y_dense
+    yy = orc.CsrRows(*workloads.dense_to_csr(y), y.shape) if csr else y.astype(float)
+    pb = orc.OProblem(yy, wl.x, np.zeros((y.shape[1], 0)), offset=wl.offset)
+    st = orc.OState(init["b"], init["gamma"], init["u"], init["v"], 1.0, init["nb_shape"])
+    cfg = orc.OConfig(max_epochs=20, mb_rows=2000, mb_cols=500, tol=1e-30, seed=0)
+    return wl, orc.fit_asgd(pb, orc.NEG_BINOMIAL, orc.LOG, (0.0, 0.0, 1.0, 0.0), cfg, st,
+                            callback=callback)
+
+
+@pytest.mark.parametrize("csr", [False, True])
+def test_oracle_c2_full_size_matches_reference(csr):
+    """BASELINE config 2 at full size (26,472 x 500 NB fp64, k=15, offset):
+    the oracle against gmfkit's own 20-epoch run (tests/golden/c2.npz); the
+    CSR-backed response (used for configs too large to densify) is the same
+    arithmetic."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_golden_checksum import y_checksum
+    g = golden("c2")
+    seen = {}
+    checks = set(g["check_steps"].tolist())
+
+    def cb(t, st):
+        if t in checks:
+            seen[t] = (st.b.copy(), st.v.copy(), st.nb_shape)
+
+    wl, (final, rep) = _c2_oracle(cb, csr)
+    assert np.array_equal(y_checksum(wl.y_dense), g["y_checksum"])
+    assert rep.iterations == int(g["iterations"])
+    assert normwise(rep.objective_trace, g["trace"]) < 1e-12
+    assert normwise(rep.nb_shape_trace, g["nb_trace"]) < 1e-12
+    for t, (b, v, nb) in seen.items():
+        assert normwise(v, g[f"step{t}_v"]) < 1e-10, t
+        assert normwise(b, g[f"step{t}_b"]) < 1e-10, t
+    rows = g["sample_rows"]
+    assert normwise(final.u[rows] @ final.v.T, g["final_u_rows"] @ g["final_v"].T) < 1e-9
+    assert rep.final_objective == pytest.approx(float(g["final_objective"]), rel=1e-11)
