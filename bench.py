@@ -436,7 +436,16 @@ def main():
         phases = {nm: buf[i] / nst / 1e3 for i, nm in enumerate(names)}
         for i, nm in ((6, "p2_totals"), (7, "p2_rows"), (8, "p2_cols"), (9, "p2_rest"), (10, "p2_norms")):
             phases[nm + "_cum"] = buf[i] / nst / 1e3
-        per = np.array(buf[16:]).reshape(-1, 16)
+        per = np.array(buf[16:16 + 32 * geometry["fit_ctas"]]).reshape(-1, 32)
+        tl = np.array(buf[16 + 32 * geometry["fit_ctas"]:]).reshape(16, 32)
+        if tl.any():   # K1 v2 event timeline of CTA 0, last step (us from its first event)
+            t0 = tl[tl > 0].min()
+            evn = ["ld_issue_start", "ld_issue_end", "ld_scatter_start", "-", "mma_gemm1", "mma_gemm23",
+                   "ew_eta_ready", "ew_computed", "ew_p_free", "ew_p_full", "-", "unit_start",
+                   "ew_drained", "-", "-", "mma_gemm1_committed"]
+            phases["k1_timeline_cta0_us"] = {
+                evn[e]: [round((v - t0) / 1e3, 2) if v > 0 else None for v in tl[e][:8]]
+                for e in range(16) if tl[e].any()}
         st_ = per[:, :5]
         oc = per[:, 5:7] / nst    # objective sub-phase clocks per step
         phases["objective_subphases_us(mean over CTAs)"] = {
@@ -446,6 +455,13 @@ def main():
         if kc.any():
             names_k = ["col_operands", "staging_wait", "y_a1_gemm1", "d2_readout_b3", "barrier",
                        "next_stage_rowside", "elementwise_gemm23", "drain_d3"]
+            if int(fit.lib.gmf_k1_version(fit.h)) == 2:   # warp-specialized K1 (gmf_tc2.cuh)
+                kc = per[:, 8:24] / nst
+                names_k = ["ew_unit_prologue", "ew_wait_eta", "-", "ew_wait_y",
+                           "ew_elementwise", "ew_wait_p_free", "ew_d2_readout_p_store",
+                           "ew_unit_drain", "mma_wait_operands", "mma_wait_eta_free", "mma_issue",
+                           "mma_wait_p_full", "ld_staging_issue", "ld_wait_staged",
+                           "ld_wait_y_free", "ld_scatter"]
             phases["k1_subphases_us(mean over CTAs)"] = {
                 nm: float(kc[:, i].mean() / 1965.0) for i, nm in enumerate(names_k)}
         t0 = st_[:, 0].min()

@@ -127,8 +127,14 @@ typedef struct gmf_desc {
   int32_t world_size;   /* ranks sharing every row block (1 = single GPU)      */
   int32_t rank;
   int32_t device;       /* CUDA device ordinal                                 */
-  int32_t reserved;
+  int32_t flags;        /* GMF_DESC_* bits                                     */
 } gmf_desc;
+
+/* gmf_desc.flags: theta_row, x, offset, csr_col and csr_val may be read up to
+   16 bytes past their end (the warp-specialized tensor-core K1 stages row
+   ranges with TMA bulk copies of their 16-byte aligned superset; without
+   the flag the handle uses the older tensor-core K1) */
+#define GMF_DESC_TAIL_PADDED 1
 
 typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py:193-226) */
   double rate_k0, rate_k1, rate_tau;
@@ -263,6 +269,10 @@ int gmf_run_stream(gmf_handle* h, int64_t n_steps, void* host_status, void* stre
 int gmf_stream_signal(gmf_handle* h, int64_t value, void* stream);
 /* K1 implementation the handle runs (GMF_K1_CUDA_CORES or GMF_K1_TENSOR) */
 int gmf_k1_impl(gmf_handle* h);
+/* K1 kernel generation the handle runs: 0 CUDA cores, 1 tensor cores (one
+   32-row chunk per step of a 256-thread CTA), 2 tensor cores, warp-specialized
+   tcgen05 pipeline (one 384-thread CTA per SM; the default when eligible) */
+int gmf_k1_version(gmf_handle* h);
 /* number of kernels this handle has launched so far (graph nodes counted) */
 int64_t gmf_launch_count(gmf_handle* h);
 int gmf_profile(gmf_handle* h, int enable, double* out, void* stream);

@@ -47,7 +47,11 @@ class GmfDesc(C.Structure):
                 ("d", C.c_int32), ("dtype", C.c_int32), ("family", C.c_int32),
                 ("link", C.c_int32), ("y_format", C.c_int32), ("has_offset", C.c_int32),
                 ("has_weights", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
-                ("device", C.c_int32), ("reserved", C.c_int32)]
+                ("device", C.c_int32), ("flags", C.c_int32)]
+
+
+# gmf_desc.flags bit: row and CSR buffers readable 16 bytes past their end
+DESC_TAIL_PADDED = 1
 
 
 class GmfConfig(C.Structure):
@@ -110,6 +114,7 @@ SIGNATURES = {
     "gmf_profile_len": (_i64, [_P]),
     "gmf_geometry": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "gmf_k1_impl": (C.c_int, [_P]),
+    "gmf_k1_version": (C.c_int, [_P]),
     "gmf_stream_ready_ptr": (_P, [_P]),
     "gmf_run_stream": (C.c_int, [_P, _i64, _P, _P]),
     "gmf_stream_signal": (C.c_int, [_P, _i64, _P]),

@@ -14,18 +14,22 @@
 namespace gmf {
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha);
-int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
-                 int fit_extra_smem, int* fit_blocks_per_sm);
+int prepare_grad(const Params& P, int dtype, int NK, int fit_extra_smem, int* fit_blocks_per_sm);
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
-int64_t colimg_bytes_total(int NK, int CT);
+int64_t colimg_bytes_total(int NK, int CT, int tcm);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
 int launch_eval_pack(const Params& P, int4* out, cudaStream_t st);
 int launch_cache_fill(const Params& P, int dtype, cudaStream_t st);
 int launch_tile_index(const Params& P, int32_t* tidx, unsigned int* unsorted, cudaStream_t st);
+int launch_tcsr(const Params& P, const int32_t* tidx, int32_t* lens, int64_t* tptr, int32_t* tent,
+                unsigned int* too_big, cudaStream_t st);
 int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
-int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm);
+int set_mbar_sleep(int on);
+int64_t rimg_bytes_of(int NK);
+int set_k1_dbg(int v);
+int64_t grad_smem_bytes(const Params& P, int dtype, int NK);
 int launch_obj(const Params& P, int dtype, cudaStream_t st);
 int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t st);
 int launch_blocknorm(const Params& P, int dtype, cudaStream_t st);
@@ -58,6 +62,7 @@ struct gmf_handle {
   int fit_grid = 0;             // co-resident CTAs of the persistent kernel
   int fit_rs = 0;               // its row splits (fit_grid / CT)
   void* prof_buf = nullptr;
+  void* tcsr_buf = nullptr;     // K1 v2 tile-CSR (tptr | tent)
   std::vector<int64_t> rbp_host, cbp_host;
   bool reset_done = false;
   int64_t launches = 0;         // kernels this handle launched (gmf_launch_count)
@@ -210,15 +215,75 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     return GMF_ERR_UNSUPPORTED;
   }
   P.tcm = tc_ok && cfg->k1_impl != GMF_K1_CUDA_CORES;
+  int n_sm = kSMs;
+  GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
+  int smem_optin = 0;
+  GMF_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device));
+  if (getenv("GMF_MBAR_SLEEP")) set_mbar_sleep(atoi(getenv("GMF_MBAR_SLEEP")));
+  if (getenv("GMF_K1_DBG")) set_k1_dbg(atoi(getenv("GMF_K1_DBG")));
+  // K1 generation on the tensor cores: v2 (warp-specialized, one CTA per SM)
+  // pays off once its units are deep pipelines (>= 8 chunks of 64 rows, e.g.
+  // BASELINE c5's 65,536-row blocks); shallow units (c3, c4: 135-270 rows per
+  // unit) keep v1's two 256-thread CTAs per SM.  GMF_TC_VERSION=1|2 forces one.
+  bool want_v2 = false;
+  {
+    const char* fv = getenv("GMF_TC_VERSION");
+    const int64_t ct2 = (jmax + 127) / 128;
+    int a = (int)ct2, b = n_sm;
+    while (b) { const int t = a % b; a = b; b = t; }
+    int64_t rs2 = n_sm / (a > 0 ? a : 1);
+    if (rs2 > (nstar_max + 31) / 32) rs2 = (nstar_max + 31) / 32;
+    if (rs2 < 1) rs2 = 1;
+    want_v2 = nstar_max / rs2 >= 512;
+    if (fv) want_v2 = atoi(fv) == 2;
+    if (getenv("GMF_TC_V1")) want_v2 = false;
+  }
+  if (P.tcm && (desc->flags & GMF_DESC_TAIL_PADDED) && want_v2) {
+    // K1 v2 (warp-specialized pipeline, gmf_tc2.cuh): the offset rides in
+    // GEMM1 as feature KA and two sentinel features follow it, so the feature
+    // bucket must hold KA + has_off + 2; the staging ring shrinks until the
+    // tile fits in shared memory
+    const int nk2 = grad_bucket(KA + (P.has_off ? 1 : 0) + 2);   // + the two sentinel features
+    if (nk2 > 0 && nk2 <= 32) {
+      Params Q = P;
+      Q.tcm = 2;
+      const int64_t lim = smem_optin - 2048;   // the fit kernel's static shared memory
+      // prefer two A1 buffers, then the largest staging ring that fits
+      for (int na1 = 2; na1 >= 1 && Q.tcm == 2 && P.tcm != 2; --na1) {
+        Q.k1_na1 = na1;
+        for (Q.k1_cap = 2048; Q.k1_cap >= 512; Q.k1_cap /= 2) {
+          if (grad_smem_bytes(Q, desc->dtype, nk2) <= lim) {
+            P.tcm = 2;
+            P.k1_cap = Q.k1_cap;
+            P.k1_na1 = na1;
+            h->NK = nk2;
+            break;
+          }
+        }
+      }
+    }
+  }
 
   const int TC = tile_cols(desc->dtype, h->NK);
   P.TC = TC;
   P.CT = (int)((jmax + TC - 1) / TC);
-  const int64_t nchunks = (nstar_max + TR - 1) / TR;
-  int64_t RS = (2 * kSMs + P.CT - 1) / P.CT;
-  if (RS > nchunks) RS = nchunks;
-  if (RS < 1) RS = 1;
-  P.RS = (int)RS;
+  if (P.tcm == 2) {
+    // units = CT x RS spread over one CTA per SM: RS = SMs / gcd(CT, SMs) makes
+    // the unit count a multiple of the SM count; at least 32 rows per unit
+    int a = P.CT, b = n_sm;
+    while (b) { const int t = a % b; a = b; b = t; }
+    int64_t RS = n_sm / (a > 0 ? a : 1);
+    const int64_t rmax = (nstar_max + 31) / 32;
+    if (RS > rmax) RS = rmax;
+    if (RS < 1) RS = 1;
+    P.RS = (int)RS;
+  } else {
+    const int64_t nchunks = (nstar_max + TR - 1) / TR;
+    int64_t RS = (2 * kSMs + P.CT - 1) / P.CT;
+    if (RS > nchunks) RS = nchunks;
+    if (RS < 1) RS = 1;
+    P.RS = (int)RS;
+  }
   P.nstar_max = nstar_max;
   P.jmax = jmax;
   int64_t nrc = (nstar_max * Kr + kThreads - 1) / kThreads;
@@ -230,9 +295,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
 
   // persistent kernel geometry: every co-resident CTA, a multiple of CT
   int fit_bps = 0;
-  int smem_optin = 0;
-  GMF_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device));
-  const int64_t k1_smem = grad_smem_bytes(desc->dtype, h->NK, P.has_w, Kr, Kc, P.tcm);
+  const int64_t k1_smem = grad_smem_bytes(P, desc->dtype, h->NK);
   if (k1_smem > smem_optin) {
     set_error("the K1 tile for p+q+d = %d (%s%s) needs %lld B of shared memory, the device "
               "allows %d", KA, desc->dtype == GMF_F64 ? "fp64" : "fp32",
@@ -240,36 +303,37 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }
-  rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, 0, &fit_bps);
+  rc = prepare_grad(P, desc->dtype, h->NK, 0, &fit_bps);
   if (rc) { delete h; return rc; }
+  // fit grid: every co-resident CTA (v1 / CUDA cores: a multiple of CT, one
+  // (tile, row split) each; v2: one CTA per SM walking the units)
+  auto fit_grid_for = [&](int bps) {
+    if (P.tcm == 2) return bps >= 1 ? n_sm : 0;
+    return P.CT > 0 ? (bps * n_sm / P.CT) * P.CT : 0;
+  };
   {
     // cache each fit CTA's tracked entries in shared memory when that keeps
     // the same number of CTAs per SM
-    int n_sm0 = kSMs;
-    GMF_CUDA(cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, desc->device));
-    const int grid0 = P.CT > 0 ? (fit_bps * n_sm0 / P.CT) * P.CT : 0;   // = fit_grid below
+    const int grid0 = fit_grid_for(fit_bps);
     const int64_t cap = grid0 > 0 ? (bufs->n_eval + grid0 - 1) / grid0 : 0;
-    if (cap > 0 && cap <= 1024 && k1_smem + cap * 16 <= smem_optin) {
+    if (cap > 0 && cap <= 1024 && k1_smem + cap * 16 + (P.tcm == 2 ? 2048 : 0) <= smem_optin) {
       int bps2 = 0;
-      rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm,
-                        (int)(cap * 16), &bps2);
+      rc = prepare_grad(P, desc->dtype, h->NK, (int)(cap * 16), &bps2);
       if (rc) { delete h; return rc; }
       if (bps2 == fit_bps) {
         P.ep_cap = (int)cap;
-        P.ep_soff = grad_smem_bytes(desc->dtype, h->NK, P.has_w, Kr, Kc, P.tcm);
+        P.ep_soff = grad_smem_bytes(P, desc->dtype, h->NK);
       } else {
-        rc = prepare_grad(desc->dtype, desc->family, h->NK, P.has_w, Kr, Kc, P.tcm, 0, &bps2);
+        rc = prepare_grad(P, desc->dtype, h->NK, 0, &bps2);
         if (rc) { delete h; return rc; }
       }
     }
   }
-  int n_sm = kSMs;
-  GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
   int coop = 0;
   GMF_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc->device));
-  h->fit_grid = coop ? (fit_bps * n_sm / P.CT) * P.CT : 0;
+  h->fit_grid = coop ? fit_grid_for(fit_bps) : 0;
   if (getenv("GMF_NO_PERSISTENT")) h->fit_grid = 0;   // diagnostics: per-step kernels only
-  h->fit_rs = h->fit_grid / (P.CT > 0 ? P.CT : 1);
+  h->fit_rs = P.tcm == 2 ? P.RS : h->fit_grid / (P.CT > 0 ? P.CT : 1);
 
   // ---- workspace carve-up ----
   const int64_t max_epochs = cfg->max_epochs;
@@ -318,7 +382,11 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const bool want_tidx = desc->y_format != GMF_Y_DENSE_I32 && col_identity && desc->n > 0;
   const int64_t o_tidx = take(want_tidx ? desc->n * (P.CT + 1) * 4 + 16 : 16);
   const bool want_img = P.tcm && col_identity;
-  const int64_t o_cimg = take(want_img ? colimg_bytes_total(h->NK, P.CT) : 16);
+  // K1 v2 operand-row images: every chunk of every row split of the largest block
+  const int64_t rimg_nch = (nstar_max / (P.RS > 0 ? P.RS : 1) + 2 + 63) / 64;
+  const int64_t o_rimg = take(P.tcm == 2 ? (int64_t)P.RS * rimg_nch * rimg_bytes_of(h->NK) : 16);
+  const int64_t o_rflag = take(P.tcm == 2 ? (int64_t)P.RS * rimg_nch * 4 + 16 : 16);
+  const int64_t o_cimg = take(want_img ? colimg_bytes_total(h->NK, P.CT, P.tcm) : 16);
   cudaError_t e = cudaMalloc(&h->ws, off);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc workspace"); }
   char* base = (char*)h->ws;
@@ -352,6 +420,10 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.vpad = base + o_vpad;
   P.nkb = h->NK;
   P.colimg = want_img ? (void*)(base + o_cimg) : nullptr;
+  P.rimg = base + o_rimg;
+  P.rimg_flag = (unsigned int*)(base + o_rflag);
+  P.rimg_epoch = (unsigned int*)(base + o_rflag + (P.tcm == 2 ? (int64_t)P.RS * rimg_nch * 4 : 0));
+  P.rimg_nch = (int)rimg_nch;
   if (bufs->n_eval > 0) {
     // the tracked sample sorted by (block-major) row; each tracked row owns a
     // cache slot that phase 2 writes with the row (the objective is an
@@ -396,6 +468,30 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     GMF_CUDA(cudaMemcpy(&unsorted, flag, 4, cudaMemcpyDeviceToHost));
     if (!unsorted) P.tidx = ti;   // columns not increasing in some row: full-row scans
   }
+  P.tptr = nullptr;
+  P.tent = nullptr;
+  if (P.tcm == 2 && P.tidx) {
+    // K1 v2 reads CSR through a tile-major copy whose entries carry their row
+    const int64_t nnz = P.nnz;
+    const int64_t tp_bytes = align256((int64_t)P.CT * (desc->n + 1) * 8);
+    const int64_t te_bytes = align256((2 * nnz + 8) * 4);
+    const int64_t ln_bytes = align256((int64_t)P.CT * desc->n * 4 + 16);
+    cudaError_t e2 = cudaMalloc(&h->tcsr_buf, tp_bytes + te_bytes + ln_bytes);
+    if (e2 != cudaSuccess) { gmf_destroy(h); return cuda_fail(e2, "cudaMalloc tile-CSR"); }
+    char* tb = (char*)h->tcsr_buf;
+    unsigned int* too_big = (unsigned int*)(tb + tp_bytes + te_bytes + ln_bytes - 16);
+    GMF_CUDA(cudaMemset(tb + tp_bytes, 0, te_bytes));
+    GMF_CUDA(cudaMemset(too_big, 0, 4));
+    rc = launch_tcsr(P, P.tidx, (int32_t*)(tb + tp_bytes + te_bytes), (int64_t*)tb,
+                     (int32_t*)(tb + tp_bytes), too_big, 0);
+    if (rc) { gmf_destroy(h); return rc; }
+    unsigned int big = 0;
+    GMF_CUDA(cudaMemcpy(&big, too_big, 4, cudaMemcpyDeviceToHost));
+    if (!big) {   // counts >= 2^23 do not fit an entry word: row-walking scatter instead
+      P.tptr = (const int64_t*)tb;
+      P.tent = (const int32_t*)(tb + tp_bytes);
+    }
+  }
   P.ep = (const int4*)(base + o_ep);
   if (bufs->n_eval > 0) {   // tracked sample packed with its Y, once per fit
     rc = launch_eval_pack(P, (int4*)(base + o_ep), 0);
@@ -432,6 +528,7 @@ int gmf_destroy(gmf_handle* h) {
   if (h->internal) cudaStreamSynchronize(h->internal);
   if (h->ws) cudaFree(h->ws);
   if (h->prof_buf) cudaFree(h->prof_buf);
+  if (h->tcsr_buf) cudaFree(h->tcsr_buf);
   if (h->host_ctrl) cudaFreeHost(h->host_ctrl);
   if (h->host_abort) cudaFreeHost(h->host_abort);
   if (h->ready_vals) cudaFreeHost(h->ready_vals);
@@ -473,7 +570,7 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
   if (rc) return rc;
   h->launches += 2;
   GMF_CUDA(cudaStreamSynchronize(st));
-  if (P.tcm && h->fit_grid > 0 && !h->residency_checked) {
+  if (P.tcm == 1 && h->fit_grid > 0 && !h->residency_checked) {
     // the tensor-core fit kernel synchronises with a software grid barrier:
     // probe once that all its CTAs are co-resident, else one CTA per SM
     rc = residency_probe(h, st);
@@ -609,7 +706,7 @@ int gmf_snapshot_blocks(gmf_handle* h, int64_t* ver, int64_t* period, void* stre
   return GMF_OK;
 }
 
-int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 16 * (int64_t)h->fit_grid : 0; }
+int64_t gmf_profile_len(gmf_handle* h) { return h ? 16 + 32 * (int64_t)h->fit_grid + 512 : 0; }
 
 int gmf_geometry(gmf_handle* h, int64_t* out8) {
   if (!h || !out8) { set_error("null handle/out"); return GMF_ERR_STATE; }
@@ -619,7 +716,7 @@ int gmf_geometry(gmf_handle* h, int64_t* out8) {
   out8[3] = h->P.TC;
   out8[4] = h->P.RS;
   out8[5] = h->NK;
-  out8[6] = grad_smem_bytes(h->desc.dtype, h->NK, h->P.has_w, h->P.Kr, h->P.Kc, h->P.tcm);
+  out8[6] = grad_smem_bytes(h->P, h->desc.dtype, h->NK);
   out8[7] = h->P.nstar_max;
   return GMF_OK;
 }
@@ -776,6 +873,8 @@ int gmf_stream_signal(gmf_handle* h, int64_t value, void* stream) {
 }
 
 int gmf_k1_impl(gmf_handle* h) { return h ? (h->P.tcm ? GMF_K1_TENSOR : GMF_K1_CUDA_CORES) : -1; }
+
+int gmf_k1_version(gmf_handle* h) { return h ? h->P.tcm : -1; }
 
 int64_t gmf_launch_count(gmf_handle* h) { return h ? h->launches : -1; }
 

@@ -79,7 +79,13 @@ struct Params {
   double lam_b, lam_g, lam_u, lam_v;
   double nbfloor, nbceil, escale, phi;
   int est_alpha, snap_stride, world;
-  int tcm;             // K1 on the tensor cores (gmf_tc.cuh)
+  int tcm;             // K1 on the tensor cores: 1 gmf_tc.cuh, 2 gmf_tc2.cuh (warp-specialized)
+  int k1_cap;          // K1 v2: tile-CSR entries staged per chunk slot
+  int k1_na1;          // K1 v2: A1 operand buffers (1 or 2)
+  void* rimg;                // K1 v2 operand-row images [RS][rimg_nch][tc2::rimg_bytes]
+  unsigned int* rimg_flag;   // [RS][rimg_nch] epoch of the last build of each image
+  unsigned int* rimg_epoch;  // builds epoch (one per step; device counter)
+  int rimg_nch;              // 64-row chunks per row split (max over blocks)
   int ep_cap;          // tracked entries cached per fit CTA in shared memory (0 = none)
   int64_t ep_soff;     // their shared-memory offset (bytes, after K1's region)
   // tracked-objective caches of the persistent kernel (entries sorted by row):
@@ -94,6 +100,8 @@ struct Params {
   // kernel runs; the copy stream then sets *ready = t + 1, which K1 waits for;
   // each step's status word is written to mapped pinned host memory
   int stream_mode;
+  const int64_t* tptr;     // tile-CSR (K1 v2): [CT][n+1] start of tile ct's entries of row i
+  const int32_t* tent;     // tile-CSR entries, int32 pairs (row, count << 8 | tile column)
   const int32_t* tidx;     // [n][CT+1] per-row start of each column tile's nonzeros (CSR,
                            // J = all columns, rows sorted by column), else null
   // tensor-core K1 column operands (R | B1h | B1l per column tile, bf16, in the
@@ -192,7 +200,7 @@ GMF_D double block_sum_all(double v, double* scr) {
 // block-wide sums of N values at once (blocks of kThreads), broadcast to every thread; xor
 // butterflies give bitwise-identical lane results (a+b == b+a), then a fixed
 // warp order (scr >= N * warps doubles)
-template <int N>
+template <int N, int NT = kThreads>
 GMF_D void block_sum_vec(double (&v)[N], double* scr) {
   #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -211,7 +219,7 @@ GMF_D void block_sum_vec(double (&v)[N], double* scr) {
   #pragma unroll
   for (int i = 0; i < N; ++i) s[i] = 0.0;
   #pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) {
+  for (int w = 0; w < NT / 32; ++w) {
     #pragma unroll
     for (int i = 0; i < N; ++i) s[i] += scr[w * N + i];
   }

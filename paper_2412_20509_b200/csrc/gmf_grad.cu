@@ -14,7 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "gmf_tc.cuh"
+#include "gmf_tc2.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -27,6 +27,9 @@ namespace gmf {
 template <typename T, int NK> struct MinBlocks {
   static constexpr int v = (sizeof(T) == 8 || NK > 32) ? 1 : 2;
 };
+
+// threads per CTA of the fit kernel: 384 for the warp-specialized K1 v2
+template <int TCM> struct FitNT { static constexpr int v = TCM == 2 ? tc2::NT : kThreads; };
 
 template <typename T, int FAM, int NK, bool TCM>
 __global__ void __launch_bounds__(kThreads, MinBlocks<T, NK>::v)
@@ -69,6 +72,47 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
       P.rec[R_NBNUM] = sn;
       P.rec[R_NBDEN] = sd;
       P.tickets[P.CT] = 0u;
+    }
+  }
+}
+
+// K1 v2 (warp-specialized tensor-core pipeline, gmf_tc2.cuh) for one step:
+// one CTA per SM walks the (column tile, row split) units; the last CTA sums
+// the per-CTA NB moment partials in fixed order
+template <int FAM, int NK>
+__global__ void __launch_bounds__(tc2::NT, 1)
+k_grad2(Params P, long long xb, long long xs, double xalpha) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double scr[tc2::NT / 32];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) tc2::Bars s_bars;
+  const Ctrl* C = P.ctrl;
+  long long blk, s;
+  double alpha;
+  if (xb >= 0) {
+    blk = xb; s = xs; alpha = xalpha;
+  } else {
+    const long long t = C->t;
+    if (C->stopped || t >= P.max_steps) return;   // uniform across the grid
+    blk = P.bseq[t];
+    s = t % P.S;
+    alpha = C->nb_shape;
+  }
+  tc2::Ctx X;
+  tc2::ctx_open(X, &s_tmem, &s_bars);
+  const unsigned int epoch = *P.rimg_epoch + 1u;   // one image build per launch
+  tc2::build_images<NK>(P, blk, P.RS, epoch);
+  tc2::grad_units<FAM, NK>(P, blk, s, alpha, P.RS, smem, X, epoch);
+  tc2::ctx_close(X);
+  const unsigned int total = gridDim.x;
+  if (last_block_ticket(P.tickets + P.CT, total)) {
+    const double sn = sum_parts<tc2::NT>(P.nbpart, total, 2, scr);
+    const double sd = sum_parts<tc2::NT>(P.nbpart + 1, total, 2, scr);
+    if (threadIdx.x == 0) {
+      P.rec[R_NBNUM] = sn;
+      P.rec[R_NBDEN] = sd;
+      P.tickets[P.CT] = 0u;
+      *P.rimg_epoch = epoch;   // every CTA has read the old value (ticket)
     }
   }
 }
@@ -158,13 +202,13 @@ struct Vec16;   // 16-byte vector of T
 template <> struct Vec16<float> { using V = float4; static constexpr int N = 4; };
 template <> struct Vec16<double> { using V = double2; static constexpr int N = 2; };
 
-template <typename T, int NK>
+template <typename T, int NK, int NT = kThreads>
 GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, int64_t lo,
                              int64_t hi) {
   using V = typename Vec16<T>::V;
   constexpr int VN = Vec16<T>::N;
   double s = 0.0;
-  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+  for (int64_t e = lo + threadIdx.x; e < hi; e += NT) {
     const int4 en = ents[e - lo];
     const int64_t i = en.x, j = en.y;
     const V* a = reinterpret_cast<const V*>(tptr<T>(P.ecache) + (int64_t)en.w * (NK + 4));
@@ -316,18 +360,21 @@ GMF_D T warp_sum(T v) {
   return v;
 }
 
-template <typename T, int FAM, int NK, bool TCM>
-__global__ void __launch_bounds__(kThreads, MinBlocks<T, NK>::v)
+template <typename T, int FAM, int NK, int TCM>
+__global__ void __launch_bounds__(FitNT<TCM>::v, TCM == 2 ? 1 : MinBlocks<T, NK>::v)
 k_fit(Params P, long long n_steps) {
+  constexpr int NT = FitNT<TCM>::v;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double scr[8 * (kThreads / 32)];
+  __shared__ double scr[8 * (NT / 32)];
   __shared__ double s_tot[8];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) tc2::Bars s_bars;
   constexpr int TC = TileK<T, NK>::TC;
   Ctrl C = *P.ctrl;
   if (C.stopped) return;
   tc::Ctx tcx;
+  tc2::Ctx tcx2;
   const int G = gridDim.x;
   unsigned int bgen = 0;   // software barriers passed by this CTA (P.gbar zeroed per launch)
   auto gsync = [&](unsigned long long timeout) -> bool {
@@ -339,16 +386,34 @@ k_fit(Params P, long long n_steps) {
       return true;
     }
   };
-  if constexpr (TCM) {
+  if constexpr (TCM == 1) {
     tc::ctx_open(tcx, &s_tmem, s_bar);
-    if (!gsync(kProbeTimeoutNs)) {   // not every CTA resident: abort, host falls back
+    // residency probe: a CTA that timed out raised the abort flag before the
+    // last arrival could open the barrier, or after it -- every CTA re-reads
+    // the flag once the barrier opened, so the launch aborts as a whole
+    bool resident = gsync(kProbeTimeoutNs);
+    if (resident) {
+      __shared__ int s_abort;
+      if (threadIdx.x == 0) s_abort = (int)ld_acquire_u32(P.gbar + 2);
+      __syncthreads();
+      resident = s_abort == 0;
+    }
+    if (!resident) {   // not every CTA resident: abort, host falls back to one CTA per SM
       tc::ctx_close(tcx);
       return;
     }
+  } else if constexpr (TCM == 2) {
+    tc2::ctx_open(tcx2, &s_tmem, &s_bars);   // cooperative launch: co-resident by construction
   }
-  const int ct = blockIdx.x % P.CT, rs = blockIdx.x / P.CT, RS = G / P.CT;
-  const int64_t gstride = (int64_t)G * kThreads;
-  const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  // K1 v2 operand-row images: one build epoch per step (every CTA reads the
+  // counter before the first grid barrier, CTA 0 advances it at the end)
+  const unsigned int epoch0 = TCM == 2 ? *P.rimg_epoch : 0u;
+  unsigned int epoch_n = epoch0;
+  // K1 v1 / CUDA cores: one (column tile, row split) per CTA; v2: units looped
+  const int ct = blockIdx.x % P.CT, rs = blockIdx.x / P.CT;
+  const int RS = TCM == 2 ? P.RS : G / P.CT;
+  const int64_t gstride = (int64_t)G * NT;
+  const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t gw = gtid >> 5, nw = gstride >> 5;
   const int Kr = P.Kr, Kc = P.Kc, kk = 2 * Kc;
@@ -362,7 +427,7 @@ k_fit(Params P, long long n_steps) {
       const double x = (double)tc[e];
       v[(int)(e % Kc) < P.p ? 0 : 1] += x * x;
     }
-    block_sum_vec<2>(v, scr);
+    block_sum_vec<2, NT>(v, scr);
     if (threadIdx.x == 0) { P.cnpart[2 * blockIdx.x] = v[0]; P.cnpart[2 * blockIdx.x + 1] = v[1]; }
   }
 
@@ -373,7 +438,7 @@ k_fit(Params P, long long n_steps) {
     int4* ep_s = reinterpret_cast<int4*>(smem + P.ep_soff);
     const int64_t per = (P.E + G - 1) / G;
     const int64_t lo = per * blockIdx.x, hi = lo + per < P.E ? lo + per : P.E;
-    for (int64_t e = threadIdx.x; e < hi - lo; e += kThreads) ep_s[e] = P.ep[lo + e];
+    for (int64_t e = threadIdx.x; e < hi - lo; e += NT) ep_s[e] = P.ep[lo + e];
     __syncthreads();
     ep_src = ep_s;
   }
@@ -393,11 +458,17 @@ k_fit(Params P, long long n_steps) {
       else if (k < P.KA) v = zg[j * P.q + (k - Kc)];
       tptr<T>(P.vpad)[e] = v;
     }
-    if constexpr (TCM) {
+    if constexpr (TCM == 1) {
       if (P.colimg_on) {   // K1's column-operand images, one task per thread
         const int nt = tc::colimg_tasks<NK>();
         for (int64_t e = gtid; e < (int64_t)P.CT * nt; e += gstride)
           tc::colimg_task<NK>(P, (int)(e / nt), (int)(e % nt));
+      }
+    } else if constexpr (TCM == 2) {
+      if (P.colimg_on) {
+        const int nt = tc2::colimg_tasks<NK>();
+        for (int64_t e = gtid; e < (int64_t)P.CT * nt; e += gstride)
+          tc2::colimg_task<NK>(P, (int)(e / nt), (int)(e % nt));
       }
     }
     if (!gsync(kBarrierTimeoutNs)) n_steps = 0;   // vpad / images complete before the first step
@@ -408,7 +479,7 @@ k_fit(Params P, long long n_steps) {
   unsigned long long t_a = prof ? gtimer() : 0, t_b;
   for (long long it = 0; it < n_steps; ++it) {
     const long long t = C.t;
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 0] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 0] = gtimer(); }
     const long long sidx = mod_nn(t, P.S);
     const bool boundary = sidx == 0;
     const bool run_grad = t < P.max_steps;
@@ -418,28 +489,31 @@ k_fit(Params P, long long n_steps) {
     // ------------------------- phase 1 -------------------------
     if (blockIdx.x == 0 && prev_blk >= 0) {   // row norms of the block updated last step
       double v[2] = {0.0, 0.0};
-      for (int i = threadIdx.x; i < G; i += kThreads) {
+      for (int i = threadIdx.x; i < G; i += NT) {
         v[0] += __ldcg(P.rnpart + 2 * i);
         v[1] += __ldcg(P.rnpart + 2 * i + 1);
       }
-      block_sum_vec<2>(v, scr);
+      block_sum_vec<2, NT>(v, scr);
       if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
     }
     if (boundary) {
       // contiguous, equal entry ranges per CTA keep the objective balanced
       double v[1] = {0.0};
       const long long c0 = profc ? clock64() : 0;
-      v[0] = obj_dev_partial<T, NK>(P, C.nb_shape, ep_src + (ep_cached ? 0 : e_lo), e_lo, e_hi);
+      v[0] = obj_dev_partial<T, NK, NT>(P, C.nb_shape, ep_src + (ep_cached ? 0 : e_lo), e_lo, e_hi);
       const long long c1 = profc ? clock64() : 0;
-      block_sum_vec<1>(v, scr);
+      block_sum_vec<1, NT>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
       if (profc && threadIdx.x == 0) {   // objective sub-phases (SM clocks): loop, reduction
-        atomicAdd(P.prof + 16 + 16 * blockIdx.x + 5, (unsigned long long)(c1 - c0));
-        atomicAdd(P.prof + 16 + 16 * blockIdx.x + 6, (unsigned long long)(clock64() - c1));
+        atomicAdd(P.prof + 16 + 32 * blockIdx.x + 5, (unsigned long long)(c1 - c0));
+        atomicAdd(P.prof + 16 + 32 * blockIdx.x + 6, (unsigned long long)(clock64() - c1));
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 0, t_b - t_a); t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 1] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 1] = gtimer(); }
+    if constexpr (TCM == 2) {   // this step's operand-row images (before the objective: overlap)
+      if (run_grad && !P.stream_mode) tc2::build_images<NK>(P, blk, RS, ++epoch_n);
+    }
     if (P.stream_mode && run_grad) {
       // streaming: this step's row block is being uploaded; wait for its flag
       // (read at the start of the step, so a block that arrived long ago
@@ -456,14 +530,20 @@ k_fit(Params P, long long n_steps) {
       }
       __syncthreads();
     }
-    if (run_grad && rs < RS) {
-      if constexpr (TCM)
+    if constexpr (TCM == 2) {
+      if (run_grad) {
+        if (P.stream_mode) tc2::build_images<NK>(P, blk, RS, ++epoch_n);   // after the block arrived
+        tc2::grad_units<FAM, NK>(P, blk, sidx, C.nb_shape, RS, smem, tcx2, epoch_n,
+                                 profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
+      }
+    } else if (run_grad && rs < RS) {
+      if constexpr (TCM == 1)
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
-                              profc ? P.prof + 16 + 16 * blockIdx.x + 8 : nullptr);
+                              profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
       else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 2] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 2] = gtimer(); }
     // Phase-2 inputs that phase 1 does not write are read across the barrier
     // so their latency hides behind it: this thread's first two row
     // coordinates (theta, EMA state) and the block's snapshot version.  The
@@ -477,11 +557,11 @@ k_fit(Params P, long long n_steps) {
       {   // two slots per thread per pass, every load of a pass in flight together
         const bool tb = boundary, tn = run_grad && P.est_alpha;
         const int64_t nmax = (int64_t)G > P.R ? (int64_t)G : P.R;
-        for (int64_t i = threadIdx.x; i < nmax; i += 2 * kThreads) {
+        for (int64_t i = threadIdx.x; i < nmax; i += 2 * NT) {
           double l[2][7];
           #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int64_t ii = i + u * kThreads;
+            const int64_t ii = i + u * NT;
             const bool ig = ii < G, ir = ii < P.R;
             const int64_t ic = ig ? ii : 0, irc = ir ? ii : 0;
             const double o0 = __ldcg(P.objpart + OBJ_W * ic);
@@ -503,7 +583,7 @@ k_fit(Params P, long long n_steps) {
           }
         }
       }
-      block_sum_vec<7>(v7, scr);
+      block_sum_vec<7, NT>(v7, scr);
     };
     SoftArrival arr;
     if constexpr (TCM) {
@@ -548,7 +628,7 @@ k_fit(Params P, long long n_steps) {
     } else {
       if (!gsync(kBarrierTimeoutNs)) break;
     }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 3] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 3] = gtimer(); }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 2, t_b - t_a); t_a = t_b; }
     // ------------------------- phase 2 -------------------------
     // totals, redundantly in every CTA: deviance, ||B||^2, ||V||^2,
@@ -571,7 +651,7 @@ k_fit(Params P, long long n_steps) {
       phase2_totals(v7);
     }
     if (profc && threadIdx.x == 0)   // phase-2 totals (SM clocks)
-      atomicAdd(P.prof + 16 + 16 * blockIdx.x + 7, (unsigned long long)(clock64() - ct0));
+      atomicAdd(P.prof + 16 + 32 * blockIdx.x + 7, (unsigned long long)(clock64() - ct0));
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 6, t_b - t_a); }
     const Decision D = decide_from(P, C, v7[0], v7[3], v7[4], v7[1], v7[2]);
     const bool upd = !D.stop;
@@ -661,7 +741,7 @@ k_fit(Params P, long long n_steps) {
       const int64_t rstride = (int64_t)TC * kk;
       int CG = 1;
       while (2 * CG * kk <= 64 && 2 * CG <= TC) CG *= 2;   // divides TC (a power of two)
-      const int EQ = CG * kk, S = kThreads / EQ;
+      const int EQ = CG * kk, S = NT / EQ;
       const int qv = threadIdx.x % EQ, sg = threadIdx.x / EQ;
       T* red = reinterpret_cast<T*>(smem);
       const int64_t ntask = (nJ + CG - 1) / CG;
@@ -700,8 +780,10 @@ k_fit(Params P, long long n_steps) {
                                         tptr<T>(P.hb_col) + j * Kc + k, g, h, s_col,
                                         k < P.p ? P.lam_b : P.lam_v, rho, at);
             tptr<T>(P.vpad)[j * NK + k] = nvv;   // the objective's padded copy of [b | v | z]
-            if constexpr (TCM) {
+            if constexpr (TCM == 1) {
               if (P.colimg_on) tc::colimg_write<NK>(P, j, k, (float)nvv);
+            } else if constexpr (TCM == 2) {
+              if (P.colimg_on) tc2::colimg_write<NK>(P, j, k, (float)nvv);
             }
             const double sq = (double)nvv * (double)nvv;
             if (k < P.p) nrm[2] += sq; else nrm[3] += sq;
@@ -724,7 +806,7 @@ k_fit(Params P, long long n_steps) {
       }
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 9, t_b - t_a); }
-    block_sum_vec<4>(nrm, scr);
+    block_sum_vec<4, NT>(nrm, scr);
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 10, t_b - t_a); }
     if (threadIdx.x == 0) {
       P.rnpart[2 * blockIdx.x] = nrm[0];
@@ -746,7 +828,7 @@ k_fit(Params P, long long n_steps) {
     C = N;
     prev_blk = upd ? blk : -1;
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 3, t_b - t_a); t_a = t_b; }
-    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 16 * blockIdx.x + 4] = gtimer(); }
+    if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 4] = gtimer(); }
     // per-step status word to pinned host memory, written after the barrier:
     // a system-memory store ahead of a barrier's gpu-scope fence would hold
     // that fence for a PCIe round trip
@@ -761,26 +843,33 @@ k_fit(Params P, long long n_steps) {
   }
   if (blockIdx.x == 0 && prev_blk >= 0) {
     double v[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < G; i += kThreads) {
+    for (int i = threadIdx.x; i < G; i += NT) {
       v[0] += __ldcg(P.rnpart + 2 * i);
       v[1] += __ldcg(P.rnpart + 2 * i + 1);
     }
-    block_sum_vec<2>(v, scr);
+    block_sum_vec<2, NT>(v, scr);
     if (threadIdx.x == 0) { P.blocksum[2 * prev_blk] = v[0]; P.blocksum[2 * prev_blk + 1] = v[1]; }
   }
-  if constexpr (TCM) tc::ctx_close(tcx);
+  if constexpr (TCM == 1) tc::ctx_close(tcx);
+  else if constexpr (TCM == 2) {
+    tc2::ctx_close(tcx2);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.rimg_epoch = epoch_n;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // host side: dispatch over (dtype, family, feature bucket)
 // ---------------------------------------------------------------------------
-template <typename T, int FAM, int NK, bool TCM>
+template <typename T, int FAM, int NK, int TCM>
 struct Inst {
-  static void* grad() { return (void*)k_grad<T, FAM, NK, TCM>; }
+  static void* grad() {
+    if constexpr (TCM == 2) return (void*)k_grad2<FAM, NK>;
+    else return (void*)k_grad<T, FAM, NK, TCM != 0>;
+  }
   static void* fit() { return (void*)k_fit<T, FAM, NK, TCM>; }
 };
 
-template <typename T, int FAM, bool TCM>
+template <typename T, int FAM, int TCM>
 static void* pick(int NK, bool fit) {
   switch (NK) {
     case 8: return fit ? Inst<T, FAM, 8, TCM>::fit() : Inst<T, FAM, 8, TCM>::grad();
@@ -790,7 +879,7 @@ static void* pick(int NK, bool fit) {
     case 32: return fit ? Inst<T, FAM, 32, TCM>::fit() : Inst<T, FAM, 32, TCM>::grad();
     case 64:   // K = p+q+d in (32, 64]: CUDA-core K1 only (c5's rank 50)
       if constexpr (!TCM)
-        return fit ? Inst<T, FAM, 64, false>::fit() : Inst<T, FAM, 64, false>::grad();
+        return fit ? Inst<T, FAM, 64, 0>::fit() : Inst<T, FAM, 64, 0>::grad();
       return nullptr;
     default: return nullptr;
   }
@@ -799,9 +888,24 @@ static void* pick(int NK, bool fit) {
 // tcm: K1 on the tensor cores (fp32 only; gmf_tc.cuh)
 static void* kernel_for(int dtype, int family, int NK, bool fit, int tcm) {
   const int fam = family == GMF_NEG_BINOMIAL ? 1 : 0;
-  if (dtype == GMF_F64) return fam ? pick<double, 1, false>(NK, fit) : pick<double, 0, false>(NK, fit);
-  if (tcm) return fam ? pick<float, 1, true>(NK, fit) : pick<float, 0, true>(NK, fit);
-  return fam ? pick<float, 1, false>(NK, fit) : pick<float, 0, false>(NK, fit);
+  if (dtype == GMF_F64) return fam ? pick<double, 1, 0>(NK, fit) : pick<double, 0, 0>(NK, fit);
+  if (tcm == 2) return fam ? pick<float, 1, 2>(NK, fit) : pick<float, 0, 2>(NK, fit);
+  if (tcm) return fam ? pick<float, 1, 1>(NK, fit) : pick<float, 0, 1>(NK, fit);
+  return fam ? pick<float, 1, 0>(NK, fit) : pick<float, 0, 0>(NK, fit);
+}
+
+static int k1_threads(int tcm) { return tcm == 2 ? tc2::NT : kThreads; }
+
+// experiment switch (GMF_MBAR_SLEEP=1): K1 v2 mbarrier waits with a suspend-time hint
+int set_mbar_sleep(int on) {
+  GMF_CUDA(cudaMemcpyToSymbol(tc2::g_mbar_sleep, &on, sizeof(int)));
+  return GMF_OK;
+}
+int64_t rimg_bytes_of(int NK) { return tc2::rimg_bytes(NK); }
+
+int set_k1_dbg(int v) {
+  GMF_CUDA(cudaMemcpyToSymbol(tc2::g_k1_dbg, &v, sizeof(int)));
+  return GMF_OK;
 }
 
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA) {
@@ -823,29 +927,36 @@ int tile_cols(int dtype, int NK) {
   return dtype == GMF_F64 ? Tile<double>::TC : Tile<float>::TC;
 }
 
-int64_t colimg_bytes_total(int NK, int CT) { return (int64_t)CT * tc::colimg_bytes(NK); }
+int64_t colimg_bytes_total(int NK, int CT, int tcm) {
+  return (int64_t)CT * (tcm == 2 ? tc2::colimg_bytes(NK) : tc::colimg_bytes(NK));
+}
 
-int64_t grad_smem_bytes(int dtype, int NK, int has_w, int Kr, int Kc, int tcm) {
-  if (tcm) return tc::smem_layout(NK).total;
-  return grad_smem(tile_cols(dtype, NK), NK, dtype == GMF_F64 ? 8 : 4, has_w, Kr, Kc).total;
+static int csr_kind(int yfmt) { return yfmt == GMF_Y_DENSE_I32 ? 0 : (yfmt == GMF_Y_CSR_PACK32 ? 2 : 1); }
+
+// dynamic shared memory of K1 (the fit kernel adds its cached tracked entries)
+int64_t grad_smem_bytes(const Params& P, int dtype, int NK) {
+  if (P.tcm == 2) return tc2::layout(NK, P.Kr, P.p, csr_kind(P.yfmt), P.k1_cap, P.k1_na1).total;
+  if (P.tcm) return tc::smem_layout(NK).total;
+  return grad_smem(tile_cols(dtype, NK), NK, dtype == GMF_F64 ? 8 : 4, P.has_w, P.Kr, P.Kc).total;
 }
 
 // opt in to >48 KB dynamic shared memory (outside any graph capture) and
 // report how many k_fit CTAs can be co-resident per SM
-int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int tcm,
-                 int fit_extra_smem, int* fit_blocks_per_sm) {
-  void* g = kernel_for(dtype, family, NK, false, tcm);
-  void* f = kernel_for(dtype, family, NK, true, tcm);
+int prepare_grad(const Params& P, int dtype, int NK, int fit_extra_smem, int* fit_blocks_per_sm) {
+  const int tcm = P.tcm;
+  void* g = kernel_for(dtype, P.fam, NK, false, tcm);
+  void* f = kernel_for(dtype, P.fam, NK, true, tcm);
   if (!g || !f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const int smem_g = (int)grad_smem_bytes(dtype, NK, has_w, Kr, Kc, tcm);
+  const int nt = k1_threads(tcm);
+  const int smem_g = (int)grad_smem_bytes(P, dtype, NK);
   const int smem = smem_g + fit_extra_smem;
   GMF_CUDA(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g));
   GMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nb = 0;
-  GMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem));
-  if (tcm) {
+  GMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, nt, smem));
+  if (tcm == 1) {
     // The occupancy calculator caps kernels that allocate tensor memory at one
-    // CTA per SM; each K1 CTA takes 256 of the 512 TMEM columns, so the SM
+    // CTA per SM; each K1 v1 CTA takes 256 of the 512 TMEM columns, so the SM
     // holds as many as registers and shared memory allow, up to two.
     cudaFuncAttributes a;
     GMF_CUDA(cudaFuncGetAttributes(&a, f));
@@ -865,11 +976,12 @@ int prepare_grad(int dtype, int family, int NK, int has_w, int Kr, int Kc, int t
       cudaFuncAttributes a;
       cudaFuncGetAttributes(&a, k);
       int n1 = 0, n2 = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k, kThreads, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k, kThreads, 0);
-      fprintf(stderr, "[gmf] %s kernel: regs %d static smem %zu dyn smem %d (max %d) local %zu maxthreads %d -> %d CTAs/SM (%d without dyn smem)\n",
-              k == f ? "fit" : "grad", a.numRegs, a.sharedSizeBytes, smem, a.maxDynamicSharedSizeBytes,
-              a.localSizeBytes, a.maxThreadsPerBlock, n1, n2);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k, nt, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, k, nt, 0);
+      fprintf(stderr, "[gmf] %s kernel (K1 %s): regs %d static smem %zu dyn smem %d (max %d) local %zu maxthreads %d -> %d CTAs/SM (%d without dyn smem)\n",
+              k == f ? "fit" : "grad", tcm == 2 ? "tc v2" : (tcm ? "tc v1" : "cuda cores"), a.numRegs,
+              a.sharedSizeBytes, smem, a.maxDynamicSharedSizeBytes, a.localSizeBytes,
+              a.maxThreadsPerBlock, n1, n2);
     }
   }
   return GMF_OK;
@@ -880,9 +992,16 @@ int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long x
   void* f = kernel_for(dtype, P.fam, NK, false, P.tcm);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   dim3 grid(P.RS, P.CT);
-  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm);
+  if (P.tcm == 2) {   // one CTA per SM walking the CT x RS units
+    int dev = 0, n_sm = kSMs;
+    GMF_CUDA(cudaGetDevice(&dev));
+    GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t units = (int64_t)P.RS * P.CT;
+    grid = dim3((unsigned)(units < n_sm ? units : n_sm));
+  }
+  const size_t smem = (size_t)grad_smem_bytes(P, dtype, NK);
   void* args[] = {(void*)&P, (void*)&xb, (void*)&xs, (void*)&xalpha};
-  GMF_CUDA(cudaLaunchKernel(f, grid, dim3(kThreads), args, smem, st));
+  GMF_CUDA(cudaLaunchKernel(f, grid, dim3(k1_threads(P.tcm)), args, smem, st));
   return GMF_OK;
 }
 
@@ -898,16 +1017,18 @@ int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs) {
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st) {
   void* f = kernel_for(dtype, P.fam, NK, true, P.tcm);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
-  const size_t smem = (size_t)grad_smem_bytes(dtype, NK, P.has_w, P.Kr, P.Kc, P.tcm) +
-                     (size_t)P.ep_cap * sizeof(int4);
+  const size_t smem = (size_t)grad_smem_bytes(P, dtype, NK) + (size_t)P.ep_cap * sizeof(int4);
   Params Q = P;
   Q.colimg_on = P.tcm && P.colimg != nullptr;   // images maintained by k_fit's own updates
   void* args[] = {(void*)&Q, (void*)&n_steps};
-  if (P.tcm) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
+  if (P.tcm == 1) {   // software grid barrier (soft_grid_sync): plain launch, fresh counters
     GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 32, st));
     GMF_CUDA(cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
   } else {
-    GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kThreads), args, smem, st));
+    // cooperative launch: every CTA co-resident by construction (K1 v2 runs
+    // one CTA per SM and synchronises through the software barrier)
+    if (P.tcm == 2) GMF_CUDA(cudaMemsetAsync(P.gbar, 0, 32, st));
+    GMF_CUDA(cudaLaunchCooperativeKernel(f, dim3(grid), dim3(k1_threads(P.tcm)), args, smem, st));
   }
   return GMF_OK;
 }

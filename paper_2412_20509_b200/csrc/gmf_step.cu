@@ -3,6 +3,8 @@
 // single-rank path runs the same bodies inside the persistent k_fit.
 #include <type_traits>
 
+#include <vector>
+
 #include "gmf_kern.cuh"
 
 namespace gmf {
@@ -566,6 +568,58 @@ __global__ void __launch_bounds__(kThreads) k_tile_index(Params P, int32_t* tidx
       for (int64_t k = lo + 1; k < hi; ++k)
         if (csr_col_at(P, k) <= csr_col_at(P, k - 1)) { atomicOr(unsorted, 1u); break; }
   }
+}
+
+// tile-CSR for K1 v2: the nonzeros of column tile ct (TC columns) of every
+// row, tile-major, each carrying its row: (row, count << 8 | column - ct TC).
+// lens[ct][i] = nonzeros of row i in tile ct (from the tile index)
+__global__ void __launch_bounds__(kThreads) k_tcsr_len(Params P, const int32_t* tidx, int32_t* lens) {
+  const int CT1 = P.CT + 1;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kThreads)
+    for (int ct = 0; ct < P.CT; ++ct) lens[(int64_t)ct * P.n + i] = tidx[i * CT1 + ct + 1] - tidx[i * CT1 + ct];
+}
+
+__global__ void __launch_bounds__(kThreads) k_tcsr_fill(Params P, const int32_t* tidx, const int64_t* tptr,
+                                                          int32_t* tent, unsigned int* too_big) {
+  const int CT1 = P.CT + 1;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kThreads) {
+    const int64_t k0 = P.rp[i];
+    for (int ct = 0; ct < P.CT; ++ct) {
+      const int64_t base = tptr[(int64_t)ct * (P.n + 1) + i];
+      const int a = tidx[i * CT1 + ct], b = tidx[i * CT1 + ct + 1];
+      for (int k = a; k < b; ++k) {
+        const int col = csr_col_at(P, k0 + k), val = csr_val_at(P, k0 + k);
+        if (val >= (1 << 23)) atomicOr(too_big, 1u);
+        tent[2 * (base + k - a)] = (int32_t)i;
+        tent[2 * (base + k - a) + 1] = (int32_t)(((uint32_t)val << 8) | (uint32_t)(col - ct * P.TC));
+      }
+    }
+  }
+}
+
+int launch_tcsr(const Params& P, const int32_t* tidx, int32_t* lens, int64_t* tptr, int32_t* tent,
+                unsigned int* too_big, cudaStream_t st) {
+  const unsigned b = (unsigned)((P.n + kThreads - 1) / kThreads < 4096 ? (P.n + kThreads - 1) / kThreads : 4096);
+  k_tcsr_len<<<b > 0 ? b : 1, kThreads, 0, st>>>(P, tidx, lens);
+  GMF_LAUNCH_CHECK("k_tcsr_len");
+  // exclusive scan in tile-major order on the host (once per handle)
+  std::vector<int32_t> h((size_t)P.CT * P.n);
+  GMF_CUDA(cudaMemcpyAsync(h.data(), lens, h.size() * 4, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> tp((size_t)P.CT * (P.n + 1));
+  int64_t run = 0;
+  for (int ct = 0; ct < P.CT; ++ct) {
+    for (int64_t i = 0; i < P.n; ++i) {
+      tp[(size_t)ct * (P.n + 1) + i] = run;
+      run += h[(size_t)ct * P.n + i];
+    }
+    tp[(size_t)ct * (P.n + 1) + P.n] = run;
+  }
+  GMF_CUDA(cudaMemcpyAsync(tptr, tp.data(), tp.size() * 8, cudaMemcpyHostToDevice, st));
+  k_tcsr_fill<<<b > 0 ? b : 1, kThreads, 0, st>>>(P, tidx, tptr, tent, too_big);
+  GMF_LAUNCH_CHECK("k_tcsr_fill");
+  GMF_CUDA(cudaStreamSynchronize(st));
+  return GMF_OK;
 }
 
 int launch_tile_index(const Params& P, int32_t* tidx, unsigned int* unsorted, cudaStream_t st) {

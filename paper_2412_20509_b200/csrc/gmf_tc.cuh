@@ -18,10 +18,11 @@
 //          (P and the chunk's A1 rows both read MN-major; [x|u] = first Kc of a)
 //
 // fp32 accuracy from bf16 operands: every operand is split x = hi + lo
-// (hi = bf16(x), lo = bf16(x - hi)); GEMM1 sums hi.hi + hi.lo + lo.hi,
-// GEMM2/3 all four products, accumulation in fp32 (TMEM).  Relative error
-// per product ~2^-17, inside the fp32 north-star tolerance (1e-4).
-//
+// (hi = bf16(x), lo = bf16(x - hi)); the column side of GEMM1 also carries a
+// third split x3 = bf16(x - hi - lo), so GEMM1 sums hi.hi + hi.lo + lo.hi +
+// hi.x3 (the intercept and offset features are exact in bf16, so large
+// intercepts b_j enter eta to ~2^-24); GEMM2/3 sum all four products,
+// accumulation in fp32 (TMEM).
 // Shared-memory operands use the canonical no-swizzle core-matrix layout
 // (8 rows x 16 bytes): K-major tiles for GEMM1/GEMM2 and the same P and A1
 // tiles read MN-major by GEMM3 (verified layouts: tools/umma_test.cu).
@@ -48,7 +49,7 @@ constexpr uint32_t T_ETA = 0, T_D2 = 128, T_D3 = 192;
 constexpr uint32_t SBO_P = 2048;      // P / R: 16 column cores x 128 B
 
 struct Smem {
-  int64_t P, R, B1h, B1l, A1, As, Y, stage, araw, off, rp, total;
+  int64_t P, R, B1h, B1l, B1x, A1, As, Y, stage, araw, off, rp, total;
   int nka;
 };
 
@@ -61,6 +62,7 @@ GMF_HD Smem smem_layout(int NK) {
   s.R = o; o = al(o + 64 * TCC * 2);
   s.B1h = o; o = al(o + TCC * s.nka * 2);
   s.B1l = o; o = al(o + TCC * s.nka * 2);
+  s.B1x = o; o = al(o + TCC * s.nka * 2);   // third split of the column operand
   s.A1 = o; o = al(o + 128 * s.nka * 2 * 2);   // hi | lo interleaved per 16 features
   s.As = o; o = al(o + TRC * 16 * 2 * 2);       // squares of features 0..15, hi | lo
   s.Y = o; o = al(o + TRC * YP * 4);
@@ -274,10 +276,36 @@ GMF_D void split8(const float (&x)[8], uint4& hi, uint4& lo) {
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// 8 fp32 values -> three bf16 splits x = s0 + s1 + s2 (error ~2^-24 |x|)
+GMF_D void split3_8(const float (&x)[8], uint4& s0, uint4& s1, uint4& s2) {
+  uint32_t a[4], b[4], c[4];
+  #pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float x0 = x[2 * u], x1 = x[2 * u + 1];
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(a[u]) : "f"(x1), "f"(x0));
+    const float r0 = x0 - __uint_as_float(a[u] << 16);
+    const float r1 = x1 - __uint_as_float(a[u] & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(b[u]) : "f"(r1), "f"(r0));
+    const float q0 = r0 - __uint_as_float(b[u] << 16);
+    const float q1 = r1 - __uint_as_float(b[u] & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(c[u]) : "f"(q1), "f"(q0));
+  }
+  s0 = make_uint4(a[0], a[1], a[2], a[3]);
+  s1 = make_uint4(b[0], b[1], b[2], b[3]);
+  s2 = make_uint4(c[0], c[1], c[2], c[3]);
+}
+
+GMF_D void split3_bf16(float x, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
+  a = __float2bfloat16_rn(x);
+  const float r = x - __bfloat162float(a);
+  b = __float2bfloat16_rn(r);
+  c = __float2bfloat16_rn(r - __bfloat162float(b));
+}
+
 // ---- column-operand images (persistent kernel, all columns every step) ----
 GMF_HD int64_t colimg_bytes(int NK) {
   const Smem L = smem_layout(NK);
-  return L.B1l + (L.B1l - L.B1h) - L.R;   // R | B1h | B1l, contiguous in smem
+  return L.B1x + (L.B1l - L.B1h) - L.R;   // R | B1h | B1l | B1x, contiguous in smem
 }
 
 // task t of column tile ct: R rows (feature k, 8 columns) then B1 rows
@@ -289,7 +317,8 @@ GMF_D void colimg_task(const Params& P, int ct, int t) {
   const int nka = L.nka, ng1 = nka / 8;
   const uint32_t sbo1 = (uint32_t)(nka / 8) * 128u;
   unsigned char* img = reinterpret_cast<unsigned char*>(P.colimg) + (int64_t)ct * colimg_bytes(NK);
-  unsigned char* Rb = img, *B1h = img + (L.B1h - L.R), *B1l = img + (L.B1l - L.R);
+  unsigned char* Rb = img, *B1h = img + (L.B1h - L.R), *B1l = img + (L.B1l - L.R),
+                *B1x = img + (L.B1x - L.R);
   const float* th_col = tptr<float>(P.th_col);
   const float* zg = tptr<float>(P.z);
   const int Kr = P.Kr, Kc = P.Kc, KA = P.KA, p = P.p, q = P.q;
@@ -329,10 +358,11 @@ GMF_D void colimg_task(const Params& P, int ct, int t) {
     else if (ok && k < KA) x = zg[j * q + (k - Kc)];
     v[u] = x * 1.4426950408889634f;
   }
-  uint4 h, l;
-  split8(v, h, l);
+  uint4 h, l, x;
+  split3_8(v, h, l, x);
   *reinterpret_cast<uint4*>(B1h + kofs(c, 8 * g, sbo1)) = h;
   *reinterpret_cast<uint4*>(B1l + kofs(c, 8 * g, sbo1)) = l;
+  *reinterpret_cast<uint4*>(B1x + kofs(c, 8 * g, sbo1)) = x;
 }
 
 template <int NK>
@@ -345,10 +375,11 @@ GMF_D void colimg_write(const Params& P, int64_t j, int k, float v) {
   const uint32_t sbo1 = (uint32_t)(L.nka / 8) * 128u;
   const int ct = (int)(j / TCC), c = (int)(j % TCC);
   unsigned char* img = reinterpret_cast<unsigned char*>(P.colimg) + (int64_t)ct * colimg_bytes(NK);
-  __nv_bfloat16 h, l;
-  split_bf16(v * 1.4426950408889634f, h, l);
+  __nv_bfloat16 h, l, x;
+  split3_bf16(v * 1.4426950408889634f, h, l, x);
   *reinterpret_cast<__nv_bfloat16*>(img + (L.B1h - L.R) + kofs(c, k, sbo1)) = h;
   *reinterpret_cast<__nv_bfloat16*>(img + (L.B1l - L.R) + kofs(c, k, sbo1)) = l;
+  *reinterpret_cast<__nv_bfloat16*>(img + (L.B1x - L.R) + kofs(c, k, sbo1)) = x;
   if (k >= P.p) {
     const int kr = P.q + (k - P.p);
     __nv_bfloat16 h2, l2;
@@ -402,6 +433,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   unsigned char* Rb = smem + L.R;
   unsigned char* B1h = smem + L.B1h;
   unsigned char* B1l = smem + L.B1l;
+  unsigned char* B1x = smem + L.B1x;
   unsigned char* A1b = smem + L.A1;
   unsigned char* Asb = smem + L.As;
   int32_t* Y = reinterpret_cast<int32_t*>(smem + L.Y);
@@ -518,9 +550,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   if (!use_img) {
     uint4 h, l;
     if (b1_task) {
-      split8(b1v, h, l);
+      uint4 x;
+      split3_8(b1v, h, l, x);
       *reinterpret_cast<uint4*>(B1h + kofs(b1c, 8 * b1g, sbo1)) = h;
       *reinterpret_cast<uint4*>(B1l + kofs(b1c, 8 * b1g, sbo1)) = l;
+      *reinterpret_cast<uint4*>(B1x + kofs(b1c, 8 * b1g, sbo1)) = x;
     }
     float r2[8];
     #pragma unroll
@@ -548,10 +582,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       const float x = *src;
       v[u] = (in_c || in_z) ? x * pre : 0.f;
     }
-    uint4 h, l;
-    split8(v, h, l);
+    uint4 h, l, x;
+    split3_8(v, h, l, x);
     *reinterpret_cast<uint4*>(B1h + kofs(c, 8 * g, sbo1)) = h;
     *reinterpret_cast<uint4*>(B1l + kofs(c, 8 * g, sbo1)) = l;
+    *reinterpret_cast<uint4*>(B1x + kofs(c, 8 * g, sbo1)) = x;
   }
   tick(0);
 
@@ -694,9 +729,11 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
         const uint64_t al = sdesc(sb + (uint32_t)L.A1 + (uint32_t)kt * 512u + 256u, 128, sboc);
         const uint64_t bh = sdesc(sb + (uint32_t)L.B1h + ko, 128, sbo1);
         const uint64_t bl = sdesc(sb + (uint32_t)L.B1l + ko, 128, sbo1);
+        const uint64_t bx = sdesc(sb + (uint32_t)L.B1x + ko, 128, sbo1);
         umma(tm + T_ETA, ah, bh, ID1, kt > 0 ? 1u : 0u);
         umma(tm + T_ETA, ah, bl, ID1, 1u);
         umma(tm + T_ETA, al, bh, ID1, 1u);
+        umma(tm + T_ETA, ah, bx, ID1, 1u);   // the column side's third split (intercepts)
       }
       umma_commit(&X.bar[0]);
     }

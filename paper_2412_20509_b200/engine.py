@@ -194,6 +194,16 @@ class DeviceFit:
             t = torch.from_numpy(a)
             return t.to(device=dev, dtype=dt if dt is not None else t.dtype)
 
+        def up_padded(a, dt=None):
+            # 16 bytes of readable tail slack (gmf_desc.flags: the tensor-core
+            # K1 stages row ranges with TMA bulk copies of 16-byte aligned supersets)
+            a = np.ascontiguousarray(a)
+            t = torch.from_numpy(a)
+            dt = dt if dt is not None else t.dtype
+            buf = torch.zeros(t.numel() + 16, device=dev, dtype=dt)
+            buf[:t.numel()].copy_(t.reshape(-1).to(dtype=dt))
+            return buf[:t.numel()].view(t.shape)
+
         # ---- response ----
         if data.csr is not None:
             indptr, indices, vals = data.csr
@@ -207,12 +217,12 @@ class DeviceFit:
             if y_format == "packed" and not fits:
                 raise ConfigError("packed CSR needs m <= 65536 and counts <= 65535")
             if y_format != "csr32" and fits:
-                self.csr_col = up(pack_csr(c2, counts))
+                self.csr_col = up_padded(pack_csr(c2, counts))
                 self.csr_val = None
                 y_format_code = _lib.Y_CSR_PACK32
             else:
-                self.csr_col = up(c2.astype(np.int32))
-                self.csr_val = up(counts)
+                self.csr_col = up_padded(c2.astype(np.int32))
+                self.csr_val = up_padded(counts)
                 y_format_code = _lib.Y_CSR_I32
         else:
             self.y_dense = up(_counts_int32(data.values[order], "response"))
@@ -224,10 +234,10 @@ class DeviceFit:
                 raise _lib.UnsupportedError("prior weights need a dense response")
             self.weights = up(data.weights[order], tdt)
         # ---- designs, offset, parameters ----
-        self.x = up(covs.x[order], tdt)
+        self.x = up_padded(covs.x[order], tdt)
         self.z = up(covs.z, tdt)
-        self.offset = None if offset is None else up(np.asarray(offset, dtype=float)[order], tdt)
-        self.theta_row = up(np.hstack([state.gamma, state.u])[order], tdt)
+        self.offset = None if offset is None else up_padded(np.asarray(offset, dtype=float)[order], tdt)
+        self.theta_row = up_padded(np.hstack([state.gamma, state.u])[order], tdt)
         self.theta_col = up(np.hstack([state.b, state.v]), tdt)
         Kr, Kc = self.q + self.d, self.p + self.d
         z = lambda r, c: torch.zeros((r, c), device=dev, dtype=tdt)
@@ -266,7 +276,7 @@ class DeviceFit:
                                  family=_lib.FAMILY_CODES[fam.kind], link=_lib.LINK_CODES[lnk.kind],
                                  y_format=y_format_code, has_offset=int(offset is not None),
                                  has_weights=int(self.weights is not None), world_size=world,
-                                 rank=rank, device=dev_index, reserved=0)
+                                 rank=rank, device=dev_index, flags=_lib.DESC_TAIL_PADDED)
         self.cfg = _lib.GmfConfig(
             rate_k0=cfg.rate_k0, rate_k1=cfg.rate_k1, rate_tau=cfg.rate_tau,
             smooth_a1=cfg.smooth_a1, smooth_a2=cfg.smooth_a2, damping=cfg.damping, tol=cfg.tol,
@@ -297,6 +307,7 @@ class DeviceFit:
         self.lib = lib
         self.rec_bytes = int(lib.gmf_record_bytes(h))
         self.k1_impl = _lib.K1_IMPL_NAMES[int(lib.gmf_k1_impl(h))]
+        self.k1_version = int(lib.gmf_k1_version(h))   # 0 CUDA cores, 1/2 tensor-core K1 v1/v2
 
     def ready_ptr(self):
         """Device address of the streaming ready counter (gmf_stream_ready_ptr)."""

@@ -40,3 +40,12 @@ def cuda_ok():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(params=["v1", "v2"])
+def k1_generation(request, monkeypatch):
+    """Run a tensor-core test on both K1 generations: v1 (two 256-thread CTAs
+    per SM, one 32-row chunk at a time) and v2 (warp-specialized tcgen05
+    pipeline, gmf_tc2.cuh).  gmf_create reads GMF_TC_VERSION."""
+    monkeypatch.setenv("GMF_TC_VERSION", "1" if request.param == "v1" else "2")
+    return request.param

@@ -129,7 +129,7 @@ def _compare_final(final, rep, ofinal, orep, n, seed=5):
     assert rep.final_objective == pytest.approx(orep.final_objective, rel=1e-3)
 
 
-def test_c3_full_size_fp32_csr_matches_oracle():
+def test_c3_full_size_fp32_csr_matches_oracle(k1_generation):
     wl, data, covs, st, cfg, pb, ost, ocfg = _csr_problem("c3", 20)
     final, rep = gk.fit_asgd(data, covs, gk.NegBinomial(st.nb_shape), gk.Log(),
                              gk.PenaltyConfig(), cfg, st, dtype="f32")
@@ -138,7 +138,7 @@ def test_c3_full_size_fp32_csr_matches_oracle():
     _compare_final(final, rep, ofinal, orep, wl.spec.n)
 
 
-def test_c4_full_size_persistent_fit_matches_oracle():
+def test_c4_full_size_persistent_fit_matches_oracle(k1_generation):
     """The headline workload through the persistent k_fit the bench times
     (one launch, no callback): 10 epochs vs the oracle, and the per-step states
     of steps 0..9 (one k_fit launch per step through the callback path: V, B,
@@ -197,7 +197,7 @@ C5_CELLS = [
 
 
 @pytest.mark.parametrize("cell", C5_CELLS, ids=lambda c: "-".join(str(v) for v in c))
-def test_c5_cell_gradient_matches_oracle(cell):
+def test_c5_cell_gradient_matches_oracle(cell, k1_generation):
     """BASELINE config 5 cells: one block of n* rows x all m columns from a
     c1-style matrix (dense, or CSR at ~90% zeros), the fused block gradient and
     NB moment sums against the fp64 oracle (1e-10 fp64, 1e-4 fp32)."""

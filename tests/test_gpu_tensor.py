@@ -59,7 +59,7 @@ CASES = [
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}m{c[1]}d{c[2]}p{c[3]}q{c[4]}{c[5]}")
 @pytest.mark.parametrize("impl", ["tensor", "cuda_cores"])
-def test_k1_block_gradient_matches_oracle(case, impl):
+def test_k1_block_gradient_matches_oracle(case, impl, k1_generation):
     n, m, d, p, q, family, offset, mbr, mbc = case
     y, x, z, off, st = _problem(7, n, m, d, p, q, family, offset)
     rng = np.random.default_rng(11)
@@ -87,7 +87,7 @@ def test_k1_block_gradient_matches_oracle(case, impl):
 
 
 @pytest.mark.parametrize("case", CASES[:3], ids=lambda c: f"n{c[0]}m{c[1]}")
-def test_k1_tensor_close_to_cuda_cores(case):
+def test_k1_tensor_close_to_cuda_cores(case, k1_generation):
     n, m, d, p, q, family, offset, mbr, mbc = case
     y, x, z, off, st = _problem(3, n, m, d, p, q, family, offset)
     I = np.arange(0, n, 2)
@@ -104,7 +104,7 @@ def test_k1_tensor_close_to_cuda_cores(case):
         assert normwise(getattr(a, f), getattr(b, f)) < TOL, f
 
 
-def test_k1_tensor_csr_equals_dense_bitwise():
+def test_k1_tensor_csr_equals_dense_bitwise(k1_generation):
     from paper_2412_20509_b200.workloads import dense_to_csr
     y, x, z, off, st = _problem(5, 300, 200, 10, 1, 0, "nb", True)
     I, J = np.arange(7, 250), np.arange(200)
@@ -133,7 +133,7 @@ def test_k1_tensor_rejects_ineligible_problems():
 
 
 @pytest.mark.parametrize("impl", ["tensor", "cuda_cores"])
-def test_fit_fp32_trajectory_per_impl(impl):
+def test_fit_fp32_trajectory_per_impl(impl, k1_generation):
     from conftest import golden
     g = golden("nb_cov_s3")
     data = gk.ResponseMatrix(g["y"].astype(float))
@@ -152,7 +152,7 @@ def test_fit_fp32_trajectory_per_impl(impl):
     assert normwise(final.u @ final.v.T, g["final_u"] @ g["final_v"].T) < 1e-3
 
 
-def test_packed_csr_equals_csr32_bitwise():
+def test_packed_csr_equals_csr32_bitwise(k1_generation):
     """Packed CSR (one uint32 per nonzero) and int32 CSR hold the same counts:
     identical trajectories on both K1 implementations."""
     from conftest import golden
@@ -175,7 +175,7 @@ def test_packed_csr_equals_csr32_bitwise():
         assert out[0] == out[1], impl
 
 
-def test_streaming_run_equals_resident_run_bitwise():
+def test_streaming_run_equals_resident_run_bitwise(k1_generation):
     """gmf_run_stream (one launch; each step waits for its row block's ready
     signal, statuses written to pinned host memory) reproduces gmf_run."""
     import torch
@@ -248,3 +248,27 @@ def test_per_step_path_matches_persistent(monkeypatch, dtype, tol):
     assert np.allclose(out[0][0], out[1][0], rtol=tol, atol=0)
     for a, b in zip(out[0][1:], out[1][1:]):
         assert normwise(b, a) < tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gen", [1, 2])
+def test_k1_generation_is_the_one_requested(gen, monkeypatch):
+    """GMF_TC_VERSION selects the tensor-core K1 generation the handle runs
+    (gmf_k1_version), so the parametrized parity tests exercise both."""
+    import torch
+    from paper_2412_20509_b200.engine import DeviceFit, Schedule
+    monkeypatch.setenv("GMF_TC_VERSION", str(gen))
+    rng = np.random.default_rng(5)
+    n, m, d = 3000, 300, 4
+    y = rng.poisson(1.5, (n, m)).astype(float)
+    st = gk.FactorizationState(rng.normal(0, .1, (m, 1)), np.zeros((n, 0)), rng.normal(0, .3, (n, d)),
+                               rng.normal(0, .3, (m, d)), 1.0, 2.0)
+    cfg = gk.SgdConfig(max_epochs=3, mb_rows=1000, mb_cols=m, tol=1e-30, seed=0)
+    fit = DeviceFit(gk.ResponseMatrix(y), gk.CovariateSet(x=np.ones((n, 1)), m=m), gk.Poisson(),
+                    gk.Log(), gk.PenaltyConfig(), cfg, st, schedule=Schedule(n, m, cfg), dtype="f32",
+                    k1_impl="tensor")
+    try:
+        assert fit.k1_version == gen
+    finally:
+        fit.close()
+        torch.cuda.synchronize()

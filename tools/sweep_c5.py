@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--quick", action="store_true", help="m = 500 only")
     ap.add_argument("--only-d", type=int, default=None, help="one rank only")
     ap.add_argument("--only-dtype", default=None, help="f32 or f64 only")
+    ap.add_argument("--only-m", type=int, default=None, help="one column count only")
+    ap.add_argument("--only-family", default=None, help="poisson or nb only")
+    ap.add_argument("--only-nstar", type=int, default=None, help="one block size only")
+    ap.add_argument("--only-format", default=None, help="dense or csr only")
     args = ap.parse_args()
     import torch
     import paper_2412_20509_b200 as gk
@@ -48,8 +52,10 @@ def main():
     peak, peak_src = bench._peak_hbm()
     N = 65536
     ms_list = [500] if args.quick else [500, 2000, 5000]
+    if args.only_m:
+        ms_list = [args.only_m]
     for m in ms_list:
-        for fmt in ("dense", "csr"):
+        for fmt in ((args.only_format,) if args.only_format else ("dense", "csr")):
             spec = workloads.WorkloadSpec("c5", N, m, 5, "poisson", "f32", fmt, 256, 1, p=1, q=1,
                                           zero_frac=0.90 if fmt == "csr" else None)
             t0 = time.perf_counter()
@@ -67,9 +73,9 @@ def main():
                 st = gk.FactorizationState(wl.truth["b"], wl.truth["gamma"],
                                            0.3 * rng.standard_normal((N, d)),
                                            0.3 * rng.standard_normal((m, d)), 1.0, 2.0)
-                for family in ("poisson", "nb"):
+                for family in ((args.only_family,) if args.only_family else ("poisson", "nb")):
                     for dtype in ((args.only_dtype,) if args.only_dtype else ("f32", "f64")):
-                        for nstar in (256, 4096, 65536):
+                        for nstar in ((args.only_nstar,) if args.only_nstar else (256, 4096, 65536)):
                             cell = {"nstar": nstar, "m": m, "d": d, "family": family,
                                     "dtype": dtype, "format": fmt}
                             try:
