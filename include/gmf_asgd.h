@@ -148,7 +148,7 @@ typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py
   int32_t est_alpha;             /* NB shape estimated (optim.py:156-168) */
   int32_t snapshot_stride;       /* 4 (optim.py:309) */
   int32_t k1_impl;               /* enum gmf_k1_impl (no reference counterpart) */
-  int32_t reserved;
+  int32_t nafill_every;          /* imputation period of unobserved entries (optim.py:432) */
 } gmf_config;
 
 typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
@@ -181,6 +181,13 @@ typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
   const int64_t* eval_row;        /* E local tracked-objective entries      */
   const int32_t* eval_col;
   int64_t n_eval;
+  /* responses with unobserved entries (dense only; NULL when fully observed):
+     n x m working response in the compute dtype -- observed counts as >= 0
+     values, an unobserved entry as -(its current imputed mean), seeded by
+     the caller with -g^{-1}(eta0) (optim.py:368-374) and refilled by the
+     gradient kernel every nafill_every steps (optim.py:430-436); the
+     tracked objective, the deviance and the information criteria skip it */
+  void* y_work;
 } gmf_buffers;
 
 typedef struct gmf_status {

@@ -61,7 +61,7 @@ class GmfConfig(C.Structure):
                 ("lam_u", C.c_double), ("lam_v", C.c_double), ("nb_floor", C.c_double),
                 ("nb_ceiling", C.c_double), ("phi", C.c_double), ("eval_scale", C.c_double),
                 ("max_epochs", C.c_int64), ("est_alpha", C.c_int32),
-                ("snapshot_stride", C.c_int32), ("k1_impl", C.c_int32), ("reserved", C.c_int32)]
+                ("snapshot_stride", C.c_int32), ("k1_impl", C.c_int32), ("nafill_every", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -75,7 +75,7 @@ class GmfBuffers(C.Structure):
                 ("row_block_ptr", _P), ("row_block_scale", _P), ("n_row_blocks", C.c_int64),
                 ("col_idx", _P), ("col_block_ptr", _P), ("col_pos", _P), ("col_block_of", _P),
                 ("n_col_blocks", C.c_int64), ("block_seq", _P), ("max_steps", C.c_int64),
-                ("eval_row", _P), ("eval_col", _P), ("n_eval", C.c_int64)]
+                ("eval_row", _P), ("eval_col", _P), ("n_eval", C.c_int64), ("y_work", _P)]
 
 
 class GmfStatus(C.Structure):

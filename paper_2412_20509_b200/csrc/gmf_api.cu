@@ -15,7 +15,7 @@ namespace gmf {
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha);
 int prepare_grad(const Params& P, int dtype, int NK, int fit_extra_smem, int* fit_blocks_per_sm);
-int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA);
+int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA, int holes);
 int64_t colimg_bytes_total(int NK, int CT, int tcm);
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st);
 int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs);
@@ -207,10 +207,18 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
                        (!P.has_off || al16(bufs->offset)) &&
                        (desc->y_format == GMF_Y_DENSE_I32 || al16(bufs->csr_col)) &&
                        (desc->y_format != GMF_Y_CSR_I32 || al16(bufs->csr_val));
-  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA) && aligned;
+  P.holes = bufs->y_work != nullptr;
+  P.y_work = bufs->y_work;
+  P.nafill = cfg->nafill_every > 0 ? cfg->nafill_every : 1;
+  if (P.holes && desc->y_format != GMF_Y_DENSE_I32) {
+    set_error("unobserved entries need a dense response (y_work)");
+    delete h;
+    return GMF_ERR_CONFIG;
+  }
+  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA, P.holes) && aligned;
   if (cfg->k1_impl == GMF_K1_TENSOR && !tc_ok) {
-    set_error("k1_impl=tensor needs fp32, no prior weights, q+d <= 16, p+d <= 16 and 16-byte "
-              "aligned row/CSR buffers (got Kr=%d Kc=%d)", Kr, Kc);
+    set_error("k1_impl=tensor needs fp32, no prior weights, no unobserved entries, q+d <= 16, "
+              "p+d <= 16 and 16-byte aligned row/CSR buffers (got Kr=%d Kc=%d)", Kr, Kc);
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }

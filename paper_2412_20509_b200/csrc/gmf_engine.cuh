@@ -42,6 +42,9 @@ struct Params {
   int64_t n, m;
   int p, q, d, KA, Kr, Kc;
   int fam, yfmt, has_w, has_off;
+  int holes;            // unobserved entries: y_work carries them (negative = imputed mean)
+  int nafill;           // refill period (optim.py:432)
+  void* y_work;         // [n][m] T working response (holes only)
   const int32_t* y;
   const int64_t* rp;
   int64_t nnz;          // rp[n] (CSR)

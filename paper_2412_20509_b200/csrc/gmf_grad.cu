@@ -58,7 +58,11 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
     tc::grad_cta<FAM, NK>(P, blk, s, alpha, rs, ct, RS, smem, tcx, nullptr);
     tc::ctx_close(tcx);
   } else {
-    grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem);
+    // holes: a standalone gradient masks them (gradients.py:66-88); inside
+    // the fit they carry the imputed mean, refilled every nafill steps
+    const int hmode = P.holes ? (xb >= 0 ? 2 : 1) : 0;
+    const bool fill = hmode == 1 && mod_nn(P.ctrl->t, P.nafill) == 0;
+    grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem, hmode, fill);
   }
 
   (void)TC;
@@ -540,7 +544,8 @@ k_fit(Params P, long long n_steps) {
       if constexpr (TCM == 1)
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
                               profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
-      else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem);
+      else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, P.holes ? 1 : 0,
+                                    P.holes && mod_nn(t, P.nafill) == 0);
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 2] = gtimer(); }
@@ -908,8 +913,8 @@ int set_k1_dbg(int v) {
   return GMF_OK;
 }
 
-int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA) {
-  return dtype == GMF_F32 && !has_w && Kr <= 16 && Kc <= 16 && KA <= 32;
+int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA, int holes) {
+  return dtype == GMF_F32 && !has_w && !holes && Kr <= 16 && Kc <= 16 && KA <= 32;
 }
 
 int grad_bucket(int KA) {

@@ -125,7 +125,7 @@ GMF_HD GradSmem grad_smem(int TC, int NK, int tsz, int has_w, int Kr, int Kc) {
   s.rp = o; o = al(o + (int64_t)(kRpMax + 1) * 8);
   s.ytile = o; o = al(o + (int64_t)TR * TC * 4);
   // a stage holds either the dense int32 Y tile or the CSR (col, val) range
-  const int64_t dense = (int64_t)TR * TC * 4, csr = (int64_t)kStageCap * 8;
+  const int64_t dense = (int64_t)TR * TC * tsz, csr = (int64_t)kStageCap * 8;   // int32 or T (holes)
   s.stage_bytes = dense > csr ? dense : csr;
   for (int b = 0; b < 2; ++b) {
     s.stage[b] = o; o = al(o + s.stage_bytes);
@@ -158,12 +158,18 @@ GMF_D double rcp_fast(double x) { return 1.0 / x; }
 // phase 1 of one chunk: eta, mu, dotD, ddotD per entry; column side into
 // registers; P tile into shared memory.  Branch-free: invalid rows/columns
 // carry weight 0, which zeroes dotD, ddotD and the NB moment terms.
-template <typename T, int FAM, int NK, int TC, bool HW>
+// HOLES: the staged Y tile holds the working response (T): observed values
+// >= 0, an unobserved entry as -(its imputed mean).  hmode 1 (the fit):
+// holes enter with their imputed mean, refilled with this step's mu when
+// `fill` (optim.py:430-436, the refill written back through ywg); hmode 2
+// (standalone minibatch gradients, gradients.py:66-88): holes carry weight 0.
+template <typename T, int FAM, int NK, int TC, bool HW, bool HOLES = false>
 GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
                   const T* __restrict__ off_s, const int32_t* __restrict__ y_s,
                   const T* __restrict__ w_s, T* __restrict__ P_s, const T (&cf)[NK],
                   T (&gacc)[NK], T (&hacc)[NK], T cm, int c, int g, int rows, T rphi, T tphi,
-                  T ralpha, T& cn, T& cd) {
+                  T ralpha, T& cn, T& cd, int hmode = 0, bool fill = false, T* ywg = nullptr,
+                  int64_t ystride = 0) {
   constexpr int NG = kThreads / TC;
   #pragma unroll 2
   for (int rr = g; rr < rows; rr += NG) {
@@ -175,8 +181,20 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
       e1 = fma(a[k + 1], cf[k + 1], e1);
     }
     const T mu = exp_pre(e0 + e1);
-    const T yv = (T)y_s[rr * TC + c];
-    const T wv = HW ? w_s[rr * TC + c] : cm;
+    T yv;
+    T wv = HW ? w_s[rr * TC + c] : cm;
+    if constexpr (HOLES) {
+      const T v = reinterpret_cast<const T*>(y_s)[rr * TC + c];
+      const bool hole = signbit(v);
+      yv = hole ? -v : v;
+      if (hole && hmode == 2) wv = T(0);
+      if (hole && hmode == 1 && fill && cm != T(0)) {
+        yv = mu;
+        ywg[(int64_t)rr * ystride] = -mu;
+      }
+    } else {
+      yv = (T)y_s[rr * TC + c];
+    }
     const T r = yv - mu;
     T dd, hh;
     if (FAM == 0) {
@@ -203,7 +221,7 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
 
 template <typename T, int FAM, int NK, int TC>
 GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct,
-                    int RS, unsigned char* smem) {
+                    int RS, unsigned char* smem, int hmode = 0, bool fill = false) {
   constexpr int NG = kThreads / TC;
   constexpr int TCQ = TC / NQ;
   __shared__ double red_scr[kThreads / 32];
@@ -303,7 +321,17 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       }
     }
     unsigned char* st = smem + L.stage[b];
-    if (!csr) {
+    if (!csr && P.holes) {   // working response (T), holes negative
+      T* y_b = reinterpret_cast<T*>(st);
+      const T* yw = tptr<T>(P.y_work);
+      for (int e = tid; e < TR * TC; e += kThreads) {
+        const int rr = e / TC, cc = e % TC;
+        const int64_t pp = cbase + cc;
+        const bool ok = rr < rows && pp < nJ;
+        const int64_t jj = ok ? (P.col_identity ? pp : (int64_t)P.cidx[j0 + pp]) : 0;
+        cp_async<sizeof(T)>(y_b + e, ok ? yw + (i0 + rr) * P.m + jj : yw, ok);
+      }
+    } else if (!csr) {
       int32_t* y_b = reinterpret_cast<int32_t*>(st);
       for (int e = tid; e < TR * TC; e += kThreads) {
         const int rr = e / TC, cc = e % TC;
@@ -412,12 +440,23 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
 
     // ---- phase 1 ----
     T cn = T(0), cd = T(0);
-    if (P.has_w)
+    if (P.holes) {
+      T* ywg = tptr<T>(P.y_work) + i0 * P.m + j;   // the chunk's first row, this thread's column j
+      if (P.has_w)
+        phase1<T, FAM, NK, TC, true, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
+                                           g, rows, rphi, tphi, ralpha, cn, cd, hmode, fill, ywg,
+                                           P.m);
+      else
+        phase1<T, FAM, NK, TC, false, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm,
+                                            c, g, rows, rphi, tphi, ralpha, cn, cd, hmode, fill,
+                                            ywg, P.m);
+    } else if (P.has_w) {
       phase1<T, FAM, NK, TC, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c, g,
                                    rows, rphi, tphi, ralpha, cn, cd);
-    else
+    } else {
       phase1<T, FAM, NK, TC, false>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c, g,
                                     rows, rphi, tphi, ralpha, cn, cd);
+    }
     nb_num += (double)cn;
     nb_den += (double)cd;
     __syncthreads();

@@ -422,8 +422,11 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
           const int64_t j = j0 + cc;
           const double eta = acc[r][h] + offs[rr];
           if (dense) {
-            const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
+            double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
             const double y = (double)P.y[i * P.m + j];
+            // unobserved entries (negative working response) are not in the
+            // masked deviance (model.py:268-276)
+            if (P.holes && signbit(tptr<T>(P.y_work)[i * P.m + j])) w = 0.0;
             s += w * dev_at<T>(P.fam, y, eta, alpha);
             if (with_const && y > 0.0) c += w * nb_loglik_term(y, alpha);
           } else {

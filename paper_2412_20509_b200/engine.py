@@ -167,9 +167,9 @@ class DeviceFit:
             raise _lib.UnsupportedError(
                 f"the fused aSGD kernels implement poisson/neg_binomial with log link, "
                 f"got {fam.kind}+{lnk.kind}")
-        if not data.fully_observed:
-            raise _lib.UnsupportedError("missing-value imputation is not on the device path "
-                                        "(fully observed responses only)")
+        holes = not data.fully_observed
+        if holes and data.csr is not None:
+            raise _lib.UnsupportedError("unobserved entries need a dense response")
         if dtype not in ("f32", "f64"):
             raise ConfigError(f"dtype must be 'f32' or 'f64', got {dtype!r}")
         if k1_impl not in _lib.K1_IMPL_CODES:
@@ -225,9 +225,28 @@ class DeviceFit:
                 self.csr_val = up_padded(counts)
                 y_format_code = _lib.Y_CSR_I32
         else:
-            self.y_dense = up(_counts_int32(data.values[order], "response"))
+            vals = data.values[order]
+            if holes:   # observed counts; the working response below carries the holes
+                vals = np.where(data.mask[order], vals, 0.0)
+            self.y_dense = up(_counts_int32(vals, "response"))
             self.csr_ptr = self.csr_col = self.csr_val = None
             y_format_code = _lib.Y_DENSE_I32
+        self.y_work = None
+        if holes:
+            # working response (optim.py:368-374): observed counts, and at every
+            # unobserved entry minus its mean at the initial state,
+            # -g^{-1}(eta0) -- the sign marks the hole, the kernel refills it
+            mo = data.mask[order]
+            eta0 = state.u[order] @ state.v.T
+            if covs.p:
+                eta0 = eta0 + covs.x[order] @ state.b.T
+            if covs.q:
+                eta0 = eta0 + state.gamma[order] @ covs.z.T
+            if offset is not None:
+                eta0 = eta0 + np.asarray(offset, dtype=float)[order][:, None]
+            with np.errstate(all="ignore"):
+                yw = np.where(mo, data.values[order], -np.exp(eta0))
+            self.y_work = up(yw, self.tdt)
         self.weights = None
         if data.weights is not None:
             if data.csr is not None:
@@ -284,7 +303,7 @@ class DeviceFit:
             lam_v=penalty.lam_v, nb_floor=1e-4, nb_ceiling=1e8, phi=float(state.phi),
             eval_scale=float(schedule.eval_scale), max_epochs=cfg.max_epochs,
             est_alpha=int(bool(est_alpha)), snapshot_stride=4,
-            k1_impl=_lib.K1_IMPL_CODES[k1_impl], reserved=0)
+            k1_impl=_lib.K1_IMPL_CODES[k1_impl], nafill_every=int(cfg.nafill_every))
         P = _lib.ptr
         self.bufs = _lib.GmfBuffers(
             y_dense=P(self.y_dense), csr_ptr=P(self.csr_ptr), csr_col=P(self.csr_col),
@@ -296,7 +315,8 @@ class DeviceFit:
             n_row_blocks=len(schedule.row_blocks), col_idx=P(self.col_idx),
             col_block_ptr=P(self.cbp), col_pos=P(self.col_pos), col_block_of=P(self.col_of),
             n_col_blocks=len(cb), block_seq=P(self.block_seq), max_steps=schedule.max_steps,
-            eval_row=P(self.eval_row), eval_col=P(self.eval_col), n_eval=n_eval)
+            eval_row=P(self.eval_row), eval_col=P(self.eval_col), n_eval=n_eval,
+            y_work=P(self.y_work))
         self.phi = float(state.phi)
         self.init_nb_shape = float(state.nb_shape)
         h = C.c_void_p()

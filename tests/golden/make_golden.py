@@ -88,9 +88,12 @@ class OffsetShim:
         goptim._entrywise_eta = self.saved["e"]
 
 
-def _run_fit(y, x, z, init, fam, cfg, offset=None, lam=None, weights=None):
+def _run_fit(y, x, z, init, fam, cfg, offset=None, lam=None, weights=None, mask=None):
     pen = lam or gk.PenaltyConfig()
-    data = gk.ResponseMatrix(y.astype(float), weights=weights)
+    yv = y.astype(float)
+    if mask is not None:
+        yv = np.where(mask, yv, np.nan)
+    data = gk.ResponseMatrix(yv, mask=mask, weights=weights)
     covs = gk.CovariateSet(x=x if x.shape[1] else None, z=z if z.shape[1] else None,
                            n=y.shape[0], m=y.shape[1])
     steps = {}
@@ -138,6 +141,9 @@ def _run_fit(y, x, z, init, fam, cfg, offset=None, lam=None, weights=None):
         out["offset"] = offset
     if weights is not None:
         out["w"] = weights
+    if mask is not None:
+        out["mask"] = mask
+        out["nafill"] = np.int64(cfg.nafill_every)
     out.update(_state_arrays("init", init_st))
     out.update(_state_arrays("final", final))
     out.update(_state_arrays("unproj", unproj))
@@ -483,12 +489,30 @@ def make_project_b23():
     return out
 
 
+def make_masked():
+    """Unobserved entries (~15 %): imputation at the initial state and every
+    nafill_every steps (optim.py:368-374, 430-436), NB with an offset."""
+    y, x, z, off, init = _nb_problem(700, 90, 1, 0, 4, 21, True)
+    mask = np.random.default_rng(22).uniform(size=y.shape) > 0.15
+    cfg = gk.SgdConfig(max_epochs=25, mb_rows=140, mb_cols=90, tol=1e-30, seed=4, nafill_every=1)
+    return _run_fit(y, x, z, init, gk.NegBinomial(1.5), cfg, offset=off, mask=mask)
+
+
+def make_masked_p3():
+    """Poisson with covariates, holes refilled every third step, S = 2."""
+    y, x, z, _, init = _nb_problem(600, 80, 2, 1, 3, 23, False)
+    mask = np.random.default_rng(24).uniform(size=y.shape) > 0.2
+    cfg = gk.SgdConfig(max_epochs=10, mb_rows=120, mb_cols=40, tol=1e-30, seed=6, nafill_every=3)
+    return _run_fit(y, x, z, init, gk.Poisson(), cfg, mask=mask)
+
+
 def main():
     makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,
-              "project_b23": make_project_b23, "c2": make_c2}
+              "project_b23": make_project_b23, "c2": make_c2, "masked": make_masked,
+              "masked_p3": make_masked_p3}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
