@@ -35,7 +35,8 @@ from .engine import _counts_int32
 from .exceptions import ConfigError
 from .model import CovariateSet, FactorizationState, ResponseMatrix
 
-__all__ = ["InitMethod", "init_ols_svd", "randomized_svd_sparse"]
+__all__ = ["InitMethod", "init_ols_svd", "init_glm_svd", "fit_glm_batched", "randomized_svd_sparse",
+           "randomized_svd_dense"]
 
 
 class _Laps:
@@ -250,4 +251,239 @@ def init_ols_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
     state = FactorizationState(host(B), host(Gm), host(U), host(V), 1.0, nb_shape)
     lap("download")
     info = {"method": "ols_svd"}
+    return (state, info) if return_info else state
+
+
+# ---------------------------------------------------------------------------
+# GLM-SVD (the reference's default initialization, initialization.py:172-214)
+# ---------------------------------------------------------------------------
+
+def _dense_inputs(data: ResponseMatrix, dev):
+    """Y, observation mask and effective weights as dense fp64 device arrays."""
+    import torch
+    n, m = data.shape
+    if data.csr is not None:
+        indptr, indices, vals = data.csr
+        Y = torch.zeros((n, m), dtype=torch.float64, device=dev)
+        rows = np.repeat(np.arange(n), np.diff(np.asarray(indptr)))
+        Y[torch.from_numpy(rows).to(dev), torch.from_numpy(np.asarray(indices, np.int64)).to(dev)] = \
+            torch.from_numpy(np.asarray(vals, dtype=float)).to(dev)
+        mask = torch.ones((n, m), dtype=torch.bool, device=dev)
+    else:
+        mask_h = data.mask if data.mask is not None else np.ones((n, m), bool)
+        Y = torch.from_numpy(np.where(mask_h, data.values, 0.0)).to(dev)
+        mask = torch.from_numpy(np.asarray(mask_h)).to(dev)
+    W = (torch.ones((n, m), dtype=torch.float64, device=dev) if data.weights is None
+         else torch.from_numpy(np.asarray(data.weights, dtype=float)).to(dev))
+    return Y, mask, torch.where(mask, W, torch.zeros_like(W))
+
+
+def _xlogy_ratio(y, mu):
+    import torch
+    return torch.where(y == 0, torch.zeros_like(y), y * torch.log(y / mu))
+
+
+def _dev0(kind, alpha, y, mu):
+    """Unit deviance without weights (families.py:362-363, 422-425)."""
+    import torch
+    if kind == "poisson":
+        return 2.0 * (_xlogy_ratio(y, mu) - (y - mu))
+    return 2.0 * (_xlogy_ratio(y, mu) - (y + alpha) * torch.log1p((y - mu) / (mu + alpha)))
+
+
+def _derivs(kind, alpha, y, eta, w):
+    """Log-link dotD / ddotD with phi = 1 (_core.pyx:79-103)."""
+    import torch
+    mu = torch.exp(eta)
+    r = y - mu
+    if kind == "poisson":
+        return -w * r, w * mu
+    inv = 1.0 / (1.0 + mu / alpha)
+    return -w * r * inv, w * mu * inv
+
+
+def _batched_deviance(kind, alpha, y, w, eta):
+    """Per-problem weighted deviance (glm.py:27-33): NaN-safe at dropped entries."""
+    import torch
+    mu = torch.exp(eta)
+    dev = _dev0(kind, alpha, y, mu)
+    return torch.where(w > 0, w * dev, torch.zeros_like(dev)).sum(0)
+
+
+def fit_glm_batched(y, w, design, kind, alpha, offset=None, coef0=None, damping=1e-8,
+                    max_iter=50, tol=1e-10, max_halvings=12):
+    """Batched penalized Fisher scoring for the m column GLMs of y (n x m) on a
+    shared design (glm.py:68-133; lam = 0), all problems on the GPU at once:
+    eta, the derivatives and the deviances are n x m device arrays, the m
+    (p x p) Fisher systems one batched solve.  Returns (coef (m, p), converged)."""
+    import torch
+    n, m = y.shape
+    p = design.shape[1]
+    dev_ = y.device
+    if p == 0:
+        return torch.zeros((m, 0), dtype=torch.float64, device=dev_), torch.ones(m, dtype=torch.bool, device=dev_)
+    off = torch.zeros_like(y) if offset is None else offset
+    coef = torch.zeros((m, p), dtype=torch.float64, device=dev_) if coef0 is None else coef0.clone()
+    eye = damping * torch.eye(p, dtype=torch.float64, device=dev_)
+    keep = w > 0
+
+    def deviance(c):
+        return _batched_deviance(kind, alpha, y, w, design @ c.T + off)
+
+    dev = deviance(coef)
+    active = torch.ones(m, dtype=torch.bool, device=dev_)
+    converged = torch.zeros(m, dtype=torch.bool, device=dev_)
+    for _ in range(max_iter):
+        eta = design @ coef.T + off
+        dotd, ddotd = _derivs(kind, alpha, y, eta, w)
+        dotd = torch.where(keep, dotd, torch.zeros_like(dotd))
+        ddotd = torch.where(keep, ddotd, torch.zeros_like(ddotd))
+        grad = dotd.T @ design
+        hess = torch.einsum("ip,ij,iq->jpq", design, ddotd, design) + eye
+        delta = -torch.linalg.solve(hess, grad[:, :, None])[:, :, 0]
+        delta[~active] = 0.0
+        step = torch.ones(m, dtype=torch.float64, device=dev_)
+        cand = coef + step[:, None] * delta
+        dev_new = deviance(cand)
+        for _ in range(max_halvings):
+            bad = active & (~torch.isfinite(dev_new) | (dev_new > dev + 1e-8))
+            if not bool(bad.any()):
+                break
+            step = torch.where(bad, step * 0.5, step)
+            cand = torch.where(bad[:, None], coef + step[:, None] * delta, cand)
+            dev_new = torch.where(bad, deviance(cand), dev_new)
+        still_bad = active & ~torch.isfinite(dev_new)
+        if bool(still_bad.any()):
+            cand = torch.where(still_bad[:, None], coef, cand)
+            dev_new = torch.where(still_bad, dev, dev_new)
+            active = active & ~still_bad
+        moved = (cand - coef).abs().amax(1)
+        scale = 1.0 + coef.abs().amax(1)
+        coef = cand
+        done = active & (moved < tol * scale)
+        converged = converged | done
+        active = active & ~done
+        dev = torch.where(torch.isfinite(dev_new), dev_new, dev)
+        if not bool(active.any()):
+            break
+    return coef, converged
+
+
+def _ols_stage_dense(y_eps, w, design, offset):
+    """One exact Gaussian/identity Fisher step (initialization.py:137-141)."""
+    import torch
+    p = design.shape[1]
+    if p == 0:
+        return torch.zeros((y_eps.shape[1], 0), dtype=torch.float64, device=y_eps.device)
+    r = y_eps - (0.0 if offset is None else offset)
+    grad = -(w * r).T @ design
+    hess = torch.einsum("ip,ij,iq->jpq", design, w, design) + \
+        _DAMPING * torch.eye(p, dtype=torch.float64, device=y_eps.device)
+    return -torch.linalg.solve(hess, grad[:, :, None])[:, :, 0]
+
+
+def _glm_or_fallback(y, w, design, kind, alpha, offset, coef_fallback, info, label):
+    """initialization.py:123-134: non-converged problems keep the OLS seed."""
+    import torch
+    coef, conv = fit_glm_batched(y, w, design, kind, alpha, offset=offset, coef0=coef_fallback)
+    bad = ~conv
+    if bool(bad.any()):
+        coef = torch.where(bad[:, None], coef_fallback, coef)
+        info.setdefault("glm_fallbacks", {})[label] = int(bad.sum().item())
+    return coef
+
+
+def randomized_svd_dense(a, k, oversample=10, n_power=2, seed=0):
+    """randomized_svd (initialization.py:62-82) of a dense device matrix, the
+    reference's probe replayed from numpy's generator."""
+    import torch
+    n, m = a.shape
+    k = min(k, min(n, m))
+    dev_ = a.device
+    if k == 0:
+        z = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev_)
+        return z(n, 0), z(0), z(m, 0)
+    if k + oversample >= min(n, m):
+        u, s, vt = torch.linalg.svd(a, full_matrices=False)
+        return u[:, :k], s[:k], vt[:k].T
+    rng = np.random.default_rng(seed)
+    probe = torch.from_numpy(rng.standard_normal((m, k + oversample))).to(dev_)
+    sketch = a @ probe
+    for _ in range(n_power):
+        q, _ = torch.linalg.qr(sketch)
+        sketch = a @ (a.T @ q)
+    q, _ = torch.linalg.qr(sketch)
+    u_small, s, vt = torch.linalg.svd(q.T @ a, full_matrices=False)
+    return (q @ u_small)[:, :k], s[:k], vt[:k].T
+
+
+def init_glm_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
+                 method: InitMethod | None = None, seed: int = 0, return_info: bool = False,
+                 *, device=None):
+    """GLM-based initialization (initialization.py:172-214) on the GPU: column
+    GLMs for B, row GLMs for Gamma given the column effects, the deviance (or
+    Pearson) residual SVD for U, column GLMs on U for V -- every batched GLM a
+    set of n x m device arrays and one batched (p x p) solve per Fisher step;
+    non-converged problems fall back to their OLS seeds as in the reference.
+    Handles unobserved entries and prior weights (zero weight at holes).
+    Scope: Poisson / negative binomial with the log link (the fit's device
+    scope); returns a host state."""
+    import torch
+    method = method or InitMethod()
+    n, m = data.shape
+    if d > min(n, m):
+        raise ConfigError("rank d cannot exceed min(n, m)")
+    if fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log":
+        raise _lib.UnsupportedError(
+            f"device initialization implements poisson/neg_binomial with log link, "
+            f"got {fam.kind}+{lnk.kind}")
+    _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       int(str(device).split(":")[-1]))
+    kind = fam.kind
+    alpha = float(getattr(fam, "nb_shape", 1.0))
+    eps = method.eps_for(lnk)
+    Y, mask, W = _dense_inputs(data, dev)
+    y_safe = torch.where(mask, Y, torch.ones_like(Y))          # _safe_y: fill 1.0
+    y_eps = torch.log(y_safe + eps)                            # perturbed_transform (log)
+    X = torch.from_numpy(np.ascontiguousarray(covs.x, dtype=float)).to(dev)
+    Z = torch.from_numpy(np.ascontiguousarray(covs.z, dtype=float)).to(dev)
+    p, q = X.shape[1], Z.shape[1]
+    info = {"method": "glm_svd"}
+
+    # stage 1: column regressions for B
+    b = _ols_stage_dense(y_eps, W, X, None)
+    if p:
+        b = _glm_or_fallback(y_safe, W, X, kind, alpha, None, b, info, "b")
+    offset = X @ b.T
+    # stage 2: row regressions for Gamma given the column effects
+    gamma = _ols_stage_dense(y_eps.T, W.T, Z, offset.T)
+    if q:
+        gamma = _glm_or_fallback(y_safe.T.contiguous(), W.T.contiguous(), Z, kind, alpha,
+                                 offset.T.contiguous(), gamma, info, "gamma")
+    eta0 = offset + (gamma @ Z.T if q else 0.0)
+    mu0 = torch.exp(torch.clamp(eta0, *_ETA_CLIP_LOG))
+    # stage 3: residual SVD for the latent scores (initialization.py:103-114)
+    if method.residual_kind == "pearson":
+        var = mu0 if kind == "poisson" else mu0 * (1.0 + mu0 / alpha)
+        r = (Y - mu0) * torch.sqrt(W / var)
+    else:
+        ud = W * _dev0(kind, alpha, Y, mu0)
+        r = torch.sign(Y - mu0) * torch.sqrt(torch.clamp(ud, min=0.0))
+    resid = torch.where(mask, r, torch.zeros_like(r))
+    left, sing, right = randomized_svd_dense(resid, d, seed=seed)
+    u = left * sing
+    # stage 4: column regressions for V with U as the design
+    if d > 0:
+        v0 = _ols_stage_dense(torch.where(mask, y_eps - eta0, torch.zeros_like(Y)), W, u, None)
+        v = _glm_or_fallback(y_safe, W, u, kind, alpha, eta0, v0, info, "v")
+    else:
+        v = torch.zeros((m, 0), dtype=torch.float64, device=dev)
+    nb_shape = 1.0
+    if kind == "neg_binomial":      # initialization.py:93-100 at mu0
+        num = float((torch.where(mask, W * mu0 ** 2, torch.zeros_like(Y))).sum().item())
+        den = float((torch.where(mask, W * ((Y - mu0) ** 2 - mu0), torch.zeros_like(Y))).sum().item())
+        nb_shape = 1e8 if den <= 0 else float(np.clip(num / den, 1e-4, 1e8))
+    host = lambda t: t.cpu().numpy()
+    state = FactorizationState(host(b), host(gamma), host(u), host(v), 1.0, nb_shape)
     return (state, info) if return_info else state

@@ -197,13 +197,11 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
     used when m <= 65536 and counts <= 65535.
     """
     started = time.perf_counter()
-    if init_state is None:
+    if init_state is None:   # optim.py:359-366: the GLM-SVD start
         if rank is None:
             raise ConfigError("pass init_state or rank")
-        raise _lib.UnsupportedError(
-            "the reference's default initialization (init_glm_svd, initialization.py:172-214) "
-            "is not on the device path; pass init_state (e.g. from "
-            "paper_2412_20509_b200.initialization.init_ols_svd)")
+        from .initialization import init_glm_svd
+        init_state = init_glm_svd(data, covs, fam, lnk, rank, seed=cfg.seed, device=device)
     init_state.check_shapes(data, covs)
     est_phi, est_alpha = _resolve_dispersion(fam, dispersion)
     if est_phi:

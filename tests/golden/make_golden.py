@@ -448,6 +448,46 @@ def make_init():
     return out
 
 
+def make_init_glm():
+    """init_glm_svd of the reference (initialization.py:172-214): Poisson / NB,
+    covariates on both sides, a masked and weighted case, the Pearson residual
+    kind, and the exact-SVD fallback."""
+    out = {}
+    cases = [("pois", gk.Poisson(), 300, 80, 2, 1, 4, False, False, "deviance"),
+             ("nb", gk.NegBinomial(2.0), 400, 60, 1, 1, 5, False, False, "deviance"),
+             ("masked", gk.NegBinomial(1.3), 350, 70, 2, 0, 3, True, True, "deviance"),
+             ("pearson", gk.Poisson(), 250, 50, 1, 0, 3, False, False, "pearson"),
+             ("small", gk.NegBinomial(1.0), 30, 12, 1, 0, 3, False, False, "deviance")]
+    for k, (key, fam, n, m, p, q, d, masked, weighted, rk) in enumerate(cases):
+        y, x, z, off, init = _nb_problem(n, m, max(p, 1), q, d, 91 + k, False)
+        x = x[:, :p]
+        rng = np.random.default_rng(191 + k)
+        mask = rng.uniform(size=y.shape) > 0.15 if masked else None
+        w = rng.uniform(0.5, 2.0, size=y.shape) if weighted else None
+        yv = y.astype(float) if mask is None else np.where(mask, y, np.nan)
+        data = gk.ResponseMatrix(yv, mask=mask, weights=w)
+        covs = gk.CovariateSet(x=x, z=z)
+        st, info = gk.init_glm_svd(data, covs, fam, gk.Log(), d, seed=3, return_info=True,
+                                   method=gk.InitMethod(residual_kind=rk))
+        out[f"{key}|y"] = y
+        out[f"{key}|x"] = x
+        out[f"{key}|z"] = z
+        out[f"{key}|d"] = np.int64(d)
+        out[f"{key}|fam"] = np.asarray(fam.kind)
+        out[f"{key}|alpha"] = np.float64(getattr(fam, "nb_shape", 1.0))
+        out[f"{key}|rk"] = np.asarray(rk)
+        if mask is not None:
+            out[f"{key}|mask"] = mask
+        if w is not None:
+            out[f"{key}|w"] = w
+        out[f"{key}|b"] = st.b
+        out[f"{key}|gamma"] = st.gamma
+        out[f"{key}|uv"] = st.u @ st.v.T
+        out[f"{key}|nb_shape"] = np.float64(st.nb_shape)
+        out[f"{key}|fallbacks"] = np.asarray(str(info.get("glm_fallbacks", {})))
+    return out
+
+
 def make_mm():
     """MatrixMarket files and the reference's dense reads of them
     (io.py:96-109); the files themselves are fixtures under golden/mm/."""
@@ -512,7 +552,7 @@ def main():
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,
               "project_b23": make_project_b23, "c2": make_c2, "masked": make_masked,
-              "masked_p3": make_masked_p3}
+              "masked_p3": make_masked_p3, "init_glm": make_init_glm}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
