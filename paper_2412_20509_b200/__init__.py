@@ -17,7 +17,13 @@ from .gradients import GradientPair, Minibatch, full_gradients, minibatch_gradie
 from .identify import check_constraints, project_constraints  # noqa: F401
 from .model import (CovariateSet, FactorizationState, PenaltyConfig, ResponseMatrix,  # noqa: F401
                     parameter_count, penalty_value)
-from .optim import (FitReport, SgdConfig, bias_correction, fit_asgd, learning_rate,  # noqa: F401
-                    penalized_objective, smooth_update)
+from .optim import (FitReport, SgdConfig, bias_correction, fit_asgd, impute_block,  # noqa: F401
+                    learning_rate, linear_predictor, penalized_objective, smooth_update,
+                    update_nb_shape_stochastic)
+from .initialization import InitMethod, init_glm_svd, init_ols_svd  # noqa: F401
+from .metrics import EvalResult, rel_deviance, rel_log_rmse  # noqa: F401
+from .select import (RankSelectionReport, cv_rank_select, elbow_pick, holdout_mask,  # noqa: F401
+                     information_criteria, residual_scores, scree_eigenvalues)
+from .io import read_matrix_market, read_matrix_market_csr  # noqa: F401
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -342,3 +342,100 @@ def penalized_objective(state, data, covs, fam, lnk, penalty, *, offset=None, dt
     """Masked half-deviance + penalty (model.py:268-276), deviance on the GPU."""
     state.check_shapes(data, covs)
     return _full_objective(state, data, covs, fam, lnk, penalty, offset, dtype, device)
+
+
+# ---------------------------------------------------------------------------
+# block helpers of the reference's public API (model.py:229-256,
+# optim.py:205-245), evaluated on the GPU
+# ---------------------------------------------------------------------------
+
+def _dev_index(device):
+    import torch
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device() if device is None else
+                        int(str(device).split(":")[-1]))
+
+
+def _eta_block_device(state, covs, rows, cols, dev, offset=None):
+    """eta for rows x cols as a device fp64 array, U V' first (BLAS order of
+    model.py:251-255), then X B', then Gamma Z'."""
+    import torch
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=float)).to(dev)
+    ri = slice(None) if rows is None else np.asarray(rows)
+    ci = slice(None) if cols is None else np.asarray(cols)
+    eta = t(state.u[ri]) @ t(state.v[ci]).T
+    if covs.p:
+        eta = eta + t(covs.x[ri]) @ t(state.b[ci]).T
+    if covs.q:
+        eta = eta + t(state.gamma[ri]) @ t(covs.z[ci]).T
+    if offset is not None:
+        eta = eta + t(np.asarray(offset, dtype=float)[ri])[:, None]
+    return eta
+
+
+def linear_predictor(state: FactorizationState, covs, rows=None, cols=None, *, offset=None,
+                     device=None) -> np.ndarray:
+    """eta block for the requested rows x cols (model.py:229-256), on the GPU."""
+    n, m = state.n, state.m
+    if rows is not None:
+        rows = np.asarray(rows)
+        if rows.size and (rows.min() < -n or rows.max() >= n):
+            raise IndexError(f"row index out of range for n={n}")
+    if cols is not None:
+        cols = np.asarray(cols)
+        if cols.size and (cols.min() < -m or cols.max() >= m):
+            raise IndexError(f"column index out of range for m={m}")
+    return _eta_block_device(state, covs, rows, cols, _dev_index(device), offset).cpu().numpy()
+
+
+def impute_block(state: FactorizationState, data, covs, lnk, mb, *, offset=None,
+                 device=None) -> np.ndarray:
+    """Working copy of the Y block with unobserved entries set to mu
+    (optim.py:232-245); observed entries untouched."""
+    import torch
+    if lnk.kind != "log":
+        raise _lib.UnsupportedError(f"device imputation implements the log link, got {lnk.kind}")
+    I, J = np.asarray(mb.row_idx), np.asarray(mb.col_idx)
+    ix = np.ix_(I, J)
+    block = np.array(data.dense()[ix], copy=True)
+    if data.csr is None:
+        miss = ~data.mask[ix]
+        if miss.any():
+            dev = _dev_index(device)
+            mu = torch.exp(_eta_block_device(state, covs, I, J, dev, offset)).cpu().numpy()
+            block[miss] = mu[miss]
+    return block
+
+
+def update_nb_shape_stochastic(state: FactorizationState, data, mb, rate: float,
+                               floor: float = 1e-4, covs=None, lnk=None, y_block=None,
+                               mu_block=None, ceiling: float = 1e8, *, offset=None,
+                               device=None) -> float:
+    """Smoothed stochastic moment update of the NB shape (optim.py:205-229):
+    alpha_hat = sum w mu^2 / sum w ((y - mu)^2 - mu) on the block (ceiling when
+    the denominator is not positive), clipped to [floor, ceiling]; the sums
+    run on the GPU in fp64."""
+    import torch
+    I, J = np.asarray(mb.row_idx), np.asarray(mb.col_idx)
+    ix = np.ix_(I, J)
+    dev = _dev_index(device)
+    if mu_block is None:
+        if lnk is None or covs is None:
+            raise ConfigError("mu_block or (covs, lnk) needed")
+        mu = torch.exp(_eta_block_device(state, covs, I, J, dev, offset))
+    else:
+        mu = torch.from_numpy(np.asarray(mu_block, dtype=float)).to(dev)
+    if y_block is None:
+        vals = data.dense()[ix]
+        y_np = vals if data.csr is not None else np.where(data.mask[ix], vals, np.nan)
+        y = torch.from_numpy(np.asarray(y_np, dtype=float)).to(dev)
+        y = torch.where(torch.isnan(y), mu, y)
+    else:
+        y = torch.from_numpy(np.asarray(y_block, dtype=float)).to(dev)
+    w = (torch.ones_like(mu) if data.weights is None else
+         torch.from_numpy(np.asarray(data.weights[ix], dtype=float)).to(dev))
+    num = float((w * mu ** 2).sum().item())
+    den = float((w * ((y - mu) ** 2 - mu)).sum().item())
+    ah = num / den if den > 0 else ceiling
+    ah = min(max(floor, ah), ceiling)
+    return (1.0 - rate) * state.nb_shape + rate * ah

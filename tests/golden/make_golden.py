@@ -488,6 +488,44 @@ def make_init_glm():
     return out
 
 
+def make_cv():
+    """cv_rank_select of the reference (select.py:148-237): two folds of 30 %
+    holdouts fitted (imputed holes, GLM-SVD start, warm starts over ranks),
+    AIC/BIC, held-out relative deviance, the scree pick (select.py:240-294)."""
+    y, x, z, _, _ = _nb_problem(240, 50, 1, 0, 2, 131, False)
+    data = gk.ResponseMatrix(y.astype(float))
+    covs = gk.CovariateSet(x=x, m=50)
+    cfg = gk.SgdConfig(max_epochs=20, mb_rows=60, mb_cols=50, tol=1e-30, seed=1)
+    rep = gk.cv_rank_select(data, covs, gk.NegBinomial(1.5), gk.Log(), [1, 2, 3], folds=2, cfg=cfg,
+                            seed=5)
+    scree = gk.scree_eigenvalues(data, covs, 4)
+    return {"y": y, "x": x, "aic": np.asarray(rep.aic), "bic": np.asarray(rep.bic),
+            "cv": np.asarray(rep.cv_deviance), "scree": np.asarray(rep.scree_eigenvalues),
+            "scree4": np.asarray(scree), "failures": np.asarray(str(rep.failures)),
+            "chosen": np.asarray([rep.chosen["cv"], rep.chosen["aic"], rep.chosen["bic"],
+                                  rep.chosen["scree"]])}
+
+
+def make_api():
+    """Block helpers of the public API: linear_predictor (model.py:229-256),
+    impute_block (optim.py:232-245), update_nb_shape_stochastic (205-229)."""
+    y, x, z, _, init = _nb_problem(120, 30, 2, 1, 3, 141, False)
+    mask = np.random.default_rng(142).uniform(size=y.shape) > 0.2
+    w = np.random.default_rng(143).uniform(0.5, 2.0, size=y.shape)
+    data = gk.ResponseMatrix(np.where(mask, y, np.nan), mask=mask, weights=w)
+    covs = gk.CovariateSet(x=x, z=z)
+    st = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], 1.0, 1.5)
+    I, J = np.array([3, 7, 8, 50, 99]), np.array([0, 4, 5, 29])
+    mb = gk.Minibatch(I, J)
+    eta = gk.linear_predictor(st, covs, I, J)
+    eta_all = gk.linear_predictor(st, covs)
+    blk = gk.impute_block(st, data, covs, gk.Log(), mb)
+    nb = gk.update_nb_shape_stochastic(st, data, mb, 0.3, covs=covs, lnk=gk.Log())
+    return {"y": y, "x": x, "z": z, "mask": mask, "w": w, "I": I, "J": J, "eta": eta,
+            "eta_all": eta_all, "block": blk, "nb": np.float64(nb),
+            **_state_arrays("st", st)}
+
+
 def make_mm():
     """MatrixMarket files and the reference's dense reads of them
     (io.py:96-109); the files themselves are fixtures under golden/mm/."""
@@ -552,7 +590,8 @@ def main():
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,
               "project_b23": make_project_b23, "c2": make_c2, "masked": make_masked,
-              "masked_p3": make_masked_p3, "init_glm": make_init_glm}
+              "masked_p3": make_masked_p3, "init_glm": make_init_glm, "cv": make_cv,
+              "api": make_api}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
