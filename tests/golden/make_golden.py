@@ -526,6 +526,35 @@ def make_api():
             **_state_arrays("st", st)}
 
 
+def make_cli():
+    """The reference CLI end to end (cli.py:151-201, 204-253): `fit` (GLM-SVD
+    start, aSGD, B1) and `cv --criterion scree` on a small CSV."""
+    import tempfile
+    from gmfkit import cli as gcli
+    from gmfkit import io as gio
+    y, x, z, _, _ = _nb_problem(160, 40, 1, 0, 2, 151, False)
+    out = {"y": y}
+    with tempfile.TemporaryDirectory() as tmp:
+        ycsv = os.path.join(tmp, "y.csv")
+        gio.write_dense_csv(ycsv, y.astype(float))
+        rc = gcli.main(["fit", "--y", ycsv, "--rank", "2", "--family", "neg_binomial",
+                        "--nb-shape", "1.5", "--max-epochs", "15", "--mb-rows", "40",
+                        "--mb-cols", "40", "--tol", "1e-30", "--out", os.path.join(tmp, "fit")])
+        out["fit_rc"] = np.int64(rc)
+        for name in ("U", "V"):
+            out[name] = gio.read_dense_csv(os.path.join(tmp, "fit", f"{name}.csv"))[0]
+        rep = gio.read_json(os.path.join(tmp, "fit", "fit_report.json"))
+        out["trace"] = np.asarray(rep["objective_trace"])
+        out["final_objective"] = np.float64(rep["final_objective"])
+        rc = gcli.main(["cv", "--y", ycsv, "--ranks", "1:3", "--criterion", "scree",
+                        "--out", os.path.join(tmp, "cv")])
+        out["cv_rc"] = np.int64(rc)
+        rr = gio.read_json(os.path.join(tmp, "cv", "rank_report.json"))
+        out["scree"] = np.asarray(rr["scree_eigenvalues"])
+        out["scree_pick"] = np.int64(rr["chosen"]["scree"])
+    return out
+
+
 def make_mm():
     """MatrixMarket files and the reference's dense reads of them
     (io.py:96-109); the files themselves are fixtures under golden/mm/."""
@@ -591,7 +620,7 @@ def main():
               "select": make_select, "init": make_init, "mm": make_mm,
               "project_b23": make_project_b23, "c2": make_c2, "masked": make_masked,
               "masked_p3": make_masked_p3, "init_glm": make_init_glm, "cv": make_cv,
-              "api": make_api}
+              "api": make_api, "cli": make_cli}
     only = sys.argv[1:] or list(makers)
     for name in only:
         arrs = makers[name]()
