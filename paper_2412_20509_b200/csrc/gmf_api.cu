@@ -27,6 +27,7 @@ int launch_tcsr(const Params& P, const int32_t* tidx, int32_t* lens, int64_t* tp
 int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
 int set_mbar_sleep(int on);
+int blocknorm_segments(int64_t nstar_max);
 int64_t rimg_bytes_of(int NK);
 int set_k1_dbg(int v);
 int64_t grad_smem_bytes(const Params& P, int dtype, int NK);
@@ -368,6 +369,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_objp = take(cta_max * OBJ_W * 8);
   const int64_t o_rnp = take(cta_max * 2 * 8);
   const int64_t o_bs = take(R * 2 * 8);
+  const int64_t o_bnp = take(R * (int64_t)blocknorm_segments(nstar_max) * 2 * 8);
   const int64_t o_lm = take(R * 8);
   const int64_t o_rho = take(ms * 8);
   const int64_t o_alp = take(ms * 8);
@@ -414,6 +416,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.totals = (double*)(base + o_tot);
   P.ready = (const unsigned long long*)(base + o_ready);
   P.blocksum = (double*)(base + o_bs);
+  P.bnpart = (double*)(base + o_bnp);
   P.snap_ver = (long long*)(base + o_lm);
   P.rho_tab = (double*)(base + o_rho);
   P.alpt_tab = (double*)(base + o_alp);
@@ -576,7 +579,7 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
   int rc = launch_blocknorm(P, h->desc.dtype, st);
   if (!rc) rc = launch_cache_fill(P, h->desc.dtype, st);   // the per-step path's objective caches
   if (rc) return rc;
-  h->launches += 2;
+  h->launches += 3;
   GMF_CUDA(cudaStreamSynchronize(st));
   if (P.tcm == 1 && h->fit_grid > 0 && !h->residency_checked) {
     // the tensor-core fit kernel synchronises with a software grid barrier:

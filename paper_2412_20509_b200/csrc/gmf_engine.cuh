@@ -132,6 +132,7 @@ struct Params {
   double* rnpart;      // [n_row_ctas][2]
   double* cnpart;      // [fit CTAs][2] column-norm partials (persistent kernel)
   double* blocksum;    // [R][2] (gamma, u) squared norms per row block
+  double* bnpart;      // [R][segments][2] partials of k_blocknorm
   // Divergence snapshots are copy-on-write: snap_ver[r] is the snapshot
   // period in which block r's pre-snapshot rows were saved to sn_row.  The
   // snapshot of period k is sn_row for blocks with snap_ver == k and the

@@ -237,19 +237,50 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
 }
 
 // per-block squared row norms (gamma part, u part), one CTA per block
+// ||Gamma_r||^2 and ||U_r||^2 of every row block r (the per-block sums the
+// tracked objective's penalty is kept in): grid (segments, blocks), each CTA
+// a fixed segment of kBnRows rows (a thread per row, no division per
+// element), its partials reduced in fixed segment order by k_blocknorm_fin
+constexpr int kBnRows = 2048;
+
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_blocknorm(Params P) {
+__global__ void __launch_bounds__(kThreads) k_blocknorm(Params P, double* part, int nseg) {
   __shared__ double scr[kThreads / 32];
-  const int64_t r = blockIdx.x;
+  const int64_t r = blockIdx.y, sg = blockIdx.x;
   const T* th = tptr<T>(P.th_row);
-  const int64_t a = P.rbp[r] * P.Kr, b = P.rbp[r + 1] * P.Kr;
+  const int64_t r0 = P.rbp[r], r1 = P.rbp[r + 1];
+  const int64_t lo = r0 + sg * kBnRows, hi = lo + kBnRows < r1 ? lo + kBnRows : r1;
+  const int Kr = P.Kr, q = P.q;
   double ng = 0.0, nu = 0.0;
-  for (int64_t e = a + threadIdx.x; e < b; e += kThreads) {
-    const double v = (double)th[e];
-    if ((int)(e % P.Kr) < P.q) ng += v * v; else nu += v * v;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+    const T* row = th + i * Kr;
+    for (int k = 0; k < Kr; ++k) {
+      const double v = (double)row[k];
+      if (k < q) ng += v * v; else nu += v * v;
+    }
   }
   ng = block_sum<kThreads>(ng, scr);
   nu = block_sum<kThreads>(nu, scr);
+  if (threadIdx.x == 0) {
+    part[2 * (r * nseg + sg)] = ng;
+    part[2 * (r * nseg + sg) + 1] = nu;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_blocknorm_fin(Params P, const double* part, int nseg) {
+  const int64_t r = blockIdx.x;
+  const int64_t nrows = P.rbp[r + 1] - P.rbp[r];
+  const int used = (int)((nrows + kBnRows - 1) / kBnRows);
+  double ng = 0.0, nu = 0.0;
+  for (int sg = threadIdx.x; sg < used; sg += 32) {
+    ng += part[2 * (r * nseg + sg)];
+    nu += part[2 * (r * nseg + sg) + 1];
+  }
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ng += __shfl_xor_sync(0xffffffffu, ng, o);
+    nu += __shfl_xor_sync(0xffffffffu, nu, o);
+  }
   if (threadIdx.x == 0) { P.blocksum[2 * r] = ng; P.blocksum[2 * r + 1] = nu; }
 }
 
@@ -539,11 +570,20 @@ int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t 
   return GMF_OK;
 }
 
+int blocknorm_segments(int64_t nstar_max) {
+  const int64_t s = (nstar_max + kBnRows - 1) / kBnRows;
+  return (int)(s > 0 ? s : 1);
+}
+
 int launch_blocknorm(const Params& P, int dtype, cudaStream_t st) {
   if (P.R <= 0) return GMF_OK;
-  if (dtype == GMF_F64) k_blocknorm<double><<<(unsigned)P.R, kThreads, 0, st>>>(P);
-  else k_blocknorm<float><<<(unsigned)P.R, kThreads, 0, st>>>(P);
+  const int nseg = blocknorm_segments(P.nstar_max);
+  const dim3 grid((unsigned)nseg, (unsigned)P.R);
+  if (dtype == GMF_F64) k_blocknorm<double><<<grid, kThreads, 0, st>>>(P, P.bnpart, nseg);
+  else k_blocknorm<float><<<grid, kThreads, 0, st>>>(P, P.bnpart, nseg);
   GMF_LAUNCH_CHECK("k_blocknorm");
+  k_blocknorm_fin<<<(unsigned)P.R, 32, 0, st>>>(P, P.bnpart, nseg);
+  GMF_LAUNCH_CHECK("k_blocknorm_fin");
   return GMF_OK;
 }
 

@@ -160,6 +160,28 @@ class _Exchange:
             dist.all_gather_into_tensor(self.gathered, self.rec, group=self.group)
         fit.step_apply(self.gathered)
 
+    def graph(self, k):
+        """k steps (objective, K1, record copy, NCCL all-gather, fixed-order
+        apply) captured as ONE CUDA graph, replayed without a per-step host
+        loop; the kernels read the step index from the device control block,
+        so replays advance the fit and turn into no-ops once it stopped.
+        Device (NCCL) exchange only; built on first use, after one eager step
+        has warmed the communicator."""
+        torch = self.torch
+        g = self.graphs.get(k) if hasattr(self, "graphs") else None
+        if g is None:
+            if not hasattr(self, "graphs"):
+                self.graphs = {}
+            side = torch.cuda.Stream(self.fit.device)
+            side.wait_stream(torch.cuda.current_stream(self.fit.device))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                for _ in range(k):
+                    self.step()
+            torch.cuda.current_stream(self.fit.device).wait_stream(side)
+            self.graphs[k] = g
+        g.replay()
+
 
 def _gather_rows(fit: DeviceFit, tensor, group, mode):
     """Global (n x k) host array of a row-sharded device tensor, original order."""
@@ -285,17 +307,31 @@ def _gathered_state(fit: DeviceFit, group, exchange, nb_shape, snapshot=False):
                               tc[:, p:].copy(), fit.phi, nb_shape)
 
 
+# multi-rank driver knobs: per-step records exchanged inside captured CUDA
+# graphs of _GRAPH_STEPS steps (device / NCCL exchange); _FORCE_EXCHANGE runs
+# the exchange path for a one-rank group too (tests of the multi-rank path on
+# a single GPU)
+_GRAPH_EXCHANGE = True
+_GRAPH_STEPS = 32
+_FORCE_EXCHANGE = False
+
+
 def _drive(fit: DeviceFit, callback, group, exchange):
     """Run steps until the device tracker stops (converged / diverged /
     max_epochs); the host only polls the status word between chunks."""
     total = fit.schedule.max_steps + 1          # + the final tracking pass
-    if fit.world > 1:
+    if fit.world > 1 or (_FORCE_EXCHANGE and group is not None):
         ex = _Exchange(fit, group, exchange)
         t = 0
+        use_graph = exchange == "device" and callback is None and _GRAPH_EXCHANGE
         while True:
             prev = t
-            ex.step()
-            t += 1
+            if use_graph and t > 0 and t + _GRAPH_STEPS <= total:
+                ex.graph(_GRAPH_STEPS)   # 32 steps per launch, status polled between
+                t += _GRAPH_STEPS
+            else:
+                ex.step()
+                t += 1
             if callback is not None or t % 32 == 0 or t >= total:
                 st = fit.status()
                 if callback is not None and st.t > prev:
