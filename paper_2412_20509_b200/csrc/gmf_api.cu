@@ -26,10 +26,8 @@ int launch_tcsr(const Params& P, const int32_t* tidx, int32_t* lens, int64_t* tp
                 unsigned int* too_big, cudaStream_t st);
 int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
-int set_mbar_sleep(int on);
 int blocknorm_segments(int64_t nstar_max);
 int64_t rimg_bytes_of(int NK);
-int set_k1_dbg(int v);
 int64_t grad_smem_bytes(const Params& P, int dtype, int NK);
 int launch_obj(const Params& P, int dtype, cudaStream_t st);
 int launch_apply(const Params& P, int dtype, const void* gathered, cudaStream_t st);
@@ -228,8 +226,6 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   GMF_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, desc->device));
   int smem_optin = 0;
   GMF_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device));
-  if (getenv("GMF_MBAR_SLEEP")) set_mbar_sleep(atoi(getenv("GMF_MBAR_SLEEP")));
-  if (getenv("GMF_K1_DBG")) set_k1_dbg(atoi(getenv("GMF_K1_DBG")));
   // K1 generation on the tensor cores: v2 (warp-specialized, one CTA per SM)
   // pays off once its units are deep pipelines (>= 8 chunks of 64 rows, e.g.
   // BASELINE c5's 65,536-row blocks); shallow units (c3, c4: 135-270 rows per

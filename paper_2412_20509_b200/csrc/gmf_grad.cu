@@ -901,17 +901,7 @@ static void* kernel_for(int dtype, int family, int NK, bool fit, int tcm) {
 
 static int k1_threads(int tcm) { return tcm == 2 ? tc2::NT : kThreads; }
 
-// experiment switch (GMF_MBAR_SLEEP=1): K1 v2 mbarrier waits with a suspend-time hint
-int set_mbar_sleep(int on) {
-  GMF_CUDA(cudaMemcpyToSymbol(tc2::g_mbar_sleep, &on, sizeof(int)));
-  return GMF_OK;
-}
 int64_t rimg_bytes_of(int NK) { return tc2::rimg_bytes(NK); }
-
-int set_k1_dbg(int v) {
-  GMF_CUDA(cudaMemcpyToSymbol(tc2::g_k1_dbg, &v, sizeof(int)));
-  return GMF_OK;
-}
 
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA, int holes) {
   return dtype == GMF_F32 && !has_w && !holes && Kr <= 16 && Kc <= 16 && KA <= 32;

@@ -257,32 +257,19 @@ GMF_D void mbar_arrive(uint64_t* bar) {
 }
 
 // mbarrier phase wait with a hang guard: a protocol error traps (the launch
-// fails with an error) instead of spinning forever
-__device__ int g_mbar_sleep;   // experiment switch: suspend-time hint on mbarrier waits
-__device__ int g_k1_dbg;       // experiment switch: bit 0 skip GEMM2/3, bit 1 skip GEMM1 splits
-
+// fails with an error) instead of spinning forever.  No global state is read
+// here: a __device__ switch consulted per wait costs the single-thread roles
+// (MMA issuer, loader) a dependent global load each time.
 GMF_D void mbar_wait(uint64_t* bar, uint32_t parity) {
-  // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
-  // the phase completes instead of spinning on the issue slots the producer
-  // and MMA warps of its scheduler need
   uint32_t done = 0;
   unsigned long long t0 = 0;
-  const int sleep = g_mbar_sleep;
   for (;;) {
-    if (sleep)
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}\n"
-          : "=r"(done)
-          : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
-          : "memory");
-    else
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}\n"
-          : "=r"(done)
-          : "r"(smem_addr(bar)), "r"(parity)
-          : "memory");
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
     if (done) break;
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -924,13 +911,11 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
             const uint64_t b1 = sdesc(sb + (uint32_t)L.B1 + b1sz + kb, 128, sbo1);
             const uint64_t b2 = sdesc(sb + (uint32_t)L.B1 + 2 * b1sz + kb, 128, sbo1);
             umma(d, a0, b0, ID1, kt > 0 ? 1u : 0u);
-            if (!(g_k1_dbg & 2)) {
-              umma(d, a0, b1, ID1, 1u);
-              umma(d, a1, b0, ID1, 1u);
-              umma(d, a0, b2, ID1, 1u);
-              umma(d, a1, b1, ID1, 1u);
-              umma(d, a2, b0, ID1, 1u);
-            }
+            umma(d, a0, b1, ID1, 1u);
+            umma(d, a1, b0, ID1, 1u);
+            umma(d, a0, b2, ID1, 1u);
+            umma(d, a1, b1, ID1, 1u);
+            umma(d, a2, b0, ID1, 1u);
           }
           umma_commit(&B.eta_full[slot]);
           umma_commit(&B.a1_free[a1s]);
@@ -951,7 +936,6 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
             #pragma unroll
             for (int gg = 0; gg < 2; ++gg) {
               const uint32_t pg = sb + (uint32_t)L.P + 32768u * gg;
-              if (g_k1_dbg & 4) continue;   // experiment: no GEMM2/3
               #pragma unroll
               for (int kt = 0; kt < TCC / 16; ++kt) {
                 const uint32_t ko = (uint32_t)kt * 256u;
@@ -963,7 +947,6 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
               // lo, paired with feature rows 8u..8u+7 twice (LBO 0)
               #pragma unroll
               for (int uu = 0; uu < 4; ++uu) {
-                if (g_k1_dbg & 8) break;   // experiment: no GEMM3
                 const uint32_t acc0 = (c == 0 && gg == 0 && uu == 0) ? 0u : 1u;
                 const uint32_t rg = 512u * (uint32_t)(4 * gg + uu);
                 umma(tm + T_D3, sdesc(pg + 4096u * uu, 2048, 128), sdesc(a3 + rg, 0, 128), ID3, acc0);
