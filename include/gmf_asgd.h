@@ -120,7 +120,9 @@ typedef struct gmf_desc {
   int32_t p, q, d;      /* row design X (n x p), column design Z (m x q), rank;
                            p+q+d <= 64 (fp64: <= 32)                           */
   int32_t dtype;        /* GMF_F32 | GMF_F64: parameters and block arithmetic  */
-  int32_t family, link; /* fused path: (POISSON|NEG_BINOMIAL, LOG)             */
+  int32_t family, link; /* fused count paths: (POISSON|NEG_BINOMIAL, LOG); any
+                           other pair -- and any fit that estimates phi --
+                           runs in general mode (GMF_DESC_REAL_RESPONSE)       */
   int32_t y_format;     /* gmf_yfmt                                            */
   int32_t has_offset;   /* per-row offset in eta (BASELINE extension)          */
   int32_t has_weights;  /* dense n x m prior weights (dense Y only)            */
@@ -135,6 +137,12 @@ typedef struct gmf_desc {
    ranges with TMA bulk copies of their 16-byte aligned superset; without
    the flag the handle uses the older tensor-core K1) */
 #define GMF_DESC_TAIL_PADDED 1
+/* general mode (families.py:267-441 with any link of :98-210, and the Pearson
+   dispersion of optim.py:175-202): the response is real-valued and lives in
+   gmf_buffers.y_work (n x m, compute dtype, fully observed; y_dense unused);
+   K1 runs on the CUDA cores with the family and link chosen at run time,
+   p+q+d <= 32 */
+#define GMF_DESC_REAL_RESPONSE 2
 
 typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py:193-226) */
   double rate_k0, rate_k1, rate_tau;
@@ -149,6 +157,10 @@ typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py
   int32_t snapshot_stride;       /* 4 (optim.py:309) */
   int32_t k1_impl;               /* enum gmf_k1_impl (no reference counterpart) */
   int32_t nafill_every;          /* imputation period of unobserved entries (optim.py:432) */
+  int32_t est_phi;               /* Pearson dispersion update each step (optim.py:465-468);
+                                    general mode only                                      */
+  int32_t reserved0;
+  double inv_resid_dof;          /* 1 / (nm - pm - qn - d(n+m) - 1), global n (optim.py:171-172) */
 } gmf_config;
 
 typedef struct gmf_buffers {  /* caller-owned device memory; rows block-major */
@@ -285,6 +297,8 @@ int64_t gmf_launch_count(gmf_handle* h);
 int gmf_profile(gmf_handle* h, int enable, double* out, void* stream);
 /* host copies of the first n trace entries (objective, nb shape) */
 int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stream);
+/* the dispersion at the same trace points (FitReport.phi_trace, optim.py:326) */
+int gmf_trace_phi_read(gmf_handle* h, double* phi, int64_t n, void* stream);
 
 /* Deviance half of penalized_objective over ALL local entries at the current
  * state: *dev_sum (device double) = sum_ij w_ij D(y_ij, mu_ij). */

@@ -433,6 +433,18 @@ def nb_moment_sums(y, mu, w):
     return float(np.sum(w * mu ** 2)), float(np.sum(w * ((y - mu) ** 2 - mu)))
 
 
+def pearson_phi_update(phi_bar, rho, y, mu, w, fcode, alpha, n, m, n_i, n_j, p, q, d):
+    """Smoothed stochastic Pearson update of phi -- optim.py:175-202:
+    phi_hat = sum_B w (y - mu)^2 / nu(mu) * (nm / n* m*) / N with
+    N = nm - mp - nq - (n + m) d - 1 (optim.py:171-172, model.py:279-283)."""
+    dof = n * m - (p * m + q * n + d * (n + m) + 1)
+    if dof <= 0:
+        raise ValueError("model is over-parameterized: nonpositive residual dof")
+    with np.errstate(all="ignore"):
+        s = float(np.sum(w * (y - mu) ** 2 / _variance(fcode, mu, alpha)))
+    return (1.0 - rho) * phi_bar + rho * (s * (n * m) / (n_i * n_j) / dof)
+
+
 def nb_shape_update(alpha_bar, rho, num, den, floor=NB_SHAPE_FLOOR, ceiling=NB_SHAPE_CEILING):
     """Smoothed moment update of the NB shape -- optim.py:205-229."""
     a_hat = num / den if den > 0 else ceiling
@@ -563,6 +575,7 @@ class OReport:
     final_objective: float = float("nan")
     objective_trace: list = field(default_factory=list)
     nb_shape_trace: list = field(default_factory=list)
+    phi_trace: list = field(default_factory=list)
     epochs_run: int = 0
     converged: bool = False
     iterations: int = 0
@@ -583,14 +596,17 @@ def replay_schedule(n, m, cfg: OConfig, n_steps=None):
 
 
 def fit_asgd(pb: OProblem, fcode, lcode, lam, cfg: OConfig, init: OState, *,
-             identify=True, est_alpha=None, callback=None, final_objective=True):
+             identify=True, est_alpha=None, est_phi=None, callback=None, final_objective=True):
     """Restatement of fit_asgd for fully observed data -- optim.py:383-489.
 
-    ``est_alpha`` defaults to the 'auto' policy (optim.py:156-168): NB
-    estimates its shape, Poisson estimates nothing.
+    ``est_alpha`` / ``est_phi`` default to the 'auto' policy (optim.py:156-168):
+    NB estimates its shape, the free-dispersion families (Gaussian, Gamma,
+    inverse Gaussian) estimate phi, Poisson and Bernoulli estimate nothing.
     """
     if est_alpha is None:
         est_alpha = fcode == NEG_BINOMIAL
+    if est_phi is None:
+        est_phi = fcode in (GAUSSIAN, GAMMA, INV_GAUSSIAN)
     st = init.copy()
     n, m = pb.n, pb.m
     p, q, d = pb.x.shape[1], pb.z.shape[1], st.u.shape[1]
@@ -605,6 +621,7 @@ def fit_asgd(pb: OProblem, fcode, lcode, lam, cfg: OConfig, init: OState, *,
     obj0 = tracked_objective(st, pb, fcode, lcode, lam, ent)
     rep.objective_trace.append(obj0)
     rep.nb_shape_trace.append(st.nb_shape)
+    rep.phi_trace.append(st.phi)
     snapshot = st.copy()
     if not np.isfinite(obj0):
         raise OracleDivergence("objective is non-finite at the initial state")
@@ -637,6 +654,9 @@ def fit_asgd(pb: OProblem, fcode, lcode, lam, cfg: OConfig, init: OState, *,
             dr = -alpha_t * gbr[I] / (hbr[I] + cfg.damping)
             st.gamma[I] += rho * dr[:, :q]
             st.u[I] += rho * dr[:, q:]
+            if est_phi:
+                st.phi = pearson_phi_update(st.phi, rho, y, mu, w, fcode, st.nb_shape, n, m,
+                                            len(I), len(J), p, q, d)
             if est_alpha:
                 num, den = nb_moment_sums(y, mu, w)
                 st.nb_shape = nb_shape_update(st.nb_shape, rho, num, den)
@@ -648,6 +668,7 @@ def fit_asgd(pb: OProblem, fcode, lcode, lam, cfg: OConfig, init: OState, *,
         prev = rep.objective_trace[-1]
         rep.objective_trace.append(obj)
         rep.nb_shape_trace.append(st.nb_shape)
+        rep.phi_trace.append(st.phi)
         if not np.isfinite(obj):
             raise OracleDivergence("objective became non-finite", state=snapshot)
         if len(rep.objective_trace) % SNAPSHOT_STRIDE == 0:

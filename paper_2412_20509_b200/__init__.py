@@ -12,7 +12,7 @@ from .exceptions import (ConfigError, DegenerateError, DivergenceError, DomainEr
                          GmfError, SingularSystemError)
 from .families import (Bernoulli, FamilySpec, Gamma, Gaussian, Identity, Inverse,  # noqa: F401
                        InverseGaussian, InverseSquared, LinkSpec, Log, Logit, NegBinomial,
-                       Poisson, canonical_link, family, link)
+                       Poisson, canonical_link, ddot_d, dot_d, family, link)
 from .gradients import GradientPair, Minibatch, full_gradients, minibatch_gradients  # noqa: F401
 from .identify import check_constraints, project_constraints  # noqa: F401
 from .model import (CovariateSet, FactorizationState, PenaltyConfig, ResponseMatrix,  # noqa: F401

@@ -52,6 +52,8 @@ class GmfDesc(C.Structure):
 
 # gmf_desc.flags bit: row and CSR buffers readable 16 bytes past their end
 DESC_TAIL_PADDED = 1
+# general mode: real-valued response in y_work, family / link at run time
+DESC_REAL_RESPONSE = 2
 
 
 class GmfConfig(C.Structure):
@@ -61,7 +63,8 @@ class GmfConfig(C.Structure):
                 ("lam_u", C.c_double), ("lam_v", C.c_double), ("nb_floor", C.c_double),
                 ("nb_ceiling", C.c_double), ("phi", C.c_double), ("eval_scale", C.c_double),
                 ("max_epochs", C.c_int64), ("est_alpha", C.c_int32),
-                ("snapshot_stride", C.c_int32), ("k1_impl", C.c_int32), ("nafill_every", C.c_int32)]
+                ("snapshot_stride", C.c_int32), ("k1_impl", C.c_int32), ("nafill_every", C.c_int32),
+                ("est_phi", C.c_int32), ("reserved0", C.c_int32), ("inv_resid_dof", C.c_double)]
 
 
 _P = C.c_void_p
@@ -105,6 +108,7 @@ SIGNATURES = {
     "gmf_run": (C.c_int, [_P, _i64, _P]),
     "gmf_status_read": (C.c_int, [_P, C.POINTER(GmfStatus), _P]),
     "gmf_trace_read": (C.c_int, [_P, _pd, _pd, _i64, _P]),
+    "gmf_trace_phi_read": (C.c_int, [_P, _pd, _i64, _P]),
     "gmf_status_raw_bytes": (_i64, []),
     "gmf_snapshot_blocks": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P]),
     "gmf_status_copy_async": (C.c_int, [_P, _P, _P]),

@@ -26,6 +26,7 @@ int launch_tcsr(const Params& P, const int32_t* tidx, int32_t* lens, int64_t* tp
                 unsigned int* too_big, cudaStream_t st);
 int tile_cols(int dtype, int NK);
 int grad_bucket(int KA);
+int grad_bucket_gen(int KA);
 int blocknorm_segments(int64_t nstar_max);
 int64_t rimg_bytes_of(int NK);
 int64_t grad_smem_bytes(const Params& P, int dtype, int NK);
@@ -80,12 +81,29 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
   if (d->m < 1 || d->n < 0) { set_error("bad shape n=%lld m=%lld", (long long)d->n, (long long)d->m); return GMF_ERR_CONFIG; }
   if (d->p < 0 || d->q < 0 || d->d < 0) { set_error("negative p/q/d"); return GMF_ERR_CONFIG; }
   if (d->dtype != GMF_F32 && d->dtype != GMF_F64) { set_error("unknown dtype %d", d->dtype); return GMF_ERR_CONFIG; }
-  if (d->link != GMF_LOG || (d->family != GMF_POISSON && d->family != GMF_NEG_BINOMIAL)) {
-    set_error("fused aSGD path supports poisson/neg_binomial with log link (family %d, link %d)",
-              d->family, d->link);
+  if (d->family < GMF_GAUSSIAN || d->family > GMF_NEG_BINOMIAL) { set_error("unknown family code %d", d->family); return GMF_ERR_DOMAIN; }
+  if (d->link < GMF_IDENTITY || d->link > GMF_INVERSE_SQUARED) { set_error("unknown link code %d", d->link); return GMF_ERR_DOMAIN; }
+  const bool fused = d->link == GMF_LOG && (d->family == GMF_POISSON || d->family == GMF_NEG_BINOMIAL);
+  const bool real = (d->flags & GMF_DESC_REAL_RESPONSE) != 0;
+  if (!fused && !real) {
+    set_error("family %d with link %d runs in general mode: pass the response as y_work with "
+              "GMF_DESC_REAL_RESPONSE", d->family, d->link);
     return GMF_ERR_UNSUPPORTED;
   }
-  if (d->y_format == GMF_Y_DENSE_I32) {
+  if (c->est_phi && !real) {
+    set_error("the Pearson dispersion update runs in general mode (GMF_DESC_REAL_RESPONSE)");
+    return GMF_ERR_UNSUPPORTED;
+  }
+  if (real) {
+    if (d->y_format != GMF_Y_DENSE_I32 || (!b->y_work && d->n > 0)) {
+      set_error("general mode needs a dense real-valued response in y_work");
+      return GMF_ERR_CONFIG;
+    }
+    if (c->est_phi && !(c->inv_resid_dof > 0)) {
+      set_error("model is over-parameterized: nonpositive residual dof");
+      return GMF_ERR_CONFIG;
+    }
+  } else if (d->y_format == GMF_Y_DENSE_I32) {
     if (!b->y_dense && d->n > 0) { set_error("dense Y pointer is NULL"); return GMF_ERR_CONFIG; }
   } else if (d->y_format == GMF_Y_CSR_I32 || d->y_format == GMF_Y_CSR_PACK32) {
     if (!b->csr_ptr) { set_error("CSR row pointer is NULL"); return GMF_ERR_CONFIG; }
@@ -141,9 +159,10 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   h->bufs = *bufs;
   const int p = desc->p, q = desc->q, d = desc->d;
   const int Kr = q + d, Kc = p + d, KA = p + q + d;
-  h->NK = grad_bucket(KA);
+  const bool gen_mode = (desc->flags & GMF_DESC_REAL_RESPONSE) != 0;
+  h->NK = gen_mode ? grad_bucket_gen(KA) : grad_bucket(KA);
   if (h->NK < 0) {
-    set_error("p+q+d = %d exceeds the fused kernel's 64-feature limit", KA);
+    set_error("p+q+d = %d exceeds the fused kernel's %d-feature limit", KA, gen_mode ? 32 : 64);
     delete h;
     return GMF_ERR_UNSUPPORTED;
   }
@@ -206,7 +225,11 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
                        (!P.has_off || al16(bufs->offset)) &&
                        (desc->y_format == GMF_Y_DENSE_I32 || al16(bufs->csr_col)) &&
                        (desc->y_format != GMF_Y_CSR_I32 || al16(bufs->csr_val));
-  P.holes = bufs->y_work != nullptr;
+  P.gen = (desc->flags & GMF_DESC_REAL_RESPONSE) ? 1 : 0;
+  P.link = desc->link;
+  P.est_phi = P.gen && cfg->est_phi;
+  P.inv_dof = cfg->inv_resid_dof;
+  P.holes = bufs->y_work != nullptr && !P.gen;
   P.y_work = bufs->y_work;
   P.nafill = cfg->nafill_every > 0 ? cfg->nafill_every : 1;
   if (P.holes && desc->y_format != GMF_Y_DENSE_I32) {
@@ -214,7 +237,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
     delete h;
     return GMF_ERR_CONFIG;
   }
-  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA, P.holes) && aligned;
+  const int tc_ok = tc_eligible(desc->dtype, P.has_w, Kr, Kc, KA, P.holes) && aligned && !P.gen;
   if (cfg->k1_impl == GMF_K1_TENSOR && !tc_ok) {
     set_error("k1_impl=tensor needs fp32, no prior weights, no unobserved entries, q+d <= 16, "
               "p+d <= 16 and 16-byte aligned row/CSR buffers (got Kr=%d Kc=%d)", Kr, Kc);
@@ -357,6 +380,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   const int64_t o_ctrl = take(sizeof(Ctrl));
   const int64_t o_tobj = take((max_epochs + 2) * 8);
   const int64_t o_tnb = take((max_epochs + 2) * 8);
+  const int64_t o_tphi = take((max_epochs + 2) * 8);
   const int64_t o_rowp = take((int64_t)P.CT * nstar_max * 2 * Kr * h->tsz);
   const int64_t o_colp = take((int64_t)P.CT * rs_max * TC * 2 * Kc * h->tsz);
   const int64_t o_nbp = take(cta_max * 2 * 8);
@@ -399,6 +423,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.ctrl = (Ctrl*)(base + o_ctrl);
   P.trace_obj = (double*)(base + o_tobj);
   P.trace_nb = (double*)(base + o_tnb);
+  P.trace_phi = (double*)(base + o_tphi);
   P.rowpart = base + o_rowp;
   P.colpart = base + o_colp;
   P.nbpart = (double*)(base + o_nbp);
@@ -804,6 +829,16 @@ int gmf_trace_read(gmf_handle* h, double* obj, double* nb, int64_t n, void* stre
   cudaStream_t st = (cudaStream_t)stream;
   if (obj) GMF_CUDA(cudaMemcpyAsync(obj, h->P.trace_obj, n * 8, cudaMemcpyDeviceToHost, st));
   if (nb) GMF_CUDA(cudaMemcpyAsync(nb, h->P.trace_nb, n * 8, cudaMemcpyDeviceToHost, st));
+  GMF_CUDA(cudaStreamSynchronize(st));
+  return GMF_OK;
+}
+
+int gmf_trace_phi_read(gmf_handle* h, double* phi, int64_t n, void* stream) {
+  if (!h || !phi) { set_error("null handle/out"); return GMF_ERR_STATE; }
+  if (n <= 0) return GMF_OK;
+  if (n > h->cfg.max_epochs + 1) n = h->cfg.max_epochs + 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  GMF_CUDA(cudaMemcpyAsync(phi, h->P.trace_phi, n * 8, cudaMemcpyDeviceToHost, st));
   GMF_CUDA(cudaStreamSynchronize(st));
   return GMF_OK;
 }

@@ -43,6 +43,10 @@ struct Params {
   int p, q, d, KA, Kr, Kc;
   int fam, yfmt, has_w, has_off;
   int holes;            // unobserved entries: y_work carries them (negative = imputed mean)
+  int gen;              // general mode: runtime family / link, y_work = the real-valued response
+  int link;             // gmf_link (general mode; the fused count paths are log-link)
+  int est_phi;          // Pearson dispersion update every step (optim.py:175-202)
+  double inv_dof;       // 1 / (nm - mp - nq - (n+m)d - 1)   (optim.py:171-172)
   int nafill;           // refill period (optim.py:432)
   void* y_work;         // [n][m] T working response (holes only)
   const int32_t* y;
@@ -120,6 +124,7 @@ struct Params {
   Ctrl* ctrl;
   double* trace_obj;
   double* trace_nb;
+  double* trace_phi;   // dispersion at each trace point (optim.py:326)
   void* rowpart;       // [CT][nstar_max][2 Kr]          T
   void* colpart;       // [CT][RS][TC][2 Kc]            T
   double* nbpart;      // [CT * RS][2]
@@ -242,6 +247,69 @@ GMF_D double sum_parts(const double* parts, int64_t n, int64_t stride, double* s
 }
 
 // ---------------------------------------------------------------------------
+// general mode: any family / link at run time (kernels/_ref.py:21-32, 96-117;
+// canonical pairs use the reference's simplified forms, the rest the generic
+// -w r / (phi nu g'), w / (phi nu g'^2)); pear = w r^2 / nu (optim.py:196-199)
+// ---------------------------------------------------------------------------
+GMF_D float gexp(float x) { return expf(x); }
+GMF_D double gexp(double x) { return exp(x); }
+GMF_D float grsqrt(float x) { return 1.f / sqrtf(x); }
+GMF_D double grsqrt(double x) { return 1.0 / sqrt(x); }
+
+template <typename T>
+GMF_D T gen_mean(int lcode, T eta) {
+  switch (lcode) {
+    case GMF_IDENTITY: return eta;
+    case GMF_LOG: return gexp(eta);
+    case GMF_LOGIT: return T(1) / (T(1) + gexp(-eta));
+    case GMF_INVERSE: return T(1) / eta;
+    default: return grsqrt(eta);
+  }
+}
+
+template <typename T>
+GMF_D T gen_variance(int fcode, T mu, T alpha) {
+  switch (fcode) {
+    case GMF_GAUSSIAN: return T(1);
+    case GMF_GAMMA: return mu * mu;
+    case GMF_INV_GAUSSIAN: return mu * mu * mu;
+    case GMF_POISSON: return mu;
+    case GMF_BERNOULLI: return mu * (T(1) - mu);
+    default: return mu * (T(1) + mu / alpha);
+  }
+}
+
+template <typename T>
+GMF_D void gen_derivs(int fcode, int lcode, T y, T mu, T w, T phi, T alpha, T& dd, T& hh, T& pear) {
+  const T r = y - mu;
+  const T nu = gen_variance<T>(fcode, mu, alpha);
+  pear = w * r * r / nu;
+  if (fcode == GMF_POISSON && lcode == GMF_LOG) { dd = -w * r / phi; hh = w * mu / phi; return; }
+  if (fcode == GMF_BERNOULLI && lcode == GMF_LOGIT) {
+    dd = -w * r / phi; hh = w * mu * (T(1) - mu) / phi; return;
+  }
+  if (fcode == GMF_GAUSSIAN && lcode == GMF_IDENTITY) { dd = -w * r / phi; hh = w / phi; return; }
+  if (fcode == GMF_GAMMA && lcode == GMF_INVERSE) { dd = w * r / phi; hh = w * mu * mu / phi; return; }
+  if (fcode == GMF_INV_GAUSSIAN && lcode == GMF_INVERSE_SQUARED) {
+    dd = w * r / (T(2) * phi); hh = w * mu * mu * mu / (T(4) * phi); return;
+  }
+  if (fcode == GMF_NEG_BINOMIAL && lcode == GMF_LOG) {
+    const T den = T(1) + mu / alpha;
+    dd = -w * r / (phi * den); hh = w * mu / (phi * den); return;
+  }
+  T g1;
+  switch (lcode) {
+    case GMF_IDENTITY: g1 = T(1); break;
+    case GMF_LOG: g1 = T(1) / mu; break;
+    case GMF_LOGIT: g1 = T(1) / (mu * (T(1) - mu)); break;
+    case GMF_INVERSE: g1 = T(-1) / (mu * mu); break;
+    default: g1 = T(-2) / (mu * mu * mu);
+  }
+  dd = -w * r / (phi * nu * g1);
+  hh = w / (phi * nu * g1 * g1);
+}
+
+// ---------------------------------------------------------------------------
 // tracker decision (optim.py:301-338), from objective totals
 // ---------------------------------------------------------------------------
 // a mod b for a, b >= 0 through the 32-bit path whenever both fit (a 64-bit
@@ -264,7 +332,7 @@ GMF_D Decision decide_from(const Params& P, const Ctrl& C, double dev, double ng
   D.boundary = mod_nn(C.t, P.S) == 0;
   D.snap = 0; D.stop = 0; D.conv = C.converged; D.div = 0; D.div_init = 0; D.streak = C.streak;
   if (D.boundary) {
-    D.obj = P.escale * dev / (2.0 * P.phi) +
+    D.obj = P.escale * dev / (2.0 * C.phi) +
             0.5 * (P.lam_b * nb + P.lam_g * ng + P.lam_u * nu + P.lam_v * nv);
     if (C.t == 0) {
       if (!isfinite(D.obj)) { D.div_init = 1; D.stop = 1; }
@@ -304,6 +372,13 @@ GMF_D Ctrl advance(const Params& P, const Ctrl& C, const Decision& D, double nb_
       double ah = nb_den > 0.0 ? nb_num / nb_den : P.nbceil;
       ah = fmin(fmax(P.nbfloor, ah), P.nbceil);
       N.nb_shape = (1.0 - rho) * C.nb_shape + rho * ah;
+    }
+    if (P.est_phi) {     // optim.py:175-202: nb_num carries sum_B w (y - mu)^2 / nu(mu)
+      const double rho = P.rho_tab[C.t];
+      const long long s = mod_nn(C.t, P.S);
+      const double nJ = (double)(P.cbp[s + 1] - P.cbp[s]);
+      const double ph = nb_num * P.rbscale[P.bseq[C.t]] * ((double)P.m / nJ) * P.inv_dof;
+      N.phi = (1.0 - rho) * C.phi + rho * ph;
     }
     N.t = C.t + 1;
   }

@@ -60,9 +60,10 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   } else {
     // holes: a standalone gradient masks them (gradients.py:66-88); inside
     // the fit they carry the imputed mean, refilled every nafill steps
-    const int hmode = P.holes ? (xb >= 0 ? 2 : 1) : 0;
+    const int hmode = P.gen ? 3 : (P.holes ? (xb >= 0 ? 2 : 1) : 0);
     const bool fill = hmode == 1 && mod_nn(P.ctrl->t, P.nafill) == 0;
-    grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem, hmode, fill);
+    grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem, hmode, fill,
+                             xb >= 0 ? P.phi : C->phi);
   }
 
   (void)TC;
@@ -226,7 +227,10 @@ GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, in
     #pragma unroll
     for (int k = 0; k < NK; ++k) eta += (double)av[k] * (double)cv[k];
     const double wv = P.has_w ? (double)tptr<T>(P.w)[i * P.m + j] : 1.0;
-    if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
+    if (P.gen)   // general mode: real-valued response, any link (fp64 per-entry algebra)
+      s += wv * unit_deviance(P.fam, (double)tptr<T>(P.y_work)[i * P.m + j],
+                              gen_mean<double>(P.link, eta), alpha);
+    else if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
       s += wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta), (float)alpha);
     else
       s += wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
@@ -544,8 +548,9 @@ k_fit(Params P, long long n_steps) {
       if constexpr (TCM == 1)
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
                               profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
-      else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, P.holes ? 1 : 0,
-                                    P.holes && mod_nn(t, P.nafill) == 0);
+      else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem,
+                                    P.gen ? 3 : (P.holes ? 1 : 0),
+                                    P.holes && mod_nn(t, P.nafill) == 0, C.phi);
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }
     if (profc) { __syncthreads(); if (threadIdx.x == 0) P.prof[16 + 32 * blockIdx.x + 2] = gtimer(); }
@@ -560,7 +565,7 @@ k_fit(Params P, long long n_steps) {
       #pragma unroll
       for (int k = 0; k < 7; ++k) v7[k] = 0.0;
       {   // two slots per thread per pass, every load of a pass in flight together
-        const bool tb = boundary, tn = run_grad && P.est_alpha;
+        const bool tb = boundary, tn = run_grad && (P.est_alpha || P.est_phi);
         const int64_t nmax = (int64_t)G > P.R ? (int64_t)G : P.R;
         for (int64_t i = threadIdx.x; i < nmax; i += 2 * NT) {
           double l[2][7];
@@ -826,6 +831,7 @@ k_fit(Params P, long long n_steps) {
       if (D.boundary) {
         P.trace_obj[C.trace_len] = D.obj;
         P.trace_nb[C.trace_len] = C.nb_shape;
+    P.trace_phi[C.trace_len] = C.phi;
       }
       if (cow) P.snap_ver[blk] = per_now;
       *P.ctrl = N;
@@ -876,6 +882,13 @@ struct Inst {
 
 template <typename T, int FAM, int TCM>
 static void* pick(int NK, bool fit) {
+  if constexpr (FAM == 2) {   // general mode: two feature buckets (build time)
+    switch (NK) {
+      case 16: return fit ? Inst<T, 2, 16, 0>::fit() : Inst<T, 2, 16, 0>::grad();
+      case 32: return fit ? Inst<T, 2, 32, 0>::fit() : Inst<T, 2, 32, 0>::grad();
+      default: return nullptr;
+    }
+  } else {
   switch (NK) {
     case 8: return fit ? Inst<T, FAM, 8, TCM>::fit() : Inst<T, FAM, 8, TCM>::grad();
     case 12: return fit ? Inst<T, FAM, 12, TCM>::fit() : Inst<T, FAM, 12, TCM>::grad();
@@ -888,10 +901,12 @@ static void* pick(int NK, bool fit) {
       return nullptr;
     default: return nullptr;
   }
+  }
 }
 
 // tcm: K1 on the tensor cores (fp32 only; gmf_tc.cuh)
-static void* kernel_for(int dtype, int family, int NK, bool fit, int tcm) {
+static void* kernel_for(int dtype, int family, int NK, bool fit, int tcm, int gen = 0) {
+  if (gen) return dtype == GMF_F64 ? pick<double, 2, 0>(NK, fit) : pick<float, 2, 0>(NK, fit);
   const int fam = family == GMF_NEG_BINOMIAL ? 1 : 0;
   if (dtype == GMF_F64) return fam ? pick<double, 1, 0>(NK, fit) : pick<double, 0, 0>(NK, fit);
   if (tcm == 2) return fam ? pick<float, 1, 2>(NK, fit) : pick<float, 0, 2>(NK, fit);
@@ -906,6 +921,8 @@ int64_t rimg_bytes_of(int NK) { return tc2::rimg_bytes(NK); }
 int tc_eligible(int dtype, int has_w, int Kr, int Kc, int KA, int holes) {
   return dtype == GMF_F32 && !has_w && !holes && Kr <= 16 && Kc <= 16 && KA <= 32;
 }
+
+int grad_bucket_gen(int KA) { return KA <= 16 ? 16 : (KA <= 32 ? 32 : -1); }
 
 int grad_bucket(int KA) {
   if (KA <= 8) return 8;
@@ -939,8 +956,8 @@ int64_t grad_smem_bytes(const Params& P, int dtype, int NK) {
 // report how many k_fit CTAs can be co-resident per SM
 int prepare_grad(const Params& P, int dtype, int NK, int fit_extra_smem, int* fit_blocks_per_sm) {
   const int tcm = P.tcm;
-  void* g = kernel_for(dtype, P.fam, NK, false, tcm);
-  void* f = kernel_for(dtype, P.fam, NK, true, tcm);
+  void* g = kernel_for(dtype, P.fam, NK, false, tcm, P.gen);
+  void* f = kernel_for(dtype, P.fam, NK, true, tcm, P.gen);
   if (!g || !f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   const int nt = k1_threads(tcm);
   const int smem_g = (int)grad_smem_bytes(P, dtype, NK);
@@ -984,7 +1001,7 @@ int prepare_grad(const Params& P, int dtype, int NK, int fit_extra_smem, int* fi
 
 int launch_grad(const Params& P, int dtype, int NK, cudaStream_t st, long long xb, long long xs,
                 double xalpha) {
-  void* f = kernel_for(dtype, P.fam, NK, false, P.tcm);
+  void* f = kernel_for(dtype, P.fam, NK, false, P.tcm, P.gen);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   dim3 grid(P.RS, P.CT);
   if (P.tcm == 2) {   // one CTA per SM walking the CT x RS units
@@ -1010,7 +1027,7 @@ int launch_colrec(const Params& P, int dtype, cudaStream_t st, long long xs) {
 }
 
 int launch_fit(const Params& P, int dtype, int NK, int grid, long long n_steps, cudaStream_t st) {
-  void* f = kernel_for(dtype, P.fam, NK, true, P.tcm);
+  void* f = kernel_for(dtype, P.fam, NK, true, P.tcm, P.gen);
   if (!f) { set_error("unsupported feature bucket %d", NK); return GMF_ERR_UNSUPPORTED; }
   const size_t smem = (size_t)grad_smem_bytes(P, dtype, NK) + (size_t)P.ep_cap * sizeof(int4);
   Params Q = P;

@@ -21,6 +21,7 @@ GMF_D int stg_col(int pack, int32_t w) { return pack ? (int)((uint32_t)w & 0xFFF
 GMF_D int stg_val(int pack, int32_t w, int32_t v) { return pack ? (int)((uint32_t)w >> 16) : (int)v; }
 
 GMF_D double y_lookup(const Params& P, int64_t i, int64_t j) {
+  if (P.gen) return 0.0;   // real-valued responses are read from y_work where needed
   if (P.yfmt == GMF_Y_DENSE_I32) return (double)P.y[i * P.m + j];
   int64_t lo = P.rp[i], hi = P.rp[i + 1];
   while (lo < hi) {
@@ -169,7 +170,7 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
                   const T* __restrict__ w_s, T* __restrict__ P_s, const T (&cf)[NK],
                   T (&gacc)[NK], T (&hacc)[NK], T cm, int c, int g, int rows, T rphi, T tphi,
                   T ralpha, T& cn, T& cd, int hmode = 0, bool fill = false, T* ywg = nullptr,
-                  int64_t ystride = 0) {
+                  int64_t ystride = 0, int fcode = 0, int lcode = 0) {
   constexpr int NG = kThreads / TC;
   #pragma unroll 2
   for (int rr = g; rr < rows; rr += NG) {
@@ -180,12 +181,14 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
       e0 = fma(a[k], cf[k], e0);
       e1 = fma(a[k + 1], cf[k + 1], e1);
     }
-    const T mu = exp_pre(e0 + e1);
+    // FAM 2 (general mode): the features are not pre-scaled, any link
+    const T mu = FAM == 2 ? gen_mean<T>(lcode, e0 + e1) : exp_pre(e0 + e1);
     T yv;
     T wv = HW ? w_s[rr * TC + c] : cm;
     if constexpr (HOLES) {
+      // hmode 3: y_work is a plain real-valued response (no holes)
       const T v = reinterpret_cast<const T*>(y_s)[rr * TC + c];
-      const bool hole = signbit(v);
+      const bool hole = hmode != 3 && signbit(v);
       yv = hole ? -v : v;
       if (hole && hmode == 2) wv = T(0);
       if (hole && hmode == 1 && fill && cm != T(0)) {
@@ -197,7 +200,12 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
     }
     const T r = yv - mu;
     T dd, hh;
-    if (FAM == 0) {
+    if (FAM == 2) {
+      T pear;
+      gen_derivs<T>(fcode, lcode, yv, mu, wv, tphi, T(1) / ralpha, dd, hh, pear);
+      if (wv == T(0)) { dd = T(0); hh = T(0); pear = T(0); }   // outside the block: no NaNs
+      cn += pear;
+    } else if (FAM == 0) {
       const T ws = wv * rphi;
       dd = -ws * r;
       hh = ws * mu;
@@ -221,7 +229,9 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
 
 template <typename T, int FAM, int NK, int TC>
 GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, int rs, int ct,
-                    int RS, unsigned char* smem, int hmode = 0, bool fill = false) {
+                    int RS, unsigned char* smem, int hmode = 0, bool fill = false,
+                    double phi = -1.0) {
+  if (phi < 0.0) phi = P.phi;   // the fit passes the live dispersion (Ctrl.phi)
   constexpr int NG = kThreads / TC;
   constexpr int TCQ = TC / NQ;
   __shared__ double red_scr[kThreads / 32];
@@ -251,7 +261,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   const T* zg = tptr<T>(P.z);
   const T* offg = tptr<T>(P.off);
   const T* wg = tptr<T>(P.w);
-  const T pre = T(Pre<T>::s);
+  const T pre = FAM == 2 ? T(1) : T(Pre<T>::s);
 
   // ---- this thread's column features [b | v | z] (phase 1), pre-scaled ----
   const int c = tid % TC, g = tid / TC;
@@ -321,7 +331,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       }
     }
     unsigned char* st = smem + L.stage[b];
-    if (!csr && P.holes) {   // working response (T), holes negative
+    if (!csr && (P.holes || P.gen)) {   // working / real-valued response (T)
       T* y_b = reinterpret_cast<T*>(st);
       const T* yw = tptr<T>(P.y_work);
       for (int e = tid; e < TR * TC; e += kThreads) {
@@ -365,9 +375,9 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
   #pragma unroll
   for (int k = 0; k < NK; ++k) { gacc[k] = T(0); hacc[k] = T(0); }
   double nb_num = 0.0, nb_den = 0.0;
-  const T rphi = T(1.0 / P.phi);
+  const T rphi = T(1.0 / phi);
   const T ralpha = T(1.0 / alpha);
-  const T tphi = T(P.phi);
+  const T tphi = T(phi);
   const int pr = tid % TR, ph = (tid / TR) & 1, pq = tid / (2 * TR);
   const int rkk = 2 * Kr;
   // incremental (row, component) walk of the row-partial output loop
@@ -440,16 +450,16 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
 
     // ---- phase 1 ----
     T cn = T(0), cd = T(0);
-    if (P.holes) {
+    if (P.holes || P.gen) {
       T* ywg = tptr<T>(P.y_work) + i0 * P.m + j;   // the chunk's first row, this thread's column j
       if (P.has_w)
         phase1<T, FAM, NK, TC, true, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
                                            g, rows, rphi, tphi, ralpha, cn, cd, hmode, fill, ywg,
-                                           P.m);
+                                           P.m, P.fam, P.link);
       else
         phase1<T, FAM, NK, TC, false, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm,
                                             c, g, rows, rphi, tphi, ralpha, cn, cd, hmode, fill,
-                                            ywg, P.m);
+                                            ywg, P.m, P.fam, P.link);
     } else if (P.has_w) {
       phase1<T, FAM, NK, TC, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c, g,
                                    rows, rphi, tphi, ralpha, cn, cd);

@@ -83,6 +83,9 @@ GMF_D double entry_dev_cached(const Params& P, int4 en, double alpha) {
     }
   }
   const double wv = P.has_w ? (double)tptr<T>(P.w)[(int64_t)en.x * P.m + en.y] : 1.0;
+  if (P.gen)   // general mode: real-valued response, any link
+    return wv * unit_deviance(P.fam, (double)tptr<T>(P.y_work)[(int64_t)en.x * P.m + en.y],
+                              gen_mean<double>(P.link, eta), alpha);
   if (sizeof(T) == 4)
     return wv * (double)unit_deviance_f(P.fam, (float)en.z, __expf((float)eta), (float)alpha);
   return wv * unit_deviance(P.fam, (double)en.z, exp(eta), alpha);
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params P, const unsigned cha
   if (D.boundary) {
     P.trace_obj[C.trace_len] = D.obj;
     P.trace_nb[C.trace_len] = C.nb_shape;
+    P.trace_phi[C.trace_len] = C.phi;
   }
   if (upd) {
     P.blocksum[2 * blk] = g2;
@@ -452,7 +456,11 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
           if (cc >= nc) continue;
           const int64_t j = j0 + cc;
           const double eta = acc[r][h] + offs[rr];
-          if (dense) {
+          if (P.gen) {   // general mode: real-valued response, any link
+            const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
+            s += w * unit_deviance(P.fam, (double)tptr<T>(P.y_work)[i * P.m + j],
+                                   gen_mean<double>(P.link, eta), alpha);
+          } else if (dense) {
             double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
             const double y = (double)P.y[i * P.m + j];
             // unobserved entries (negative working response) are not in the

@@ -159,17 +159,31 @@ class DeviceFit:
 
     def __init__(self, data, covs, fam, lnk, penalty, cfg, state: FactorizationState, *,
                  schedule: Schedule, offset=None, dtype="f64", device=None, world=1, rank=0,
-                 est_alpha=False, k1_impl="auto", y_format="auto"):
+                 est_alpha=False, est_phi=False, k1_impl="auto", y_format="auto"):
         import torch
         _lib.require_cuda()
         lib = _lib.lib()
-        if fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log":
-            raise _lib.UnsupportedError(
-                f"the fused aSGD kernels implement poisson/neg_binomial with log link, "
-                f"got {fam.kind}+{lnk.kind}")
+        # the fused count kernels cover poisson / neg_binomial with the log
+        # link; every other family / link pair, and any fit that estimates phi
+        # (optim.py:175-202), runs in general mode: real-valued dense response,
+        # family and link chosen at run time on the CUDA-core K1
+        general = est_phi or fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log"
         holes = not data.fully_observed
         if holes and data.csr is not None:
             raise _lib.UnsupportedError("unobserved entries need a dense response")
+        if general:
+            if data.csr is not None:
+                raise _lib.UnsupportedError(
+                    f"{fam.kind}+{lnk.kind}"
+                    f"{' with an estimated dispersion' if est_phi else ''} runs in general mode, "
+                    "which needs a dense response")
+            if holes:
+                raise _lib.UnsupportedError(
+                    "general mode (non-count family / link, or estimated phi) needs a fully "
+                    "observed response")
+            if k1_impl == "tensor":
+                raise _lib.UnsupportedError("general mode runs K1 on the CUDA cores")
+            fam.check_y(data.values)   # DomainError as families.py:239-241
         if dtype not in ("f32", "f64"):
             raise ConfigError(f"dtype must be 'f32' or 'f64', got {dtype!r}")
         if k1_impl not in _lib.K1_IMPL_CODES:
@@ -224,6 +238,10 @@ class DeviceFit:
                 self.csr_col = up_padded(c2.astype(np.int32))
                 self.csr_val = up_padded(counts)
                 y_format_code = _lib.Y_CSR_I32
+        elif general:
+            self.y_dense = None
+            self.csr_ptr = self.csr_col = self.csr_val = None
+            y_format_code = _lib.Y_DENSE_I32
         else:
             vals = data.values[order]
             if holes:   # observed counts; the working response below carries the holes
@@ -232,7 +250,10 @@ class DeviceFit:
             self.csr_ptr = self.csr_col = self.csr_val = None
             y_format_code = _lib.Y_DENSE_I32
         self.y_work = None
-        if holes:
+        self.general = general
+        if general:   # the real-valued response itself (GMF_DESC_REAL_RESPONSE)
+            self.y_work = up(data.values[order], self.tdt)
+        elif holes:
             # working response (optim.py:368-374): observed counts, and at every
             # unobserved entry minus its mean at the initial state,
             # -g^{-1}(eta0) -- the sign marks the hole, the kernel refills it
@@ -295,7 +316,12 @@ class DeviceFit:
                                  family=_lib.FAMILY_CODES[fam.kind], link=_lib.LINK_CODES[lnk.kind],
                                  y_format=y_format_code, has_offset=int(offset is not None),
                                  has_weights=int(self.weights is not None), world_size=world,
-                                 rank=rank, device=dev_index, flags=_lib.DESC_TAIL_PADDED)
+                                 rank=rank, device=dev_index,
+                                 flags=_lib.DESC_TAIL_PADDED |
+                                 (_lib.DESC_REAL_RESPONSE if general else 0))
+        dof = self.n * self.m - (self.p * self.m + self.q * self.n + self.d * (self.n + self.m) + 1)
+        if est_phi and dof <= 0:
+            raise ConfigError("model is over-parameterized: nonpositive residual dof")
         self.cfg = _lib.GmfConfig(
             rate_k0=cfg.rate_k0, rate_k1=cfg.rate_k1, rate_tau=cfg.rate_tau,
             smooth_a1=cfg.smooth_a1, smooth_a2=cfg.smooth_a2, damping=cfg.damping, tol=cfg.tol,
@@ -303,7 +329,8 @@ class DeviceFit:
             lam_v=penalty.lam_v, nb_floor=1e-4, nb_ceiling=1e8, phi=float(state.phi),
             eval_scale=float(schedule.eval_scale), max_epochs=cfg.max_epochs,
             est_alpha=int(bool(est_alpha)), snapshot_stride=4,
-            k1_impl=_lib.K1_IMPL_CODES[k1_impl], nafill_every=int(cfg.nafill_every))
+            k1_impl=_lib.K1_IMPL_CODES[k1_impl], nafill_every=int(cfg.nafill_every),
+            est_phi=int(bool(est_phi)), inv_resid_dof=(1.0 / dof if dof > 0 else 0.0))
         P = _lib.ptr
         self.bufs = _lib.GmfBuffers(
             y_dense=P(self.y_dense), csr_ptr=P(self.csr_ptr), csr_col=P(self.csr_col),
@@ -381,6 +408,13 @@ class DeviceFit:
             self.h, obj.ctypes.data_as(C.POINTER(C.c_double)),
             nb.ctypes.data_as(C.POINTER(C.c_double)), n, self.stream()), "gmf_trace_read")
         return obj[:n], nb[:n]
+
+    def phi_trace(self, n):
+        phi = np.zeros(max(n, 1))
+        _lib.check(self.lib.gmf_trace_phi_read(
+            self.h, phi.ctypes.data_as(C.POINTER(C.c_double)), n, self.stream()),
+            "gmf_trace_phi_read")
+        return phi[:n]
 
     def minibatch_grad(self, row_block, col_block, nb_shape):
         torch = self.torch

@@ -226,8 +226,6 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
         init_state = init_glm_svd(data, covs, fam, lnk, rank, seed=cfg.seed, device=device)
     init_state.check_shapes(data, covs)
     est_phi, est_alpha = _resolve_dispersion(fam, dispersion)
-    if est_phi:
-        raise _lib.UnsupportedError("Pearson dispersion updates are not on the device path")
     if offset is not None and np.asarray(offset).shape != (data.n,):
         raise ConfigError("offset must have one entry per row")
     n, m = data.shape
@@ -236,33 +234,37 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
     sched = Schedule(n, m, cfg, mask=mask)
     fit = DeviceFit(data, covs, fam, lnk, penalty, cfg, init_state, schedule=sched,
                     offset=offset, dtype=dtype, device=device, world=world, rank=my_rank,
-                    est_alpha=est_alpha, k1_impl=k1_impl, y_format=y_format)
+                    est_alpha=est_alpha, est_phi=est_phi, k1_impl=k1_impl, y_format=y_format)
     try:
         fit.reset()
         _drive(fit, callback, process_group, exchange)
         st = fit.status()
         trace, nb_trace = fit.trace(int(st.trace_len))
+        phi_trace = fit.phi_trace(int(st.trace_len))
         if st.diverged_init:
             raise DivergenceError("objective is non-finite at the initial state")
 
-        def host_state(snapshot, nb):
+        def host_state(snapshot, nb, phi):
             if world == 1:
-                return fit.download_state(snapshot=snapshot, nb_shape=nb)
-            return _gathered_state(fit, process_group, exchange, nb, snapshot)
+                return fit.download_state(snapshot=snapshot, nb_shape=nb, phi=phi)
+            got = _gathered_state(fit, process_group, exchange, nb, snapshot)
+            got.phi = float(phi)
+            return got
 
         if st.diverged:
-            snap_nb = float(nb_trace[max(int(st.snapshot_trace_len) - 1, 0)])
+            k_snap = max(int(st.snapshot_trace_len) - 1, 0)
             raise DivergenceError("objective became non-finite; carrying the last finite state",
-                                  state=host_state(True, snap_nb))
+                                  state=host_state(True, float(nb_trace[k_snap]),
+                                                   float(phi_trace[k_snap])))
         info = None
         if identify_mode and world == 1:
             dev = _Dev(fit.torch, fit.device, fit.tdt, fit.theta_row, fit.theta_col, fit.x,
                        fit.z, covs.p, covs.q, init_state.rank)
             info = project_on_device(dev, n, m, identify_mode)
             dev_sum = fit.objective_dev()
-            final = fit.download_state(nb_shape=st.nb_shape)
+            final = fit.download_state(nb_shape=st.nb_shape, phi=st.phi)
         else:
-            final = host_state(False, st.nb_shape)
+            final = host_state(False, st.nb_shape, st.phi)
             if identify_mode:
                 from .identify import project_constraints
                 final, info = project_constraints(final, covs, identify_mode, return_info=True,
@@ -286,7 +288,7 @@ def fit_asgd(data, covs, fam, lnk, penalty, cfg: SgdConfig, init_state=None, *, 
             epochs_run=int(st.trace_len) - 1,
             converged=bool(st.converged),
             elapsed_seconds=time.perf_counter() - started,
-            phi_trace=[float(init_state.phi)] * int(st.trace_len),
+            phi_trace=[float(v) for v in phi_trace],
             nb_shape_trace=[float(v) for v in nb_trace],
             diagnostics={"iterations": int(st.t),
                          "row_blocks": [b.tolist() for b in sched.row_blocks],

@@ -613,8 +613,95 @@ def make_masked_p3():
     return _run_fit(y, x, z, init, gk.Poisson(), cfg, mask=mask)
 
 
+GENERAL_CASES = (
+    # name, family, link, dispersion policy, (p, q, d), seed
+    ("gauss_id", "gaussian", "identity", "auto", (1, 1, 3), 31),
+    ("gamma_log", "gamma", "log", "auto", (1, 0, 3), 32),
+    ("bern_logit", "bernoulli", "logit", "auto", (1, 1, 2), 33),
+    ("ig_log", "inverse_gaussian", "log", "auto", (1, 0, 2), 34),
+    ("qpois", "poisson", "log", "estimate", (2, 1, 3), 35),
+    ("gamma_inv", "gamma", "inverse", "fixed", (1, 0, 2), 36),
+    ("pois_id", "poisson", "identity", "auto", (1, 0, 2), 37),
+)
+
+
+def _general_problem(fam_kind, lnk_kind, n, m, p, q, d, seed):
+    """Real-valued (or count) responses simulated by gmfkit's own family
+    samplers at a known state; the init is the truth perturbed."""
+    rng = np.random.default_rng(seed)
+    x = np.hstack([np.ones((n, 1)), rng.normal(0, 1, (n, p - 1))]) if p else np.zeros((n, 0))
+    z = rng.normal(0, 0.3, (m, q)) if q else np.zeros((m, 0))
+    u = rng.normal(0, 0.25, (n, d))
+    v = rng.normal(0, 0.25, (m, d))
+    gamma = rng.normal(0, 0.2, (n, q))
+    b = rng.normal(0, 0.15, (m, p))
+    if p:
+        # the intercept places eta inside the link's domain with margin
+        b[:, 0] += {"identity": 3.0, "log": 0.8, "logit": 0.0, "inverse": 1.5,
+                    "inverse_squared": 1.5}[lnk_kind]
+    eta = u @ v.T + x @ b.T + gamma @ z.T
+    lnk = gk.link(lnk_kind)
+    fam = gk.family(fam_kind)
+    mu = lnk.inverse(eta)
+    y = fam.sample(mu, phi=0.4 if fam.has_free_dispersion else 1.0, rng=rng)
+    init = {"b": b + 0.03 * rng.normal(size=b.shape), "gamma": gamma * 0.8,
+            "u": u + 0.05 * rng.normal(size=u.shape), "v": v + 0.05 * rng.normal(size=v.shape),
+            "phi": 1.0, "nb_shape": 1.0}
+    return y, x, z, init
+
+
+def make_general():
+    """Families and links beyond Poisson/NB+log, and the Pearson dispersion
+    update (families.py:267-441, optim.py:175-202, 465-468): whole fits of the
+    reference, per-step states, phi traces, step-0 gradients."""
+    out = {"cases": np.asarray([c[0] for c in GENERAL_CASES])}
+    for name, fk, lk, disp, (p, q, d), seed in GENERAL_CASES:
+        n, m = 360, 48
+        y, x, z, init = _general_problem(fk, lk, n, m, p, q, d, seed)
+        data = gk.ResponseMatrix(y.astype(float))
+        covs = gk.CovariateSet(x=x if p else None, z=z if q else None, n=n, m=m)
+        fam, lnk = gk.family(fk), gk.link(lk)
+        cfg = gk.SgdConfig(max_epochs=24, mb_rows=90, mb_cols=m, tol=1e-30, seed=seed,
+                           rate_k0=0.01, rate_k1=0.01)
+        pen = gk.PenaltyConfig()
+        st0 = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], 1.0, 1.0)
+        steps = {}
+
+        def cb(t, st, steps=steps):
+            if t in CHECK_STEPS:
+                steps[t] = st.copy()
+
+        rng = np.random.default_rng(cfg.seed)
+        rb = goptim._partition(rng, n, cfg.mb_rows)
+        cb_ = goptim._partition(rng, m, m)
+        goptim._eval_entries(data, cfg.max_eval_entries, rng)
+        first = int(rng.integers(len(rb)))
+        g0 = gk.minibatch_gradients(st0, data, covs, fam, lnk, pen, gk.Minibatch(rb[first], cb_[0]))
+        final, rep = gk.fit_asgd(data, covs, fam, lnk, pen, cfg, st0, dispersion=disp, callback=cb)
+        unproj, _ = gk.fit_asgd(data, covs, fam, lnk, pen, cfg, st0, dispersion=disp,
+                                identify_mode=None)
+        arrs = {"y": y, "x": x, "z": z, "family": np.asarray(fk), "link": np.asarray(lk),
+                "dispersion": np.asarray(disp), "first_block": np.int64(first),
+                "g0_g_row": g0.g_rowside, "g0_h_row": g0.h_rowside,
+                "g0_g_col": g0.g_colside, "g0_h_col": g0.h_colside,
+                "trace": np.asarray(rep.objective_trace), "phi_trace": np.asarray(rep.phi_trace),
+                "final_objective": np.float64(rep.final_objective),
+                "epochs_run": np.int64(rep.epochs_run),
+                "cfg": np.asarray([cfg.max_epochs, cfg.mb_rows, cfg.mb_cols, cfg.seed],
+                                  dtype=np.int64),
+                "check_steps": np.asarray(sorted(steps), dtype=np.int64)}
+        arrs.update(_state_arrays("init", st0))
+        arrs.update(_state_arrays("final", final))
+        arrs.update(_state_arrays("unproj", unproj))
+        for t, st in steps.items():
+            arrs.update(_state_arrays(f"step{t}", st))
+        assert np.all(np.isfinite(rep.objective_trace)), name
+        out.update({f"{name}__{k}": v for k, v in arrs.items()})
+    return out
+
+
 def main():
-    makers = {"c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
+    makers = {"general": make_general, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,

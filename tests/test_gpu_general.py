@@ -1,0 +1,133 @@
+"""GPU parity of general mode -- any family / link at run time on the
+CUDA-core K1, real-valued responses, the Pearson dispersion update -- against
+the reference's own fits (tests/golden/general.npz from gmfkit) and the
+oracle.  fp64: trajectories to 1e-9; fp32: north-star tolerances."""
+import numpy as np
+import pytest
+
+from conftest import golden, normwise
+from oracle import asgd_oracle as orc
+from test_general_oracle import CASES, case
+
+pytestmark = pytest.mark.gpu
+
+gk = pytest.importorskip("paper_2412_20509_b200")
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _setup(c):
+    n, m = c["y"].shape
+    data = gk.ResponseMatrix(c["y"].astype(float))
+    covs = gk.CovariateSet(x=c["x"] if c["x"].shape[1] else None,
+                           z=c["z"] if c["z"].shape[1] else None, n=n, m=m)
+    fam, lnk = gk.family(str(c["family"])), gk.link(str(c["link"]))
+    me, mr, mc, seed = (int(v) for v in c["cfg"])
+    cfg = gk.SgdConfig(max_epochs=me, mb_rows=mr, mb_cols=mc, tol=1e-30, seed=seed)
+    init = gk.FactorizationState(c["init_b"], c["init_gamma"], c["init_u"], c["init_v"], 1.0, 1.0)
+    return data, covs, fam, lnk, cfg, init
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_general_fit_fp64_matches_reference(name):
+    c = case(golden("general"), name)
+    data, covs, fam, lnk, cfg, init = _setup(c)
+    seen = {}
+
+    def cb(t, st):
+        if t in set(c["check_steps"].tolist()):
+            seen[t] = st.copy()
+
+    final, rep = gk.fit_asgd(data, covs, fam, lnk, gk.PenaltyConfig(), cfg, init,
+                             dispersion=str(c["dispersion"]), callback=cb, dtype="f64")
+    assert rep.epochs_run == int(c["epochs_run"])
+    assert normwise(rep.objective_trace, c["trace"]) < 1e-9
+    assert normwise(rep.phi_trace, c["phi_trace"]) < 1e-9
+    assert seen
+    for t, st in seen.items():
+        for blk in ("b", "gamma", "u", "v"):
+            assert normwise(getattr(st, blk), c[f"step{t}_{blk}"]) < 1e-8, (t, blk)
+    assert abs(final.phi - float(c["final_phi"])) < 1e-9 * float(c["final_phi"])
+    assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 1e-7
+    fo = float(c["final_objective"])
+    assert abs(rep.final_objective - fo) < 1e-9 * abs(fo)
+    assert rep.diagnostics["algorithm"] == "asgd"
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_general_fit_fp32(name):
+    c = case(golden("general"), name)
+    data, covs, fam, lnk, cfg, init = _setup(c)
+    final, rep = gk.fit_asgd(data, covs, fam, lnk, gk.PenaltyConfig(), cfg, init,
+                             dispersion=str(c["dispersion"]), dtype="f32")
+    assert normwise(rep.objective_trace, c["trace"]) < 1e-3
+    assert normwise(rep.phi_trace, c["phi_trace"]) < 1e-3
+    assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 1e-3
+    fo = float(c["final_objective"])
+    assert abs(rep.final_objective - fo) < 1e-3 * abs(fo)
+
+
+@pytest.mark.parametrize("name", ["gauss_id", "gamma_inv", "pois_id"])
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-4)])
+def test_general_step0_gradient(name, dtype, tol):
+    c = case(golden("general"), name)
+    data, covs, fam, lnk, cfg, init = _setup(c)
+    from paper_2412_20509_b200.engine import Schedule
+    sch = Schedule(*c["y"].shape, cfg)
+    mb = gk.Minibatch(sch.row_blocks[int(c["first_block"])], sch.col_blocks[0])
+    g = gk.minibatch_gradients(init, data, covs, fam, lnk, gk.PenaltyConfig(), mb, dtype=dtype)
+    for mine, key in ((g.g_rowside, "g0_g_row"), (g.h_rowside, "g0_h_row"),
+                      (g.g_colside, "g0_g_col"), (g.h_colside, "g0_h_col")):
+        assert normwise(mine, c[key]) < tol, key
+
+
+def test_general_wide_bucket_and_objective():
+    """K = p+q+d in (16, 32] runs the second general bucket; penalized_objective
+    of a non-count family on the GPU against the oracle."""
+    rng = np.random.default_rng(5)
+    n, m, d = 300, 40, 18
+    x = np.ones((n, 1))
+    u, v = rng.normal(0, 0.15, (n, d)), rng.normal(0, 0.15, (m, d))
+    b = rng.normal(2.0, 0.1, (m, 1))
+    y = u @ v.T + x @ b.T + rng.normal(0, 0.5, (n, m))
+    st = gk.FactorizationState(b, np.zeros((n, 0)), u, v, 0.7, 1.0)
+    data, covs = gk.ResponseMatrix(y), gk.CovariateSet(x=x, m=m)
+    pen = gk.PenaltyConfig()
+    got = gk.penalized_objective(st, data, covs, gk.Gaussian(), gk.Identity(), pen)
+    pb = orc.OProblem(y, x, np.zeros((m, 0)))
+    ost = orc.OState(b, np.zeros((n, 0)), u, v, 0.7, 1.0)
+    want = orc.penalized_objective(ost, pb, orc.GAUSSIAN, orc.IDENTITY, (0.0, 0.0, 1.0, 0.0))
+    assert abs(got - want) < 1e-10 * abs(want)
+    cfg = gk.SgdConfig(max_epochs=6, mb_rows=100, mb_cols=m, tol=1e-30, seed=2)
+    final, rep = gk.fit_asgd(data, covs, gk.Gaussian(), gk.Identity(), pen, cfg, st, dtype="f64")
+    ocfg = orc.OConfig(max_epochs=6, mb_rows=100, mb_cols=m, tol=1e-30, seed=2)
+    ofinal, orep = orc.fit_asgd(pb, orc.GAUSSIAN, orc.IDENTITY, (0.0, 0.0, 1.0, 0.0), ocfg, ost)
+    assert normwise(rep.objective_trace, orep.objective_trace) < 1e-9
+    assert normwise(rep.phi_trace, orep.phi_trace) < 1e-9
+    assert normwise(final.u @ final.v.T, ofinal.u @ ofinal.v.T) < 1e-7
+
+
+def test_general_mode_limits():
+    """What general mode refuses, with the reference's error taxonomy."""
+    from paper_2412_20509_b200 import _lib
+    rng = np.random.default_rng(0)
+    n, m, d = 60, 12, 2
+    y = rng.gamma(2.0, 1.0, (n, m))
+    st = gk.FactorizationState(np.zeros((m, 1)), np.zeros((n, 0)), rng.normal(0, .1, (n, d)),
+                               rng.normal(0, .1, (m, d)), 1.0, 1.0)
+    covs = gk.CovariateSet(x=np.ones((n, 1)), m=m)
+    cfg = gk.SgdConfig(max_epochs=2, mb_rows=30, mb_cols=m)
+    bad = y.copy()
+    bad[3, 4] = -1.0
+    with pytest.raises(gk.DomainError):      # gamma responses must be positive
+        gk.fit_asgd(gk.ResponseMatrix(bad), covs, gk.Gamma(), gk.Log(), gk.PenaltyConfig(), cfg, st)
+    mask = np.ones((n, m), bool)
+    mask[0, 0] = False
+    with pytest.raises(_lib.UnsupportedError):   # no imputation in general mode
+        gk.fit_asgd(gk.ResponseMatrix(np.where(mask, y, np.nan), mask=mask), covs, gk.Gamma(),
+                    gk.Log(), gk.PenaltyConfig(), cfg, st)
