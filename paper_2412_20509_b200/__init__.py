@@ -19,7 +19,7 @@ from .model import (CovariateSet, FactorizationState, PenaltyConfig, ResponseMat
                     parameter_count, penalty_value)
 from .optim import (FitReport, SgdConfig, bias_correction, fit_asgd, impute_block,  # noqa: F401
                     learning_rate, linear_predictor, penalized_objective, smooth_update,
-                    update_nb_shape_stochastic)
+                    update_dispersion_stochastic, update_nb_shape_stochastic)
 from .initialization import InitMethod, init_glm_svd, init_ols_svd  # noqa: F401
 from .metrics import EvalResult, rel_deviance, rel_log_rmse  # noqa: F401
 from .select import (RankSelectionReport, cv_rank_select, elbow_pick, holdout_mask,  # noqa: F401

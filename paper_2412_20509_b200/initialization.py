@@ -284,34 +284,106 @@ def _xlogy_ratio(y, mu):
 
 
 def _dev0(kind, alpha, y, mu):
-    """Unit deviance without weights (families.py:362-363, 422-425)."""
+    """Unit deviance without weights (families.py:267-425, every family)."""
     import torch
     if kind == "poisson":
         return 2.0 * (_xlogy_ratio(y, mu) - (y - mu))
-    return 2.0 * (_xlogy_ratio(y, mu) - (y + alpha) * torch.log1p((y - mu) / (mu + alpha)))
+    if kind == "neg_binomial":
+        return 2.0 * (_xlogy_ratio(y, mu) - (y + alpha) * torch.log1p((y - mu) / (mu + alpha)))
+    if kind == "gaussian":
+        return (y - mu) ** 2
+    if kind == "gamma":
+        return 2.0 * ((y - mu) / mu - torch.log(y / mu))
+    if kind == "inverse_gaussian":
+        return (y - mu) ** 2 / (y * mu ** 2)
+    mc = torch.clamp(mu, 1e-10, 1.0 - 1e-10)          # bernoulli (families.py:389-391)
+    return 2.0 * (_xlogy_ratio(y, mc) + _xlogy_ratio(1.0 - y, 1.0 - mc))
 
 
-def _derivs(kind, alpha, y, eta, w):
-    """Log-link dotD / ddotD with phi = 1 (_core.pyx:79-103)."""
+def _mean(link, eta):
+    """g^{-1}(eta) (kernels/_ref.py:21-32)."""
     import torch
-    mu = torch.exp(eta)
-    r = y - mu
+    if link == "identity":
+        return eta
+    if link == "log":
+        return torch.exp(eta)
+    if link == "logit":
+        return torch.sigmoid(eta)
+    if link == "inverse":
+        return 1.0 / eta
+    return 1.0 / torch.sqrt(eta)
+
+
+def _variance(kind, alpha, mu):
+    if kind == "gaussian":
+        return mu * 0 + 1.0
+    if kind == "gamma":
+        return mu * mu
+    if kind == "inverse_gaussian":
+        return mu * mu * mu
     if kind == "poisson":
+        return mu
+    if kind == "bernoulli":
+        return mu * (1.0 - mu)
+    return mu * (1.0 + mu / alpha)
+
+
+def _derivs(kind, alpha, y, eta, w, link="log"):
+    """dotD / ddotD with phi = 1: the canonical pairs' simplified forms, else
+    -w r / (nu g'), w / (nu g'^2) (kernels/_ref.py:96-117)."""
+    import torch
+    mu = _mean(link, eta)
+    r = y - mu
+    pair = (kind, link)
+    if pair == ("poisson", "log"):
         return -w * r, w * mu
-    inv = 1.0 / (1.0 + mu / alpha)
-    return -w * r * inv, w * mu * inv
+    if pair == ("neg_binomial", "log"):
+        inv = 1.0 / (1.0 + mu / alpha)
+        return -w * r * inv, w * mu * inv
+    if pair == ("bernoulli", "logit"):
+        return -w * r, w * mu * (1.0 - mu)
+    if pair == ("gaussian", "identity"):
+        return -w * r, w * torch.ones_like(mu)
+    if pair == ("gamma", "inverse"):
+        return w * r, w * mu * mu
+    if pair == ("inverse_gaussian", "inverse_squared"):
+        return w * r / 2.0, w * mu ** 3 / 4.0
+    nu = _variance(kind, alpha, mu)
+    g1 = {"identity": lambda: torch.ones_like(mu), "log": lambda: 1.0 / mu,
+          "logit": lambda: 1.0 / (mu * (1.0 - mu)), "inverse": lambda: -1.0 / (mu * mu),
+          "inverse_squared": lambda: -2.0 / mu ** 3}[link]()
+    return -w * r / (nu * g1), w / (nu * g1 * g1)
 
 
-def _batched_deviance(kind, alpha, y, w, eta):
+def _batched_deviance(kind, alpha, y, w, eta, link="log"):
     """Per-problem weighted deviance (glm.py:27-33): NaN-safe at dropped entries."""
     import torch
-    mu = torch.exp(eta)
-    dev = _dev0(kind, alpha, y, mu)
+    dev = _dev0(kind, alpha, y, _mean(link, eta))
     return torch.where(w > 0, w * dev, torch.zeros_like(dev)).sum(0)
 
 
+def _perturbed_transform(link, y, eps):
+    """g_eps(y) (initialization.py:47-59)."""
+    import torch
+    if link == "identity":
+        return y.clone()
+    if link == "log":
+        return torch.log(y + eps)
+    if link == "logit":
+        c = torch.clamp(y, eps, 1.0 - eps)
+        return torch.log(c / (1.0 - c))
+    c = torch.clamp(y, min=eps)
+    return 1.0 / c if link == "inverse" else 1.0 / (c * c)
+
+
+_ETA_CLIP = {"log": (-700.0, 700.0), "logit": (-700.0, 700.0), "inverse": (1e-8, float("inf")),
+             "inverse_squared": (1e-8, float("inf")),
+             "identity": (-float("inf"), float("inf"))}   # initialization.py:217-225
+_SAFE_FILL = {"bernoulli": 0.5, "gaussian": 0.0}           # initialization.py:117-120, else 1.0
+
+
 def fit_glm_batched(y, w, design, kind, alpha, offset=None, coef0=None, damping=1e-8,
-                    max_iter=50, tol=1e-10, max_halvings=12):
+                    max_iter=50, tol=1e-10, max_halvings=12, link="log"):
     """Batched penalized Fisher scoring for the m column GLMs of y (n x m) on a
     shared design (glm.py:68-133; lam = 0), all problems on the GPU at once:
     eta, the derivatives and the deviances are n x m device arrays, the m
@@ -328,14 +400,14 @@ def fit_glm_batched(y, w, design, kind, alpha, offset=None, coef0=None, damping=
     keep = w > 0
 
     def deviance(c):
-        return _batched_deviance(kind, alpha, y, w, design @ c.T + off)
+        return _batched_deviance(kind, alpha, y, w, design @ c.T + off, link)
 
     dev = deviance(coef)
     active = torch.ones(m, dtype=torch.bool, device=dev_)
     converged = torch.zeros(m, dtype=torch.bool, device=dev_)
     for _ in range(max_iter):
         eta = design @ coef.T + off
-        dotd, ddotd = _derivs(kind, alpha, y, eta, w)
+        dotd, ddotd = _derivs(kind, alpha, y, eta, w, link)
         dotd = torch.where(keep, dotd, torch.zeros_like(dotd))
         ddotd = torch.where(keep, ddotd, torch.zeros_like(ddotd))
         grad = dotd.T @ design
@@ -382,10 +454,11 @@ def _ols_stage_dense(y_eps, w, design, offset):
     return -torch.linalg.solve(hess, grad[:, :, None])[:, :, 0]
 
 
-def _glm_or_fallback(y, w, design, kind, alpha, offset, coef_fallback, info, label):
+def _glm_or_fallback(y, w, design, kind, alpha, offset, coef_fallback, info, label, link="log"):
     """initialization.py:123-134: non-converged problems keep the OLS seed."""
     import torch
-    coef, conv = fit_glm_batched(y, w, design, kind, alpha, offset=offset, coef0=coef_fallback)
+    coef, conv = fit_glm_batched(y, w, design, kind, alpha, offset=offset, coef0=coef_fallback,
+                                 link=link)
     bad = ~conv
     if bool(bad.any()):
         coef = torch.where(bad[:, None], coef_fallback, coef)
@@ -425,27 +498,23 @@ def init_glm_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
     Pearson) residual SVD for U, column GLMs on U for V -- every batched GLM a
     set of n x m device arrays and one batched (p x p) solve per Fisher step;
     non-converged problems fall back to their OLS seeds as in the reference.
-    Handles unobserved entries and prior weights (zero weight at holes).
-    Scope: Poisson / negative binomial with the log link (the fit's device
-    scope); returns a host state."""
+    Handles unobserved entries and prior weights (zero weight at holes), every
+    family and link of the reference, and the Pearson start of phi for the
+    free-dispersion families (initialization.py:85-90); returns a host state."""
     import torch
     method = method or InitMethod()
     n, m = data.shape
     if d > min(n, m):
         raise ConfigError("rank d cannot exceed min(n, m)")
-    if fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log":
-        raise _lib.UnsupportedError(
-            f"device initialization implements poisson/neg_binomial with log link, "
-            f"got {fam.kind}+{lnk.kind}")
     _lib.require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else
                        int(str(device).split(":")[-1]))
-    kind = fam.kind
+    kind, link = fam.kind, lnk.kind
     alpha = float(getattr(fam, "nb_shape", 1.0))
     eps = method.eps_for(lnk)
     Y, mask, W = _dense_inputs(data, dev)
-    y_safe = torch.where(mask, Y, torch.ones_like(Y))          # _safe_y: fill 1.0
-    y_eps = torch.log(y_safe + eps)                            # perturbed_transform (log)
+    y_safe = torch.where(mask, Y, torch.full_like(Y, _SAFE_FILL.get(kind, 1.0)))   # _safe_y
+    y_eps = _perturbed_transform(link, y_safe, eps)
     X = torch.from_numpy(np.ascontiguousarray(covs.x, dtype=float)).to(dev)
     Z = torch.from_numpy(np.ascontiguousarray(covs.z, dtype=float)).to(dev)
     p, q = X.shape[1], Z.shape[1]
@@ -454,19 +523,18 @@ def init_glm_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
     # stage 1: column regressions for B
     b = _ols_stage_dense(y_eps, W, X, None)
     if p:
-        b = _glm_or_fallback(y_safe, W, X, kind, alpha, None, b, info, "b")
+        b = _glm_or_fallback(y_safe, W, X, kind, alpha, None, b, info, "b", link)
     offset = X @ b.T
     # stage 2: row regressions for Gamma given the column effects
     gamma = _ols_stage_dense(y_eps.T, W.T, Z, offset.T)
     if q:
         gamma = _glm_or_fallback(y_safe.T.contiguous(), W.T.contiguous(), Z, kind, alpha,
-                                 offset.T.contiguous(), gamma, info, "gamma")
+                                 offset.T.contiguous(), gamma, info, "gamma", link)
     eta0 = offset + (gamma @ Z.T if q else 0.0)
-    mu0 = torch.exp(torch.clamp(eta0, *_ETA_CLIP_LOG))
+    mu0 = _mean(link, torch.clamp(eta0, *_ETA_CLIP[link]))
     # stage 3: residual SVD for the latent scores (initialization.py:103-114)
     if method.residual_kind == "pearson":
-        var = mu0 if kind == "poisson" else mu0 * (1.0 + mu0 / alpha)
-        r = (Y - mu0) * torch.sqrt(W / var)
+        r = (Y - mu0) * torch.sqrt(W / _variance(kind, alpha, mu0))
     else:
         ud = W * _dev0(kind, alpha, Y, mu0)
         r = torch.sign(Y - mu0) * torch.sqrt(torch.clamp(ud, min=0.0))
@@ -476,7 +544,7 @@ def init_glm_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
     # stage 4: column regressions for V with U as the design
     if d > 0:
         v0 = _ols_stage_dense(torch.where(mask, y_eps - eta0, torch.zeros_like(Y)), W, u, None)
-        v = _glm_or_fallback(y_safe, W, u, kind, alpha, eta0, v0, info, "v")
+        v = _glm_or_fallback(y_safe, W, u, kind, alpha, eta0, v0, info, "v", link)
     else:
         v = torch.zeros((m, 0), dtype=torch.float64, device=dev)
     nb_shape = 1.0
@@ -484,6 +552,11 @@ def init_glm_svd(data: ResponseMatrix, covs: CovariateSet, fam, lnk, d: int,
         num = float((torch.where(mask, W * mu0 ** 2, torch.zeros_like(Y))).sum().item())
         den = float((torch.where(mask, W * ((Y - mu0) ** 2 - mu0), torch.zeros_like(Y))).sum().item())
         nb_shape = 1e8 if den <= 0 else float(np.clip(num / den, 1e-4, 1e8))
+    phi = 1.0
+    if fam.has_free_dispersion:     # initialization.py:85-90 at mu0
+        r2 = torch.where(mask, W * (Y - mu0) ** 2 / _variance(kind, alpha, mu0), torch.zeros_like(Y))
+        dof = max(int(mask.sum().item()) - (p * m + q * n + (n + m) * d + 1), 1)
+        phi = float(r2.sum().item()) / dof
     host = lambda t: t.cpu().numpy()
-    state = FactorizationState(host(b), host(gamma), host(u), host(v), 1.0, nb_shape)
+    state = FactorizationState(host(b), host(gamma), host(u), host(v), phi, nb_shape)
     return (state, info) if return_info else state

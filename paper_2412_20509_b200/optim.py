@@ -27,7 +27,7 @@ from . import _lib
 from .engine import DeviceFit, Schedule
 from .exceptions import ConfigError, DivergenceError
 from .identify import _Dev, project_on_device
-from .model import FactorizationState, penalty_value
+from .model import FactorizationState, parameter_count, penalty_value
 
 __all__ = ["SgdConfig", "FitReport", "learning_rate", "smooth_update", "bias_correction",
            "fit_asgd"]
@@ -443,6 +443,65 @@ def impute_block(state: FactorizationState, data, covs, lnk, mb, *, offset=None,
             mu = torch.exp(_eta_block_device(state, covs, I, J, dev, offset)).cpu().numpy()
             block[miss] = mu[miss]
     return block
+
+
+def _mean_device(lnk, eta):
+    """mu = g^{-1}(eta) on the device through the C ABI seam (kernels/_ref.py:21-32)."""
+    import torch
+    mu = torch.empty_like(eta)
+    st = torch.cuda.current_stream(eta.device).cuda_stream
+    _lib.check(_lib.lib().gmf_mean_of_eta(_lib.LINK_CODES[lnk.kind], _lib.F64, _lib.ptr(eta),
+                                          _lib.ptr(mu), eta.numel(), st), "gmf_mean_of_eta")
+    return mu
+
+
+def _variance_device(fam, mu):
+    kind = fam.kind
+    if kind == "gaussian":
+        return mu * 0 + 1.0
+    if kind == "gamma":
+        return mu * mu
+    if kind == "inverse_gaussian":
+        return mu * mu * mu
+    if kind == "poisson":
+        return mu
+    if kind == "bernoulli":
+        return mu * (1.0 - mu)
+    return mu * (1.0 + mu / float(fam.nb_shape))
+
+
+def update_dispersion_stochastic(state: FactorizationState, data, covs, fam, mb, rate: float,
+                                 lnk=None, y_block=None, mu_block=None, *, offset=None,
+                                 device=None) -> float:
+    """Smoothed stochastic Pearson update of phi (optim.py:175-202):
+    phi_hat = (1/N) (nm / n* m*) sum_B w (y - mu)^2 / nu(mu) with
+    N = nm - mp - nq - (n+m)d - 1; the block sums run on the GPU in fp64
+    (inside a fit the same sum is fused into K1)."""
+    import torch
+    n, m = data.shape
+    dof = n * m - parameter_count(n, m, covs.p, covs.q, state.rank)
+    if dof <= 0:
+        raise ConfigError("model is over-parameterized: nonpositive residual dof")
+    I, J = np.asarray(mb.row_idx), np.asarray(mb.col_idx)
+    ix = np.ix_(I, J)
+    dev = _dev_index(device)
+    if mu_block is None:
+        if lnk is None:
+            raise ConfigError("mu_block or lnk needed")
+        mu = _mean_device(lnk, _eta_block_device(state, covs, I, J, dev, offset).contiguous())
+    else:
+        mu = torch.from_numpy(np.asarray(mu_block, dtype=float)).to(dev)
+    if y_block is None:
+        vals = data.dense()[ix]
+        y_np = vals if data.csr is not None else np.where(data.mask[ix], vals, np.nan)
+        y = torch.from_numpy(np.asarray(y_np, dtype=float)).to(dev)
+        y = torch.where(torch.isnan(y), mu, y)
+    else:
+        y = torch.from_numpy(np.asarray(y_block, dtype=float)).to(dev)
+    w = (torch.ones_like(mu) if data.weights is None else
+         torch.from_numpy(np.asarray(data.weights[ix], dtype=float)).to(dev))
+    s = float((w * (y - mu) ** 2 / _variance_device(fam, mu)).sum().item())
+    return (1.0 - rate) * state.phi + rate * (s * (n * m) / (I.size * J.size) / dof)
 
 
 def update_nb_shape_stochastic(state: FactorizationState, data, mb, rate: float,

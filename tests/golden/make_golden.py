@@ -700,8 +700,27 @@ def make_general():
     return out
 
 
+def make_init_general():
+    """init_glm_svd of the reference for the general families / links, incl.
+    the Pearson start of phi (initialization.py:85-90, 172-214)."""
+    out = {"cases": np.asarray([c[0] for c in GENERAL_CASES])}
+    for name, fk, lk, disp, (p, q, d), seed in GENERAL_CASES:
+        n, m = 240, 40
+        y, x, z, _ = _general_problem(fk, lk, n, m, p, q, d, seed + 100)
+        data = gk.ResponseMatrix(y.astype(float))
+        covs = gk.CovariateSet(x=x if p else None, z=z if q else None, n=n, m=m)
+        st, info = gk.init_glm_svd(data, covs, gk.family(fk), gk.link(lk), d, seed=5,
+                                   return_info=True)
+        out.update({f"{name}__y": y, f"{name}__x": x, f"{name}__z": z, f"{name}__d": np.int64(d),
+                    f"{name}__family": np.asarray(fk), f"{name}__link": np.asarray(lk),
+                    f"{name}__b": st.b, f"{name}__gamma": st.gamma, f"{name}__uv": st.u @ st.v.T,
+                    f"{name}__phi": np.float64(st.phi),
+                    f"{name}__fallbacks": np.asarray(str(info.get("glm_fallbacks", {})))})
+    return out
+
+
 def main():
-    makers = {"general": make_general, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
+    makers = {"general": make_general, "init_general": make_init_general, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,

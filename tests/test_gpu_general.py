@@ -131,3 +131,52 @@ def test_general_mode_limits():
     with pytest.raises(_lib.UnsupportedError):   # no imputation in general mode
         gk.fit_asgd(gk.ResponseMatrix(np.where(mask, y, np.nan), mask=mask), covs, gk.Gamma(),
                     gk.Log(), gk.PenaltyConfig(), cfg, st)
+
+
+def test_update_dispersion_stochastic_matches_oracle():
+    c = case(golden("general"), "gamma_log")
+    data, covs, fam, lnk, cfg, init = _setup(c)
+    from paper_2412_20509_b200.engine import Schedule
+    sch = Schedule(*c["y"].shape, cfg)
+    I, J = sch.row_blocks[0], sch.col_blocks[0]
+    got = gk.update_dispersion_stochastic(init, data, covs, fam, gk.Minibatch(I, J), 0.3, lnk)
+    pb = orc.OProblem(c["y"].astype(float), c["x"], c["z"])
+    ost = orc.OState(c["init_b"], c["init_gamma"], c["init_u"], c["init_v"], 1.0, 1.0)
+    y, w, mu, _, _ = orc.block_derivs(ost, pb, I, J, orc.GAMMA, orc.LOG)
+    n, m = c["y"].shape
+    want = orc.pearson_phi_update(1.0, 0.3, y, mu, w, orc.GAMMA, 1.0, n, m, len(I), len(J),
+                                  c["x"].shape[1], c["z"].shape[1], c["init_u"].shape[1])
+    assert abs(got - want) < 1e-12 * abs(want)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_init_glm_svd_general_matches_reference(name):
+    """The reference's default start for every family / link, with the Pearson
+    start of phi (initialization.py:85-90, 172-214)."""
+    c = case(golden("init_general"), name)
+    n, m = c["y"].shape
+    data = gk.ResponseMatrix(c["y"].astype(float))
+    covs = gk.CovariateSet(x=c["x"] if c["x"].shape[1] else None,
+                           z=c["z"] if c["z"].shape[1] else None, n=n, m=m)
+    st, info = gk.init_glm_svd(data, covs, gk.family(str(c["family"])), gk.link(str(c["link"])),
+                               int(c["d"]), seed=5, return_info=True)
+    assert str(info.get("glm_fallbacks", {})) == str(c["fallbacks"])
+    assert normwise(st.b, c["b"]) < 1e-7
+    if c["gamma"].size:
+        assert normwise(st.gamma, c["gamma"]) < 1e-7
+    assert normwise(st.u @ st.v.T, c["uv"]) < 1e-6
+    assert st.phi == pytest.approx(float(c["phi"]), rel=1e-8)
+
+
+def test_fit_asgd_rank_only_general_family():
+    """fit_asgd(rank=d) for a non-count family: GLM-SVD start, then general mode."""
+    c = case(golden("init_general"), "gamma_log")
+    n, m = c["y"].shape
+    data = gk.ResponseMatrix(c["y"].astype(float))
+    covs = gk.CovariateSet(x=c["x"], n=n, m=m)
+    cfg = gk.SgdConfig(max_epochs=6, mb_rows=80, mb_cols=m, tol=1e-30, seed=5)
+    final, rep = gk.fit_asgd(data, covs, gk.Gamma(), gk.Log(), gk.PenaltyConfig(), cfg,
+                             rank=int(c["d"]))
+    assert rep.epochs_run == 6 and np.all(np.isfinite(rep.objective_trace))
+    assert rep.phi_trace[0] == pytest.approx(float(c["phi"]), rel=1e-8)
+    assert rep.phi_trace[-1] != rep.phi_trace[0]
