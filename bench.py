@@ -335,6 +335,46 @@ def _aux_legs(wl, data, covs, st, fam, dev, reps=3):
                                                   "sketches; host CSR upload included"}}
 
 
+def _fp64_c2_leg(dev, steps=2000, warmup=50):
+    """The reference's own precision beside the fp32 headline: BASELINE config
+    2 (26,472 x 500 NB, k = 15, offset, dense, mb 2,000 rows) in fp64 on the
+    CUDA-core K1, one persistent launch of `steps` aSGD steps, CUDA events."""
+    import torch
+    import paper_2412_20509_b200 as gk
+    from paper_2412_20509_b200 import workloads
+    from paper_2412_20509_b200.engine import DeviceFit, Schedule
+    wl = workloads.generate("c2", device=str(dev))
+    sp = wl.spec
+    data = gk.ResponseMatrix(wl.y_dense.astype(float))
+    covs = gk.CovariateSet(x=wl.x, z=wl.z if sp.q else None, m=sp.m)
+    st = gk.FactorizationState(**wl.init_state())
+    cfg = gk.SgdConfig(max_epochs=warmup + steps + 8, mb_rows=sp.mb_rows, mb_cols=sp.m,
+                       tol=1e-30, seed=0)
+    sched = Schedule(sp.n, sp.m, cfg)
+    fit = DeviceFit(data, covs, gk.NegBinomial(st.nb_shape), gk.Log(), gk.PenaltyConfig(), cfg, st,
+                    schedule=sched, offset=wl.offset, dtype="f64", device=dev.index,
+                    est_alpha=True)
+    try:
+        fit.reset()
+        fit.run(warmup)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fit.run(steps)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        status = fit.status()
+        assert status.t == warmup + steps and not status.stopped
+        sizes = np.array([b.size for b in sched.row_blocks])
+        entries = float(sizes[sched.block_seq[warmup:warmup + steps]].sum()) * sp.m
+    finally:
+        fit.close()
+    return {"workload": _workload_desc("c2"), "dtype": "f64", "k1_impl": fit.k1_impl,
+            "steps": steps, "warmup": warmup, "ms_per_step": ms / steps,
+            "value": entries / (ms / 1e3), "unit": UNIT}
+
+
 def _workload_desc(name):
     return {
         "c1": "c1: Poisson GMF 1,000 x 100, k=5, X=Z=1, dense int32, mb 100 rows x all columns, fp64",
@@ -606,6 +646,12 @@ def main():
             aux = _aux_legs(wl, data, covs, st, fam, dev)
         except Exception as err:   # reported, never fatal to the headline line
             aux = {"error": f"{type(err).__name__}: {err}"}
+    fp64_c2 = None
+    if rank == 0 and world == 1 and not args.no_aux and args.config == "c4":
+        try:
+            fp64_c2 = _fp64_c2_leg(dev)
+        except Exception as err:
+            fp64_c2 = {"error": f"{type(err).__name__}: {err}"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -622,6 +668,7 @@ def main():
                        "geometry": geometry, "k1_impl": fit.k1_impl, "y_storage": fit.y_format},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(timed_launches), "clocks": clocks, "aux": aux,
+            "fp64_c2": fp64_c2,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

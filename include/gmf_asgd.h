@@ -143,6 +143,10 @@ typedef struct gmf_desc {
    K1 runs on the CUDA cores with the family and link chosen at run time,
    p+q+d <= 32 */
 #define GMF_DESC_REAL_RESPONSE 2
+/* evaluation-only handle: holds a state for gmf_entries_eval (mu at listed
+   entries, held-out scores; select.py:141-145) under ANY family / link, with
+   an empty response; the fit, gradient and deviance calls return GMF_ERR_STATE */
+#define GMF_DESC_EVAL_ONLY 4
 
 typedef struct gmf_config {   /* SgdConfig (optim.py:61-106) + penalty (model.py:193-226) */
   double rate_k0, rate_k1, rate_tau;

@@ -54,6 +54,8 @@ class GmfDesc(C.Structure):
 DESC_TAIL_PADDED = 1
 # general mode: real-valued response in y_work, family / link at run time
 DESC_REAL_RESPONSE = 2
+# evaluation-only handle (gmf_entries_eval under any family / link)
+DESC_EVAL_ONLY = 4
 
 
 class GmfConfig(C.Structure):

@@ -85,7 +85,8 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
   if (d->link < GMF_IDENTITY || d->link > GMF_INVERSE_SQUARED) { set_error("unknown link code %d", d->link); return GMF_ERR_DOMAIN; }
   const bool fused = d->link == GMF_LOG && (d->family == GMF_POISSON || d->family == GMF_NEG_BINOMIAL);
   const bool real = (d->flags & GMF_DESC_REAL_RESPONSE) != 0;
-  if (!fused && !real) {
+  const bool eval_only = (d->flags & GMF_DESC_EVAL_ONLY) != 0;
+  if (!fused && !real && !eval_only) {
     set_error("family %d with link %d runs in general mode: pass the response as y_work with "
               "GMF_DESC_REAL_RESPONSE", d->family, d->link);
     return GMF_ERR_UNSUPPORTED;
@@ -615,6 +616,7 @@ int gmf_reset(gmf_handle* h, double nb_shape, void* stream) {
 int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, double nb_shape,
                        void* g_row, void* h_row, void* g_col, void* h_col, double* nb_sums,
                        void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h) { set_error("null handle"); return GMF_ERR_STATE; }
   const Params& P = h->P;
   if (row_block < 0 || row_block >= P.R || col_block < 0 || col_block >= P.S) {
@@ -635,6 +637,7 @@ int gmf_minibatch_grad(gmf_handle* h, int64_t row_block, int64_t col_block, doub
 }
 
 int gmf_step_local(gmf_handle* h, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !h->reset_done) { set_error("gmf_step_local before gmf_reset"); return GMF_ERR_STATE; }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_obj(h->P, h->desc.dtype, st);
@@ -663,6 +666,7 @@ int gmf_record_copy(gmf_handle* h, void* dst, void* stream) {
 }
 
 int gmf_run(gmf_handle* h, int64_t n_steps, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !h->reset_done) { set_error("gmf_run before gmf_reset"); return GMF_ERR_STATE; }
   if (h->desc.world_size != 1) { set_error("gmf_run is single-rank; use step_local/step_apply"); return GMF_ERR_STATE; }
   if (n_steps <= 0) return GMF_OK;
@@ -795,6 +799,7 @@ int gmf_status_decode(const void* raw, gmf_status* out) {
 }
 
 int gmf_time_grad(gmf_handle* h, int64_t row_block, int32_t iters, double* avg_ms, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !avg_ms || iters < 1) { set_error("gmf_time_grad: bad arguments"); return GMF_ERR_CONFIG; }
   if (row_block < 0 || row_block >= h->P.R) { set_error("row block out of range"); return GMF_ERR_CONFIG; }
   GMF_CUDA(cudaSetDevice(h->desc.device));
@@ -844,6 +849,7 @@ int gmf_trace_phi_read(gmf_handle* h, double* phi, int64_t n, void* stream) {
 }
 
 int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !dev_sum) { set_error("null handle/out"); return GMF_ERR_STATE; }
   gmf_status s;
   int rc = gmf_status_read(h, &s, stream);
@@ -854,11 +860,12 @@ int gmf_objective_full(gmf_handle* h, double* dev_sum, void* stream) {
 }
 
 int gmf_loglik_full(gmf_handle* h, double* out2, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !out2) { set_error("null handle/out"); return GMF_ERR_STATE; }
   gmf_status s;
   int rc = gmf_status_read(h, &s, stream);
   if (rc) return rc;
-  const int nb = h->desc.family == GMF_NEG_BINOMIAL;
+  const int nb = h->desc.family == GMF_NEG_BINOMIAL && !h->P.gen;   // general mode: caller adds c(phi)
   cudaStream_t st = (cudaStream_t)stream;
   if (!nb) GMF_CUDA(cudaMemsetAsync(out2 + 1, 0, sizeof(double), st));
   h->launches += 1;
@@ -887,6 +894,7 @@ int gmf_entries_eval(gmf_handle* h, const int64_t* rows, const int32_t* cols, co
 void* gmf_stream_ready_ptr(gmf_handle* h) { return h ? (void*)h->P.ready : nullptr; }
 
 int gmf_run_stream(gmf_handle* h, int64_t n_steps, void* host_status, void* stream) {
+  if (h && (h->desc.flags & GMF_DESC_EVAL_ONLY)) { set_error("evaluation-only handle (GMF_DESC_EVAL_ONLY): no fit, gradient or deviance calls"); return GMF_ERR_STATE; }
   if (!h || !h->reset_done) { set_error("gmf_run_stream before gmf_reset"); return GMF_ERR_STATE; }
   if (h->desc.world_size != 1) { set_error("gmf_run_stream is single-rank"); return GMF_ERR_STATE; }
   if (h->fit_grid <= 0) { set_error("gmf_run_stream needs the persistent fit kernel"); return GMF_ERR_UNSUPPORTED; }

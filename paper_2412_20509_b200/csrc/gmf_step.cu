@@ -383,7 +383,7 @@ constexpr int kFullRows = 32, kFullCols = 64;
 GMF_HD int full_stride(int K) { return K | 1; }
 GMF_HD int full_smem_bytes(int K) { return (kFullRows + kFullCols) * full_stride(K) * 8; }
 
-template <typename T>
+template <typename T, bool GEN = false>
 __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, int with_const,
                                                       double* part, unsigned int* ticket,
                                                       double* out) {
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
           if (cc >= nc) continue;
           const int64_t j = j0 + cc;
           const double eta = acc[r][h] + offs[rr];
-          if (P.gen) {   // general mode: real-valued response, any link
+          if constexpr (GEN) {   // general mode: real-valued response, any link
             const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
             s += w * unit_deviance(P.fam, (double)tptr<T>(P.y_work)[i * P.m + j],
                                    gen_mean<double>(P.link, eta), alpha);
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(kThreads) k_entries(Params P, double alpha, co
   double s[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t k = blockIdx.x * (int64_t)kThreads + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * kThreads) {
-    const double mu = exp(eta_at<T>(P, rows[k], cols[k]));
+    const double mu = gen_mean<double>(P.link, eta_at<T>(P, rows[k], cols[k]));
     if (mu_out) mu_out[k] = mu;
     if (out) score_entry(P.fam, y[k], mu, ybar, alpha, s);
   }
@@ -724,11 +724,21 @@ int launch_objfull(const Params& P, int dtype, double alpha, int with_const, dou
   const int K = P.d + P.p + P.q;
   const int smem = full_smem_bytes(K);
   if (dtype == GMF_F64) {
+    if (P.gen) {
+      GMF_CUDA(cudaFuncSetAttribute(k_objfull<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_objfull<double, true><<<grid, kThreads, smem, st>>>(P, alpha, with_const, part, ticket, out);
+    } else {
     GMF_CUDA(cudaFuncSetAttribute(k_objfull<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_objfull<double><<<grid, kThreads, smem, st>>>(P, alpha, with_const, part, ticket, out);
+    }
   } else {
+    if (P.gen) {
+      GMF_CUDA(cudaFuncSetAttribute(k_objfull<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_objfull<float, true><<<grid, kThreads, smem, st>>>(P, alpha, with_const, part, ticket, out);
+    } else {
     GMF_CUDA(cudaFuncSetAttribute(k_objfull<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_objfull<float><<<grid, kThreads, smem, st>>>(P, alpha, with_const, part, ticket, out);
+    }
   }
   GMF_LAUNCH_CHECK("k_objfull");
   return GMF_OK;

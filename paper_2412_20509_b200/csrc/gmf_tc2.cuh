@@ -886,6 +886,28 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
         constexpr uint32_t ID1 = idesc(128, 128, 0, 0);
         constexpr uint32_t ID2 = idesc(128, 64, 0, 0);
         constexpr uint32_t ID3 = idesc(128, 32, 1, 1);
+        // A single thread issues every MMA, so its instruction stream is a
+        // dependent chain: the shared-memory descriptors are unit invariants
+        // (base + a small start-address increment per K step; the 14-bit
+        // address field never carries), built once here, and umma_nc carries
+        // no memory clobber (volatile asm keeps the MMA / commit / wait order),
+        // so the increments are hoisted and overlapped instead of re-derived
+        // between issues.
+        const uint64_t dR = sdesc(sb + (uint32_t)L.R, 128, SBO_P);
+        const uint64_t dB1_0 = sdesc(sb + (uint32_t)L.B1, 128, sbo1);
+        const uint64_t dB1_1 = sdesc(sb + (uint32_t)L.B1 + b1sz, 128, sbo1);
+        const uint64_t dB1_2 = sdesc(sb + (uint32_t)L.B1 + 2 * b1sz, 128, sbo1);
+        const uint64_t dA1 = sdesc(sb + (uint32_t)L.A1, 128, sbo1);   // slot 0, split 0
+        const uint64_t dP2_0 = sdesc(sb + (uint32_t)L.P, 128, SBO_P);           // GEMM2, group 0
+        const uint64_t dP3_0 = sdesc(sb + (uint32_t)L.P, 2048, 128);            // GEMM3 dd, group 0
+        const uint64_t dA3 = sdesc(sb + (uint32_t)L.A3, 0, 128);                // A3 slot 0
+        auto adv = [](uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); };
+        auto umma_nc = [](uint32_t d, uint64_t a, uint64_t bb, uint32_t id, uint32_t acc) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+              "l"(a), "l"(bb), "r"(id), "r"(acc));
+        };
         // GEMM1 runs one chunk ahead of the elementwise warps' demand: in the
         // in-order tensor pipe GEMM1(c+1) precedes GEMM2/3(c-1)
         auto gemm1 = [&](int c) {
@@ -900,22 +922,18 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
           fence_after();
           const uint32_t d = tm + (uint32_t)(128 * slot);
           const uint32_t a1s = gcc % (uint32_t)L.na1;
+          const uint64_t a0b = adv(dA1, a1s * 3u * a1sz);
           #pragma unroll
           for (int kt = 0; kt < nka / 16; ++kt) {
-            const uint32_t ko = (uint32_t)kt * 256u + a1s * 3u * a1sz;
             const uint32_t kb = (uint32_t)kt * 256u;
-            const uint64_t a0 = sdesc(sb + (uint32_t)L.A1 + ko, 128, sbo1);
-            const uint64_t a1 = sdesc(sb + (uint32_t)L.A1 + a1sz + ko, 128, sbo1);
-            const uint64_t a2 = sdesc(sb + (uint32_t)L.A1 + 2 * a1sz + ko, 128, sbo1);
-            const uint64_t b0 = sdesc(sb + (uint32_t)L.B1 + kb, 128, sbo1);
-            const uint64_t b1 = sdesc(sb + (uint32_t)L.B1 + b1sz + kb, 128, sbo1);
-            const uint64_t b2 = sdesc(sb + (uint32_t)L.B1 + 2 * b1sz + kb, 128, sbo1);
-            umma(d, a0, b0, ID1, kt > 0 ? 1u : 0u);
-            umma(d, a0, b1, ID1, 1u);
-            umma(d, a1, b0, ID1, 1u);
-            umma(d, a0, b2, ID1, 1u);
-            umma(d, a1, b1, ID1, 1u);
-            umma(d, a2, b0, ID1, 1u);
+            const uint64_t a0 = adv(a0b, kb), a1 = adv(a0b, a1sz + kb), a2 = adv(a0b, 2 * a1sz + kb);
+            const uint64_t b0 = adv(dB1_0, kb), b1 = adv(dB1_1, kb), b2 = adv(dB1_2, kb);
+            umma_nc(d, a0, b0, ID1, kt > 0 ? 1u : 0u);
+            umma_nc(d, a0, b1, ID1, 1u);
+            umma_nc(d, a1, b0, ID1, 1u);
+            umma_nc(d, a0, b2, ID1, 1u);
+            umma_nc(d, a1, b1, ID1, 1u);
+            umma_nc(d, a2, b0, ID1, 1u);
           }
           umma_commit(&B.eta_full[slot]);
           umma_commit(&B.a1_free[a1s]);
@@ -927,7 +945,7 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
           gemm1(c + 1);
           {
             const uint32_t gp = gc0 + (uint32_t)c;
-            const uint32_t a3 = sb + (uint32_t)L.A3 + (gp & 1u) * 8192u;
+            const uint64_t a3 = adv(dA3, (gp & 1u) * 8192u);
             mbar_wait(&B.p_full, gp & 1u);
             mbar_wait(&B.a3_full[gp & 1u], (gp >> 1) & 1u);
             tick(kt_mm, 11);
@@ -935,13 +953,11 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
             fence_after();
             #pragma unroll
             for (int gg = 0; gg < 2; ++gg) {
-              const uint32_t pg = sb + (uint32_t)L.P + 32768u * gg;
+              const uint64_t p2 = adv(dP2_0, 32768u * gg), p3 = adv(dP3_0, 32768u * gg);
               #pragma unroll
-              for (int kt = 0; kt < TCC / 16; ++kt) {
-                const uint32_t ko = (uint32_t)kt * 256u;
-                umma(tm + T_D2 + 64u * gg, sdesc(pg + ko, 128, SBO_P),
-                     sdesc(sb + (uint32_t)L.R + ko, 128, SBO_P), ID2, kt > 0 ? 1u : 0u);
-              }
+              for (int kt = 0; kt < TCC / 16; ++kt)
+                umma_nc(tm + T_D2 + 64u * gg, adv(p2, 256u * kt), adv(dR, 256u * kt), ID2,
+                        kt > 0 ? 1u : 0u);
               // D3[col][f] += P^T . [a_hi | a_lo] (dd) and P^T . [a2_hi | a2_lo] (hh);
               // K-step u = stacked rows 16u..16u+15 = group rows 8u..8u+7 hi then
               // lo, paired with feature rows 8u..8u+7 twice (LBO 0)
@@ -949,9 +965,8 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
               for (int uu = 0; uu < 4; ++uu) {
                 const uint32_t acc0 = (c == 0 && gg == 0 && uu == 0) ? 0u : 1u;
                 const uint32_t rg = 512u * (uint32_t)(4 * gg + uu);
-                umma(tm + T_D3, sdesc(pg + 4096u * uu, 2048, 128), sdesc(a3 + rg, 0, 128), ID3, acc0);
-                umma(tm + T_D3 + 32, sdesc(pg + 16384u + 4096u * uu, 2048, 128),
-                     sdesc(a3 + 4096u + rg, 0, 128), ID3, acc0);
+                umma_nc(tm + T_D3, adv(p3, 4096u * uu), adv(a3, rg), ID3, acc0);
+                umma_nc(tm + T_D3 + 32, adv(p3, 16384u + 4096u * uu), adv(a3, 4096u + rg), ID3, acc0);
               }
             }
             umma_commit(&B.p_free);

@@ -159,7 +159,8 @@ class DeviceFit:
 
     def __init__(self, data, covs, fam, lnk, penalty, cfg, state: FactorizationState, *,
                  schedule: Schedule, offset=None, dtype="f64", device=None, world=1, rank=0,
-                 est_alpha=False, est_phi=False, k1_impl="auto", y_format="auto"):
+                 est_alpha=False, est_phi=False, k1_impl="auto", y_format="auto",
+                 eval_only=False):
         import torch
         _lib.require_cuda()
         lib = _lib.lib()
@@ -167,7 +168,8 @@ class DeviceFit:
         # link; every other family / link pair, and any fit that estimates phi
         # (optim.py:175-202), runs in general mode: real-valued dense response,
         # family and link chosen at run time on the CUDA-core K1
-        general = est_phi or fam.kind not in ("poisson", "neg_binomial") or lnk.kind != "log"
+        general = (est_phi or fam.kind not in ("poisson", "neg_binomial")
+                   or lnk.kind != "log") and not eval_only
         holes = not data.fully_observed
         if holes and data.csr is not None:
             raise _lib.UnsupportedError("unobserved entries need a dense response")
@@ -318,7 +320,8 @@ class DeviceFit:
                                  has_weights=int(self.weights is not None), world_size=world,
                                  rank=rank, device=dev_index,
                                  flags=_lib.DESC_TAIL_PADDED |
-                                 (_lib.DESC_REAL_RESPONSE if general else 0))
+                                 (_lib.DESC_REAL_RESPONSE if general else 0) |
+                                 (_lib.DESC_EVAL_ONLY if eval_only else 0))
         dof = self.n * self.m - (self.p * self.m + self.q * self.n + self.d * (self.n + self.m) + 1)
         if est_phi and dof <= 0:
             raise ConfigError("model is over-parameterized: nonpositive residual dof")

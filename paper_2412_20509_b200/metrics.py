@@ -84,8 +84,6 @@ def rel_log_rmse(y_test, mu_hat, ybar_train: float, *, device=None) -> float:
 
 def rel_deviance(y_test, mu_hat, ybar_train: float, fam: FamilySpec, *, device=None) -> float:
     """sum D(y, mu_hat) / sum D(y, ybar_train) over the test entries (metrics.py:48-55)."""
-    if fam.kind not in ("poisson", "neg_binomial"):
-        raise _lib.UnsupportedError(f"device scoring implements poisson/neg_binomial, got {fam.kind}")
     s = score_sums(y_test, mu_hat, ybar_train, fam, device=device)
     if s[1] == 0.0:
         raise DegenerateError("all test responses equal the train mean baseline")

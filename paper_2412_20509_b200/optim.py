@@ -338,7 +338,9 @@ def _drive(fit: DeviceFit, callback, group, exchange):
                 st = fit.status()
                 if callback is not None and st.t > prev:
                     # collective: every rank gathers the live state (optim.py:474-475)
-                    callback(int(st.t) - 1, _gathered_state(fit, group, exchange, st.nb_shape))
+                    live = _gathered_state(fit, group, exchange, st.nb_shape)
+                    live.phi = float(st.phi)
+                    callback(int(st.t) - 1, live)
                 if st.stopped:
                     return
         return
@@ -348,7 +350,7 @@ def _drive(fit: DeviceFit, callback, group, exchange):
             fit.run(1)
             st = fit.status()
             if st.t > st0.t:
-                callback(int(st.t) - 1, fit.download_state(nb_shape=st.nb_shape))
+                callback(int(st.t) - 1, fit.download_state(nb_shape=st.nb_shape, phi=st.phi))
             if st.stopped:
                 return
     chunk = 16

@@ -30,14 +30,14 @@ __all__ = ["information_criteria", "loglik_terms", "mu_at", "heldout_scores", "R
            "holdout_mask", "cv_rank_select", "scree_eigenvalues", "residual_scores", "elbow_pick"]
 
 
-def _state_fit(state, data, covs, fam, lnk, offset, dtype, device):
+def _state_fit(state, data, covs, fam, lnk, offset, dtype, device, eval_only=False):
     """A zero-step device handle holding ``state`` over ``data`` (one row block)."""
     from .optim import SgdConfig
     cfg = SgdConfig(max_epochs=1)
     sched = Schedule(state.n, state.m, cfg, row_blocks=[np.arange(state.n)],
                      col_blocks=[np.arange(state.m)], n_steps=0)
     fit = DeviceFit(data, covs, fam, lnk, PenaltyConfig(), cfg, state, schedule=sched,
-                    offset=offset, dtype=dtype, device=device)
+                    offset=offset, dtype=dtype, device=device, eval_only=eval_only)
     fit.reset(fam.nb_shape if fam.kind == "neg_binomial" else 1.0)
     return fit
 
@@ -51,9 +51,39 @@ def loglik_terms(state: FactorizationState, data: ResponseMatrix, covs: Covariat
     fit = _state_fit(state, data, covs, fam, lnk, offset, dtype, device)
     try:
         dev, const = fit.loglik_full()
+        if fit.general:
+            const = _general_constant(fit, data, fam, state.phi)
     finally:
         fit.close()
     return dev, const
+
+
+def _general_constant(fit, data, fam, phi):
+    """c(phi) of select.py:57-79 for a general-mode fit (fully observed):
+    n log phi (Gaussian, inverse Gaussian), 2 sum(lgamma(s) - s log s + s) with
+    s = w / phi (Gamma), the NB saturated terms for a non-log link, else 0."""
+    torch = fit.torch
+    n_obs = data.n * data.m
+    kind = fam.kind
+    if kind in ("gaussian", "inverse_gaussian"):
+        return float(n_obs * np.log(phi))
+    if kind == "gamma":
+        if fit.weights is None:
+            s = 1.0 / phi
+            from math import lgamma
+            return float(2.0 * n_obs * (lgamma(s) - s * np.log(s) + s))
+        s = fit.weights.double() / phi
+        return float((2.0 * (torch.lgamma(s) - s * torch.log(s) + s)).sum().item())
+    if kind == "neg_binomial":
+        a = float(fam.nb_shape)
+        y = fit.y_work.double()
+        w = 1.0 if fit.weights is None else fit.weights.double()
+        sat = (torch.lgamma(y + a) - torch.lgamma(torch.tensor(a, device=y.device, dtype=y.dtype))
+               - torch.lgamma(y + 1.0) - (y + a) * torch.log(y + a) + a * np.log(a))
+        ylogy = torch.where(y > 0, y * torch.log(torch.where(y > 0, y, torch.ones_like(y))),
+                            torch.zeros_like(y))
+        return float((-2.0 * (w * (sat + ylogy))).sum().item())
+    return 0.0
 
 
 def information_criteria(state: FactorizationState, data: ResponseMatrix, covs: CovariateSet,
@@ -89,7 +119,7 @@ def mu_at(state: FactorizationState, covs: CovariateSet, lnk, rows, cols, *, off
     """g^{-1}(eta) at the listed entries (select.py:141-145), on the GPU."""
     empty = ResponseMatrix(csr=(np.zeros(state.n + 1, np.int64), np.zeros(0, np.int32),
                                 np.zeros(0, np.int32)), shape=(state.n, state.m))
-    fit = _state_fit(state, empty, covs, Poisson(), lnk, offset, dtype, device)
+    fit = _state_fit(state, empty, covs, Poisson(), lnk, offset, dtype, device, eval_only=True)
     try:
         r, c = _entries(fit, rows, cols)
         out = fit.torch.empty(r.numel(), dtype=fit.torch.float64, device=fit.device)
@@ -111,12 +141,9 @@ def heldout_scores(state: FactorizationState, covs: CovariateSet, fam, lnk, rows
         raise ConfigError("test set is empty")
     if y.size != np.asarray(rows).size:
         raise ConfigError("y_test and mu_hat must have the same length")
-    if fam.kind not in ("poisson", "neg_binomial"):
-        raise _lib.UnsupportedError(f"device scoring implements poisson/neg_binomial, got {fam.kind}")
     empty = ResponseMatrix(csr=(np.zeros(state.n + 1, np.int64), np.zeros(0, np.int32),
                                 np.zeros(0, np.int32)), shape=(state.n, state.m))
-    fit = _state_fit(state, empty, covs, fam if fam.kind == "neg_binomial" else Poisson(), lnk,
-                     offset, dtype, device)
+    fit = _state_fit(state, empty, covs, fam, lnk, offset, dtype, device, eval_only=True)
     try:
         torch = fit.torch
         r, c = _entries(fit, rows, cols)

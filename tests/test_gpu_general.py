@@ -52,6 +52,7 @@ def test_general_fit_fp64_matches_reference(name):
     for t, st in seen.items():
         for blk in ("b", "gamma", "u", "v"):
             assert normwise(getattr(st, blk), c[f"step{t}_{blk}"]) < 1e-8, (t, blk)
+        assert abs(st.phi - float(c[f"step{t}_phi"])) < 1e-9 * float(c[f"step{t}_phi"])
     assert abs(final.phi - float(c["final_phi"])) < 1e-9 * float(c["final_phi"])
     assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 1e-7
     fo = float(c["final_objective"])
@@ -180,3 +181,31 @@ def test_fit_asgd_rank_only_general_family():
     assert rep.epochs_run == 6 and np.all(np.isfinite(rep.objective_trace))
     assert rep.phi_trace[0] == pytest.approx(float(c["phi"]), rel=1e-8)
     assert rep.phi_trace[-1] != rep.phi_trace[0]
+
+
+@pytest.mark.parametrize("name", ["gauss_id", "gamma_log", "bern_logit", "gamma_inv", "ig_log"])
+def test_model_selection_general_family(name):
+    """information_criteria (with the family's dispersion constant), mu_at and
+    held-out scores for non-count families / links (select.py:57-96, 141-145;
+    metrics.py:35-55) against the oracle."""
+    from paper_2412_20509_b200.select import heldout_scores, information_criteria, mu_at
+    c = case(golden("general"), name)
+    data, covs, fam, lnk, cfg, _ = _setup(c)
+    st = gk.FactorizationState(c["unproj_b"], c["unproj_gamma"], c["unproj_u"], c["unproj_v"],
+                               float(c["unproj_phi"]), 1.0)
+    pb = orc.OProblem(c["y"].astype(float), c["x"], c["z"])
+    ost = orc.OState(st.b, st.gamma, st.u, st.v, st.phi, 1.0)
+    fc, lc = orc.FAMILY_CODES[fam.kind], orc.LINK_CODES[lnk.kind]
+    aic, bic = information_criteria(st, data, covs, fam, lnk)
+    oaic, obic = orc.information_criteria(ost, pb, fc, lc, 1.0)
+    assert abs(aic - oaic) < 1e-10 * abs(oaic) and abs(bic - obic) < 1e-10 * abs(obic)
+    rng = np.random.default_rng(9)
+    rows, cols = rng.integers(0, c["y"].shape[0], 500), rng.integers(0, c["y"].shape[1], 500)
+    mu = mu_at(st, covs, lnk, rows, cols)
+    omu = orc.mu_at(ost, pb, lc, rows, cols)
+    assert normwise(mu, omu) < 1e-12
+    y_test = c["y"][rows, cols].astype(float)
+    ybar = float(c["y"].mean())
+    res = heldout_scores(st, covs, fam, lnk, rows, cols, y_test, ybar)
+    assert res.rel_deviance == pytest.approx(orc.rel_deviance(fc, y_test, omu, ybar, 1.0), rel=1e-10)
+    assert gk.rel_deviance(y_test, omu, ybar, fam) == pytest.approx(res.rel_deviance, rel=1e-10)
