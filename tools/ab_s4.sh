@@ -19,8 +19,8 @@ for f in ('c5','c5b'):
         if 'nstar' in c: print(n,f,c['format'],c['m'],c['d'],'step_us',c['step_us'],'k1_us',c['k1_us'],'%.3e'%c['entries_per_s'])
 PY
 }
-run prev GMF_LIB_PATH=/root/repo/alt/prev/libgmf_asgd.so
+run head GMF_LIB_PATH=/root/repo/alt/head/libgmf_asgd.so
 run new A=1
-run prev2 GMF_LIB_PATH=/root/repo/alt/prev/libgmf_asgd.so
+run head2 GMF_LIB_PATH=/root/repo/alt/head/libgmf_asgd.so
 run new2 A=1
 timeout 900 python -m pytest tests/test_gpu_tensor.py tests/test_gpu_configs.py -x -q 2>&1 | tail -2
