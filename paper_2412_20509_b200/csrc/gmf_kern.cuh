@@ -574,10 +574,10 @@ GMF_D void colpart_sum(const Params& P, int64_t pos, int k, int RS, T& gs, T& hs
 }
 
 // row-side sums of (row il of the block, k) over the CT column tiles
-template <typename T>
+template <typename T, int W = 4>
 GMF_D void rowpart_sum(const Params& P, int64_t il, int k, T& gs, T& hs) {
-  // the column tiles' loads issued together, 4 per pass, fixed-order adds
-  constexpr int W = 4;
+  // the column tiles' loads issued together, W per pass, fixed-order adds
+  // (the sum is sequential in the tile index whatever W is)
   const T* rp = tptr<T>(P.rowpart);
   const int64_t cstride = P.nstar_max * (2 * P.Kr);
   const T* src = rp + il * (2 * P.Kr) + k;

@@ -1035,8 +1035,13 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
         tick(kt_ld, 12);
         if (csr) {
           scatter(c + 1);
-        } else if (c + 2 < nch && (P.m & 3) == 0 && P.col_identity && ncv > 0) {
-          // dense: the chunk after next into L2 (one bulk prefetch per row)
+        } else if (nka == 32 && c + 2 < nch && (P.m & 3) == 0 && P.col_identity && ncv > 0) {
+          // dense: the chunk after next into L2 (one bulk prefetch per row).
+          // Only with the 32-feature operands, whose longer GEMM1 leaves this
+          // warp slack: with 16 features the prefetches took half the loader's
+          // time and delayed the operand copies that gate GEMM1 (deep dense
+          // cell K1 1.17 -> 0.92 ms without them), and the elementwise warps
+          // already load the counts a whole chunk ahead
           const int rows2 = rows_of(nrows, c + 2);
           for (int r = lane; r < rows2; r += 32) {
             const int64_t i = r0 + rlo + (int64_t)(c + 2) * CR + r;
