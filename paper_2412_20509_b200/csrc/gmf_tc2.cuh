@@ -699,7 +699,11 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
       issue_a1(0);
       issue_csr(0);
       issue_a3(0);
-      issue_a1(1);
+      // with a single A1 buffer (shared memory short: CSR with 32-feature
+      // operands) chunk 1's copy waits for GEMM1 of chunk 0, which the MMA
+      // warp only issues after this prologue's barrier: it is issued in the
+      // loader's role section below instead
+      if (L.na1 >= 2) issue_a1(1);
       issue_csr(1);
     }
     if (P.colimg_on) mbar_wait(&B.cimg, X.nu & 1u);
@@ -1028,6 +1032,7 @@ GMF_D void grad_units(const Params& P, long long blk, long long s, double alpha,
         if (lane == 0) mbar_arrive(&B.y_full[ys]);
         tick(kt_ld, 15);
       };
+      if (L.na1 < 2) issue_a1(1);
       if (csr) scatter(0);
       for (int c = 0; c < nch; ++c) {
         issue_a1(c + 2);

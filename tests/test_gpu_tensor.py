@@ -272,3 +272,50 @@ def test_k1_generation_is_the_one_requested(gen, monkeypatch):
     finally:
         fit.close()
         torch.cuda.synchronize()
+
+
+def _grad_vs_oracle(y, x, z, off, st, I, J, family, data):
+    n, m = y.shape
+    covs = gk.CovariateSet(x=x if x.shape[1] else None, z=z if z.shape[1] else None, n=n, m=m)
+    lam = (0.3, 0.2, 1.0, 0.7)
+    fam = gk.NegBinomial(2.0) if family == "nb" else gk.Poisson()
+    gp = gk.minibatch_gradients(st, data, covs, fam, gk.Log(), gk.PenaltyConfig(lam=1.0, blocks=lam),
+                                gk.Minibatch(I, J), offset=off, dtype="f32", k1_impl="tensor")
+    pb = orc.OProblem(y, x, z, offset=off)
+    ost = orc.OState(st.b, st.gamma, st.u, st.v, 1.0, 2.0)
+    ref = orc.minibatch_gradients(ost, pb, I, J, orc.NEG_BINOMIAL if family == "nb" else orc.POISSON,
+                                  orc.LOG, lam)
+    errs = {k: normwise(mine, r) for k, mine, r in (
+        ("g_row", gp.g_rowside, ref.g_row), ("h_row", gp.h_rowside, ref.h_row),
+        ("g_col", gp.g_colside, ref.g_col), ("h_col", gp.h_colside, ref.h_col))}
+    return gp, errs
+
+
+@pytest.mark.parametrize("family", ["poisson", "nb"])
+def test_k1_v2_csr_with_32_feature_operands(family, monkeypatch):
+    """K1 v2 on a CSR response with K = p+q+d + sentinels in (16, 32]: shared
+    memory then holds a single A1 buffer, whose second chunk can only be
+    staged once GEMM1 of the first has run (a c5 sweep cell, 65,536 x 500
+    d = 15 CSR, found the prologue waiting for it before the MMA warp ran)."""
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    monkeypatch.setenv("GMF_TC_VERSION", "2")
+    y, x, z, off, st = _problem(21, 900, 200, 15, 1, 1, family, False)
+    I, J = np.arange(13, 880), np.arange(200)
+    data = gk.ResponseMatrix(csr=dense_to_csr(y), shape=y.shape)
+    _, errs = _grad_vs_oracle(y, x, z, off, st, I, J, family, data)
+    assert max(errs.values()) < TOL, errs
+
+
+@pytest.mark.parametrize("fmt", ["dense", "csr"])
+def test_k1_v2_wide_matrix_two_units_per_cta(fmt, monkeypatch):
+    """Wide matrix on K1 v2: 8 column tiles x 37 row ranges = two units per CTA
+    (the per-unit prologue / drain and the mbarrier phases carried across
+    units), 24 chunks per unit."""
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    monkeypatch.setenv("GMF_TC_VERSION", "2")
+    y, x, z, off, st = _problem(22, 1500, 1000, 5, 1, 1, "nb", True)
+    I, J = np.arange(1500), np.arange(1000)
+    data = gk.ResponseMatrix(y) if fmt == "dense" else gk.ResponseMatrix(csr=dense_to_csr(y),
+                                                                         shape=y.shape)
+    _, errs = _grad_vs_oracle(y, x, z, off, st, I, J, "nb", data)
+    assert max(errs.values()) < TOL, errs
