@@ -60,7 +60,7 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   } else {
     // holes: a standalone gradient masks them (gradients.py:66-88); inside
     // the fit they carry the imputed mean, refilled every nafill steps
-    const int hmode = P.gen ? 3 : (P.holes ? (xb >= 0 ? 2 : 1) : 0);
+    const int hmode = FAM == 2 ? 3 : (P.holes ? (xb >= 0 ? 2 : 1) : 0);
     const bool fill = hmode == 1 && mod_nn(P.ctrl->t, P.nafill) == 0;
     grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem, hmode, fill,
                              xb >= 0 ? P.phi : C->phi);
@@ -207,7 +207,7 @@ struct Vec16;   // 16-byte vector of T
 template <> struct Vec16<float> { using V = float4; static constexpr int N = 4; };
 template <> struct Vec16<double> { using V = double2; static constexpr int N = 2; };
 
-template <typename T, int NK, int NT = kThreads>
+template <typename T, int NK, int NT = kThreads, bool GEN = false>
 GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, int64_t lo,
                              int64_t hi) {
   using V = typename Vec16<T>::V;
@@ -227,7 +227,7 @@ GMF_D double obj_dev_partial(const Params& P, double alpha, const int4* ents, in
     #pragma unroll
     for (int k = 0; k < NK; ++k) eta += (double)av[k] * (double)cv[k];
     const double wv = P.has_w ? (double)tptr<T>(P.w)[i * P.m + j] : 1.0;
-    if (P.gen)   // general mode: real-valued response, any link (fp64 per-entry algebra)
+    if constexpr (GEN)   // general mode: real-valued response, any link (fp64 per-entry algebra)
       s += wv * unit_deviance(P.fam, (double)tptr<T>(P.y_work)[i * P.m + j],
                               gen_mean<double>(P.link, eta), alpha);
     else if (sizeof(T) == 4)   // fp32 path: fp32 transcendentals, fp64 accumulation
@@ -508,7 +508,8 @@ k_fit(Params P, long long n_steps) {
       // contiguous, equal entry ranges per CTA keep the objective balanced
       double v[1] = {0.0};
       const long long c0 = profc ? clock64() : 0;
-      v[0] = obj_dev_partial<T, NK, NT>(P, C.nb_shape, ep_src + (ep_cached ? 0 : e_lo), e_lo, e_hi);
+      v[0] = obj_dev_partial<T, NK, NT, FAM == 2>(P, C.nb_shape, ep_src + (ep_cached ? 0 : e_lo),
+                                                   e_lo, e_hi);
       const long long c1 = profc ? clock64() : 0;
       block_sum_vec<1, NT>(v, scr);
       if (threadIdx.x == 0) P.objpart[OBJ_W * blockIdx.x] = v[0];
@@ -549,7 +550,7 @@ k_fit(Params P, long long n_steps) {
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
                               profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
       else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem,
-                                    P.gen ? 3 : (P.holes ? 1 : 0),
+                                    FAM == 2 ? 3 : (P.holes ? 1 : 0),
                                     P.holes && mod_nn(t, P.nafill) == 0, C.phi);
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }

@@ -331,7 +331,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
       }
     }
     unsigned char* st = smem + L.stage[b];
-    if (!csr && (P.holes || P.gen)) {   // working / real-valued response (T)
+    if (!csr && (FAM == 2 || P.holes)) {   // working / real-valued response (T)
       T* y_b = reinterpret_cast<T*>(st);
       const T* yw = tptr<T>(P.y_work);
       for (int e = tid; e < TR * TC; e += kThreads) {
@@ -450,7 +450,7 @@ GMF_D void grad_cta(const Params& P, long long blk, long long s, double alpha, i
 
     // ---- phase 1 ----
     T cn = T(0), cd = T(0);
-    if (P.holes || P.gen) {
+    if (FAM == 2 || P.holes) {
       T* ywg = tptr<T>(P.y_work) + i0 * P.m + j;   // the chunk's first row, this thread's column j
       if (P.has_w)
         phase1<T, FAM, NK, TC, true, true>(a_s, cd2_s, off_s, y_s, w_s, P_s, cf, gacc, hacc, cm, c,
