@@ -103,3 +103,28 @@ def test_two_gpus_nccl_exchange_matches_single_rank(tmp_path):
     g = golden("nb_offset")
     assert normwise(r["trace"], g["trace"]) < 1e-10
     assert normwise(r["uv"], g["unproj_u"] @ g["unproj_v"].T) < 1e-8
+
+
+def test_general_mode_through_the_exchange_path(nccl_group, monkeypatch):
+    """General mode (Gamma / log with the Pearson dispersion update) on the
+    per-step kernels of the multi-rank path, eager and graph-captured: the
+    Pearson sums ride in the rank record and phi advances in k_apply."""
+    from paper_2412_20509_b200 import optim
+    from test_general_oracle import case
+    c = case(golden("general"), "gamma_log")
+    n, m = c["y"].shape
+    data = gk.ResponseMatrix(c["y"].astype(float))
+    covs = gk.CovariateSet(x=c["x"], n=n, m=m)
+    me, mr, mc, seed = (int(v) for v in c["cfg"])
+    cfg = gk.SgdConfig(max_epochs=me, mb_rows=mr, mb_cols=mc, tol=1e-30, seed=seed)
+    st = gk.FactorizationState(c["init_b"], c["init_gamma"], c["init_u"], c["init_v"], 1.0, 1.0)
+    monkeypatch.setattr(optim, "_FORCE_EXCHANGE", True)
+    for graph in (False, True):
+        monkeypatch.setattr(optim, "_GRAPH_EXCHANGE", graph)
+        final, rep = gk.fit_asgd(data, covs, gk.Gamma(), gk.Log(), gk.PenaltyConfig(), cfg, st,
+                                 dtype="f64", process_group=nccl_group, exchange="device",
+                                 identify_mode=None)
+        assert normwise(rep.objective_trace, c["trace"]) < 1e-9, graph
+        assert normwise(rep.phi_trace, c["phi_trace"]) < 1e-9, graph
+        assert normwise(final.u @ final.v.T, c["unproj_u"] @ c["unproj_v"].T) < 1e-7, graph
+        assert abs(final.phi - float(c["unproj_phi"])) < 1e-9 * float(c["unproj_phi"])
