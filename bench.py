@@ -119,13 +119,17 @@ class Clocks:
 
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws == 1:
+    if ws == 1 and not os.environ.get("GMF_BENCH_FORCE_EXCHANGE"):
         return 1, 0, 0, None
     import torch
     import torch.distributed as dist
     lr = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(lr)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    if ws == 1:   # test hook: the multi-rank code path on a one-rank NCCL group
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29581", rank=0, world_size=1,
+                                device_id=torch.device("cuda", lr))
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     return ws, dist.get_rank(), lr, dist.group.WORLD
 
 
@@ -415,14 +419,29 @@ def main():
                     offset=wl.offset, dtype=sp.dtype, device=local, world=world, rank=rank,
                     est_alpha=sp.family == "neg_binomial", k1_impl=args.k1_impl)
     fit.reset()
-    ex = _Exchange(fit, group, "device") if world > 1 else None
+    ex = _Exchange(fit, group, "device") if group is not None else None
+
+    state = {"eager_done": False}
 
     def steps(k):
+        # N = 1: one persistent launch.  N > 1: the rank step (objective, K1,
+        # record copy, NCCL all-gather, fixed-order apply) replayed as CUDA
+        # graphs of 32 steps, as fit_asgd drives it (optim._Exchange.graph);
+        # one eager step first warms the communicator, the remainder is eager
         if ex is None:
             fit.run(k)
-        else:
-            for _ in range(k):
-                ex.step()
+            return
+        if not state["eager_done"] and k > 0:
+            n0 = fit.launch_count()
+            ex.step()
+            state["per_step"] = fit.launch_count() - n0   # kernels of one rank step
+            state["eager_done"] = True
+            k -= 1
+        while k >= 32:
+            ex.graph(32)
+            k -= 32
+        for _ in range(k):
+            ex.step()
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -448,6 +467,8 @@ def main():
     e1.record()
     barrier()
     timed_launches = fit.launch_count() - launches0
+    if ex is not None:   # graph replays launch their captured kernels without the host counter
+        timed_launches = state.get("per_step", 0) * K
     w1 = time.perf_counter()
     ms = e0.elapsed_time(e1)
     clocks = clk.stop(w0, w1)
@@ -671,7 +692,7 @@ def main():
             "fp64_c2": fp64_c2,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if group is not None:
         torch.distributed.destroy_process_group()
 
 
