@@ -56,6 +56,8 @@ DESC_TAIL_PADDED = 1
 DESC_REAL_RESPONSE = 2
 # evaluation-only handle (gmf_entries_eval under any family / link)
 DESC_EVAL_ONLY = 4
+# general mode with unobserved entries marked by sign (nonnegative responses)
+DESC_REAL_HOLES = 8
 
 
 class GmfConfig(C.Structure):

@@ -95,6 +95,11 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
     set_error("the Pearson dispersion update runs in general mode (GMF_DESC_REAL_RESPONSE)");
     return GMF_ERR_UNSUPPORTED;
   }
+  if ((d->flags & GMF_DESC_REAL_HOLES) && (!real || d->family == GMF_GAUSSIAN)) {
+    set_error("unobserved entries in general mode are marked by sign: the family's responses "
+              "must be nonnegative (not gaussian)");
+    return GMF_ERR_UNSUPPORTED;
+  }
   if (real) {
     if (d->y_format != GMF_Y_DENSE_I32 || (!b->y_work && d->n > 0)) {
       set_error("general mode needs a dense real-valued response in y_work");
@@ -230,7 +235,7 @@ int gmf_create(const gmf_desc* desc, const gmf_config* cfg, const gmf_buffers* b
   P.link = desc->link;
   P.est_phi = P.gen && cfg->est_phi;
   P.inv_dof = cfg->inv_resid_dof;
-  P.holes = bufs->y_work != nullptr && !P.gen;
+  P.holes = bufs->y_work != nullptr && (!P.gen || (desc->flags & GMF_DESC_REAL_HOLES));
   P.y_work = bufs->y_work;
   P.nafill = cfg->nafill_every > 0 ? cfg->nafill_every : 1;
   if (P.holes && desc->y_format != GMF_Y_DENSE_I32) {

@@ -60,7 +60,8 @@ k_grad(Params P, long long xb, long long xs, double xalpha) {
   } else {
     // holes: a standalone gradient masks them (gradients.py:66-88); inside
     // the fit they carry the imputed mean, refilled every nafill steps
-    const int hmode = FAM == 2 ? 3 : (P.holes ? (xb >= 0 ? 2 : 1) : 0);
+    // general mode without holes: hmode 3 (y_work is the plain response)
+    const int hmode = P.holes ? (xb >= 0 ? 2 : 1) : (FAM == 2 ? 3 : 0);
     const bool fill = hmode == 1 && mod_nn(P.ctrl->t, P.nafill) == 0;
     grad_cta<T, FAM, NK, TC>(P, blk, s, alpha, rs, ct, RS, smem, hmode, fill,
                              xb >= 0 ? P.phi : C->phi);
@@ -550,7 +551,7 @@ k_fit(Params P, long long n_steps) {
         tc::grad_cta<FAM, NK>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem, tcx,
                               profc ? P.prof + 16 + 32 * blockIdx.x + 8 : nullptr);
       else grad_cta<T, FAM, NK, TC>(P, blk, sidx, C.nb_shape, rs, ct, RS, smem,
-                                    FAM == 2 ? 3 : (P.holes ? 1 : 0),
+                                    P.holes ? 1 : (FAM == 2 ? 3 : 0),
                                     P.holes && mod_nn(t, P.nafill) == 0, C.phi);
     }
     if (prof) { t_b = gtimer(); atomicAdd(P.prof + 1, t_b - t_a); t_a = t_b; }

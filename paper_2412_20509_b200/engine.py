@@ -115,6 +115,21 @@ def permute_csr(indptr, indices, data, order):
     return new_ptr, np.asarray(indices)[src].astype(np.int32), np.asarray(data)[src]
 
 
+def _mean_of_eta(kind, eta):
+    """g^{-1}(eta) without domain checks (kernels/_ref.py:21-32), for seeding
+    the working response at unobserved entries."""
+    with np.errstate(all="ignore"):
+        if kind == "identity":
+            return np.asarray(eta, dtype=float)
+        if kind == "log":
+            return np.exp(eta)
+        if kind == "logit":
+            return 1.0 / (1.0 + np.exp(-eta))
+        if kind == "inverse":
+            return 1.0 / eta
+        return 1.0 / np.sqrt(eta)
+
+
 def _counts_int32(vals, what):
     v = np.asarray(vals)
     if v.dtype.kind in "iu":
@@ -179,13 +194,13 @@ class DeviceFit:
                     f"{fam.kind}+{lnk.kind}"
                     f"{' with an estimated dispersion' if est_phi else ''} runs in general mode, "
                     "which needs a dense response")
-            if holes:
+            if holes and fam.kind == "gaussian":
                 raise _lib.UnsupportedError(
-                    "general mode (non-count family / link, or estimated phi) needs a fully "
-                    "observed response")
+                    "general mode marks unobserved entries by sign, so the family's responses "
+                    "must be nonnegative: gaussian responses need a fully observed matrix")
             if k1_impl == "tensor":
                 raise _lib.UnsupportedError("general mode runs K1 on the CUDA cores")
-            fam.check_y(data.values)   # DomainError as families.py:239-241
+            fam.check_y(data.values[data.mask] if holes else data.values)   # DomainError (families.py:239-241)
         if dtype not in ("f32", "f64"):
             raise ConfigError(f"dtype must be 'f32' or 'f64', got {dtype!r}")
         if k1_impl not in _lib.K1_IMPL_CODES:
@@ -253,7 +268,7 @@ class DeviceFit:
             y_format_code = _lib.Y_DENSE_I32
         self.y_work = None
         self.general = general
-        if general:   # the real-valued response itself (GMF_DESC_REAL_RESPONSE)
+        if general and not holes:   # the real-valued response itself (GMF_DESC_REAL_RESPONSE)
             self.y_work = up(data.values[order], self.tdt)
         elif holes:
             # working response (optim.py:368-374): observed counts, and at every
@@ -268,7 +283,7 @@ class DeviceFit:
             if offset is not None:
                 eta0 = eta0 + np.asarray(offset, dtype=float)[order][:, None]
             with np.errstate(all="ignore"):
-                yw = np.where(mo, data.values[order], -np.exp(eta0))
+                yw = np.where(mo, data.values[order], -_mean_of_eta(lnk.kind, eta0))
             self.y_work = up(yw, self.tdt)
         self.weights = None
         if data.weights is not None:
@@ -321,6 +336,7 @@ class DeviceFit:
                                  rank=rank, device=dev_index,
                                  flags=_lib.DESC_TAIL_PADDED |
                                  (_lib.DESC_REAL_RESPONSE if general else 0) |
+                                 (_lib.DESC_REAL_HOLES if general and holes else 0) |
                                  (_lib.DESC_EVAL_ONLY if eval_only else 0))
         dof = self.n * self.m - (self.p * self.m + self.q * self.n + self.d * (self.n + self.m) + 1)
         if est_phi and dof <= 0:

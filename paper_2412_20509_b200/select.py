@@ -59,11 +59,14 @@ def loglik_terms(state: FactorizationState, data: ResponseMatrix, covs: Covariat
 
 
 def _general_constant(fit, data, fam, phi):
-    """c(phi) of select.py:57-79 for a general-mode fit (fully observed):
-    n log phi (Gaussian, inverse Gaussian), 2 sum(lgamma(s) - s log s + s) with
-    s = w / phi (Gamma), the NB saturated terms for a non-log link, else 0."""
+    """c(phi) of select.py:57-79 for a general-mode fit, over the observed
+    entries: n_obs log phi (Gaussian, inverse Gaussian), 2 sum(lgamma(s) -
+    s log s + s) with s = w / phi (Gamma), the NB saturated terms for a
+    non-log link, else 0."""
     torch = fit.torch
-    n_obs = data.n * data.m
+    n_obs = int(data.n_observed)
+    # unobserved entries carry a negative working response
+    obs = None if data.fully_observed else ~torch.signbit(fit.y_work)
     kind = fam.kind
     if kind in ("gaussian", "inverse_gaussian"):
         return float(n_obs * np.log(phi))
@@ -73,16 +76,20 @@ def _general_constant(fit, data, fam, phi):
             from math import lgamma
             return float(2.0 * n_obs * (lgamma(s) - s * np.log(s) + s))
         s = fit.weights.double() / phi
-        return float((2.0 * (torch.lgamma(s) - s * torch.log(s) + s)).sum().item())
+        t = 2.0 * (torch.lgamma(s) - s * torch.log(s) + s)
+        return float((t if obs is None else torch.where(obs, t, torch.zeros_like(t))).sum().item())
     if kind == "neg_binomial":
         a = float(fam.nb_shape)
         y = fit.y_work.double()
+        if obs is not None:
+            y = torch.where(obs, y, torch.zeros_like(y))
         w = 1.0 if fit.weights is None else fit.weights.double()
         sat = (torch.lgamma(y + a) - torch.lgamma(torch.tensor(a, device=y.device, dtype=y.dtype))
                - torch.lgamma(y + 1.0) - (y + a) * torch.log(y + a) + a * np.log(a))
         ylogy = torch.where(y > 0, y * torch.log(torch.where(y > 0, y, torch.ones_like(y))),
                             torch.zeros_like(y))
-        return float((-2.0 * (w * (sat + ylogy))).sum().item())
+        t = -2.0 * (w * (sat + ylogy))
+        return float((t if obs is None else torch.where(obs, t, torch.zeros_like(t))).sum().item())
     return 0.0
 
 

@@ -506,6 +506,21 @@ def make_cv():
                                   rep.chosen["scree"]])}
 
 
+def make_cv_gamma():
+    """cv_rank_select of the reference for a non-count family (Gamma / log,
+    estimated dispersion): masked train fits, GLM-SVD starts, AIC/BIC with the
+    Gamma dispersion constant, held-out relative deviance."""
+    y, x, z, _ = _general_problem("gamma", "log", 200, 40, 1, 0, 2, 141)
+    data = gk.ResponseMatrix(y)
+    covs = gk.CovariateSet(x=x, m=40)
+    cfg = gk.SgdConfig(max_epochs=16, mb_rows=50, mb_cols=40, tol=1e-30, seed=2)
+    rep = gk.cv_rank_select(data, covs, gk.Gamma(), gk.Log(), [1, 2, 3], folds=2, cfg=cfg, seed=6)
+    return {"y": y, "x": x, "aic": np.asarray(rep.aic), "bic": np.asarray(rep.bic),
+            "cv": np.asarray(rep.cv_deviance), "failures": np.asarray(str(rep.failures)),
+            "chosen": np.asarray([rep.chosen["cv"], rep.chosen["aic"], rep.chosen["bic"],
+                                  rep.chosen["scree"]])}
+
+
 def make_api():
     """Block helpers of the public API: linear_predictor (model.py:229-256),
     impute_block (optim.py:232-245), update_nb_shape_stochastic (205-229)."""
@@ -700,6 +715,38 @@ def make_general():
     return out
 
 
+def make_general_masked():
+    """Unobserved entries under non-count families (optim.py:368-374, 430-436
+    with families.py:267-396): whole fits of the reference on ~15 % masked
+    responses, nafill_every = 2."""
+    out = {"cases": np.asarray(["gamma_log", "bern_logit", "ig_log"])}
+    for name, fk, lk, disp, (p, q, d), seed in GENERAL_CASES:
+        if name not in ("gamma_log", "bern_logit", "ig_log"):
+            continue
+        n, m = 300, 40
+        y, x, z, init = _general_problem(fk, lk, n, m, p, q, d, seed + 200)
+        mask = np.random.default_rng(seed + 300).uniform(size=y.shape) > 0.15
+        data = gk.ResponseMatrix(np.where(mask, y, np.nan), mask=mask)
+        covs = gk.CovariateSet(x=x if p else None, z=z if q else None, n=n, m=m)
+        fam, lnk = gk.family(fk), gk.link(lk)
+        cfg = gk.SgdConfig(max_epochs=20, mb_rows=75, mb_cols=m, tol=1e-30, seed=seed,
+                           nafill_every=2)
+        st0 = gk.FactorizationState(init["b"], init["gamma"], init["u"], init["v"], 1.0, 1.0)
+        final, rep = gk.fit_asgd(data, covs, fam, lnk, gk.PenaltyConfig(), cfg, st0,
+                                 dispersion=disp, identify_mode=None)
+        arrs = {"y": y, "mask": mask, "x": x, "z": z, "family": np.asarray(fk),
+                "link": np.asarray(lk), "dispersion": np.asarray(disp),
+                "trace": np.asarray(rep.objective_trace), "phi_trace": np.asarray(rep.phi_trace),
+                "final_objective": np.float64(rep.final_objective),
+                "cfg": np.asarray([cfg.max_epochs, cfg.mb_rows, cfg.mb_cols, cfg.seed,
+                                   cfg.nafill_every], dtype=np.int64)}
+        arrs.update(_state_arrays("init", st0))
+        arrs.update(_state_arrays("final", final))
+        assert np.all(np.isfinite(rep.objective_trace)), name
+        out.update({f"{name}__{k}": v for k, v in arrs.items()})
+    return out
+
+
 def make_init_general():
     """init_glm_svd of the reference for the general families / links, incl.
     the Pearson start of phi (initialization.py:85-90, 172-214)."""
@@ -720,7 +767,8 @@ def make_init_general():
 
 
 def main():
-    makers = {"general": make_general, "init_general": make_init_general, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
+    makers = {"general": make_general, "init_general": make_init_general,
+              "general_masked": make_general_masked, "cv_gamma": make_cv_gamma, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,

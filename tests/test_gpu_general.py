@@ -129,9 +129,10 @@ def test_general_mode_limits():
         gk.fit_asgd(gk.ResponseMatrix(bad), covs, gk.Gamma(), gk.Log(), gk.PenaltyConfig(), cfg, st)
     mask = np.ones((n, m), bool)
     mask[0, 0] = False
-    with pytest.raises(_lib.UnsupportedError):   # no imputation in general mode
-        gk.fit_asgd(gk.ResponseMatrix(np.where(mask, y, np.nan), mask=mask), covs, gk.Gamma(),
-                    gk.Log(), gk.PenaltyConfig(), cfg, st)
+    yg = rng.normal(0, 1, (n, m))
+    with pytest.raises(_lib.UnsupportedError):   # holes are marked by sign: not for gaussian
+        gk.fit_asgd(gk.ResponseMatrix(np.where(mask, yg, np.nan), mask=mask), covs, gk.Gaussian(),
+                    gk.Identity(), gk.PenaltyConfig(), cfg, st)
 
 
 def test_update_dispersion_stochastic_matches_oracle():
@@ -209,3 +210,44 @@ def test_model_selection_general_family(name):
     res = heldout_scores(st, covs, fam, lnk, rows, cols, y_test, ybar)
     assert res.rel_deviance == pytest.approx(orc.rel_deviance(fc, y_test, omu, ybar, 1.0), rel=1e-10)
     assert gk.rel_deviance(y_test, omu, ybar, fam) == pytest.approx(res.rel_deviance, rel=1e-10)
+
+
+@pytest.mark.parametrize("name", ["gamma_log", "bern_logit", "ig_log"])
+def test_general_fit_with_unobserved_entries(name):
+    """General mode on a masked response (holes marked by sign, imputed on the
+    device every nafill_every steps; optim.py:368-374, 430-436) against the
+    reference's own fits (make_golden.py general_masked)."""
+    c = case(golden("general_masked"), name)
+    n, m = c["y"].shape
+    mask = c["mask"]
+    data = gk.ResponseMatrix(np.where(mask, c["y"], np.nan), mask=mask)
+    covs = gk.CovariateSet(x=c["x"] if c["x"].shape[1] else None,
+                           z=c["z"] if c["z"].shape[1] else None, n=n, m=m)
+    me, mr, mc, seed, nafill = (int(v) for v in c["cfg"])
+    cfg = gk.SgdConfig(max_epochs=me, mb_rows=mr, mb_cols=mc, tol=1e-30, seed=seed,
+                       nafill_every=nafill)
+    st = gk.FactorizationState(c["init_b"], c["init_gamma"], c["init_u"], c["init_v"], 1.0, 1.0)
+    final, rep = gk.fit_asgd(data, covs, gk.family(str(c["family"])), gk.link(str(c["link"])),
+                             gk.PenaltyConfig(), cfg, st, dispersion=str(c["dispersion"]),
+                             identify_mode=None, dtype="f64")
+    assert normwise(rep.objective_trace, c["trace"]) < 1e-9
+    assert normwise(rep.phi_trace, c["phi_trace"]) < 1e-9
+    assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 1e-7
+    fo = float(c["final_objective"])
+    assert abs(rep.final_objective - fo) < 1e-9 * abs(fo)
+
+
+def test_cv_rank_select_gamma_matches_reference():
+    """cv_rank_select for a non-count family: masked general-mode train fits
+    with GLM-SVD starts, AIC/BIC with the Gamma constant, held-out deviance."""
+    from paper_2412_20509_b200.select import cv_rank_select
+    g = golden("cv_gamma")
+    data = gk.ResponseMatrix(g["y"].astype(float))
+    covs = gk.CovariateSet(x=g["x"], m=40)
+    cfg = gk.SgdConfig(max_epochs=16, mb_rows=50, mb_cols=40, tol=1e-30, seed=2)
+    rep = cv_rank_select(data, covs, gk.Gamma(), gk.Log(), [1, 2, 3], folds=2, cfg=cfg, seed=6)
+    assert str(rep.failures) == str(g["failures"])
+    assert normwise(rep.aic, g["aic"]) < 1e-6
+    assert normwise(rep.bic, g["bic"]) < 1e-6
+    assert normwise(np.asarray(rep.cv_deviance), g["cv"]) < 1e-5
+    assert [rep.chosen[k] for k in ("cv", "aic", "bic", "scree")] == g["chosen"].tolist()
