@@ -143,9 +143,10 @@ typedef struct gmf_desc {
    K1 runs on the CUDA cores with the family and link chosen at run time,
    p+q+d <= 32 */
 #define GMF_DESC_REAL_RESPONSE 2
-/* general mode with unobserved entries: y_work marks a hole as minus its
-   imputed mean exactly as the count path does (optim.py:368-374, 430-436), so
-   the family's responses must be nonnegative (every family but Gaussian) */
+/* general mode with unobserved entries: y_work marks a hole by the least
+   significant mantissa bit of its imputed mean (seeded with g^{-1}(eta0),
+   refilled on the device every nafill_every steps; optim.py:368-374,
+   430-436); the caller clears that bit in the observed values (<= 1 ulp) */
 #define GMF_DESC_REAL_HOLES 8
 /* evaluation-only handle: holds a state for gmf_entries_eval (mu at listed
    entries, held-out scores; select.py:141-145) under ANY family / link, with

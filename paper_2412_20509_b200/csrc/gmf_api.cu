@@ -95,10 +95,9 @@ int validate(const gmf_desc* d, const gmf_config* c, const gmf_buffers* b) {
     set_error("the Pearson dispersion update runs in general mode (GMF_DESC_REAL_RESPONSE)");
     return GMF_ERR_UNSUPPORTED;
   }
-  if ((d->flags & GMF_DESC_REAL_HOLES) && (!real || d->family == GMF_GAUSSIAN)) {
-    set_error("unobserved entries in general mode are marked by sign: the family's responses "
-              "must be nonnegative (not gaussian)");
-    return GMF_ERR_UNSUPPORTED;
+  if ((d->flags & GMF_DESC_REAL_HOLES) && !real) {
+    set_error("GMF_DESC_REAL_HOLES needs GMF_DESC_REAL_RESPONSE");
+    return GMF_ERR_CONFIG;
   }
   if (real) {
     if (d->y_format != GMF_Y_DENSE_I32 || (!b->y_work && d->n > 0)) {

@@ -251,6 +251,14 @@ GMF_D double sum_parts(const double* parts, int64_t n, int64_t stride, double* s
 // canonical pairs use the reference's simplified forms, the rest the generic
 // -w r / (phi nu g'), w / (phi nu g'^2)); pear = w r^2 / nu (optim.py:196-199)
 // ---------------------------------------------------------------------------
+// general mode marks an unobserved entry of the working response by the least
+// significant mantissa bit (observed values have it cleared by the caller: at
+// most one ulp; the sign is taken by real-valued responses)
+GMF_D bool lsb_set(float v) { return (__float_as_uint(v) & 1u) != 0u; }
+GMF_D bool lsb_set(double v) { return (__double_as_longlong(v) & 1ll) != 0ll; }
+GMF_D float with_lsb(float v) { return __uint_as_float(__float_as_uint(v) | 1u); }
+GMF_D double with_lsb(double v) { return __longlong_as_double(__double_as_longlong(v) | 1ll); }
+
 GMF_D float gexp(float x) { return expf(x); }
 GMF_D double gexp(double x) { return exp(x); }
 GMF_D float grsqrt(float x) { return 1.f / sqrtf(x); }

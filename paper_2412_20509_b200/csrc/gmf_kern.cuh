@@ -188,12 +188,14 @@ GMF_D void phase1(const T* __restrict__ a_s, const T* __restrict__ cd2_s,
     if constexpr (HOLES) {
       // hmode 3: y_work is a plain real-valued response (no holes)
       const T v = reinterpret_cast<const T*>(y_s)[rr * TC + c];
-      const bool hole = hmode != 3 && signbit(v);
-      yv = hole ? -v : v;
+      // count paths: a hole is minus its imputed mean; general mode (FAM 2):
+      // the imputed mean with its last mantissa bit set
+      const bool hole = hmode != 3 && (FAM == 2 ? lsb_set(v) : signbit(v));
+      yv = (hole && FAM != 2) ? -v : v;
       if (hole && hmode == 2) wv = T(0);
       if (hole && hmode == 1 && fill && cm != T(0)) {
         yv = mu;
-        ywg[(int64_t)rr * ystride] = -mu;
+        ywg[(int64_t)rr * ystride] = FAM == 2 ? with_lsb(mu) : -mu;
       }
     } else {
       yv = (T)y_s[rr * TC + c];

@@ -458,11 +458,11 @@ __global__ void __launch_bounds__(kThreads) k_objfull(Params P, double alpha, in
           const double eta = acc[r][h] + offs[rr];
           if constexpr (GEN) {   // general mode: real-valued response, any link
             const double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
-            const double yv = (double)tptr<T>(P.y_work)[i * P.m + j];
-            // unobserved entries (negative working response) are not in the
-            // masked deviance (model.py:268-276)
-            if (!(P.holes && signbit(yv)))
-              s += w * unit_deviance(P.fam, yv, gen_mean<double>(P.link, eta), alpha);
+            const T yt = tptr<T>(P.y_work)[i * P.m + j];
+            // unobserved entries (last mantissa bit set) are not in the masked
+            // deviance (model.py:268-276)
+            if (!(P.holes && lsb_set(yt)))
+              s += w * unit_deviance(P.fam, (double)yt, gen_mean<double>(P.link, eta), alpha);
           } else if (dense) {
             double w = P.has_w ? (double)wg[i * P.m + j] : 1.0;
             const double y = (double)P.y[i * P.m + j];

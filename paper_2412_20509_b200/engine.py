@@ -194,10 +194,6 @@ class DeviceFit:
                     f"{fam.kind}+{lnk.kind}"
                     f"{' with an estimated dispersion' if est_phi else ''} runs in general mode, "
                     "which needs a dense response")
-            if holes and fam.kind == "gaussian":
-                raise _lib.UnsupportedError(
-                    "general mode marks unobserved entries by sign, so the family's responses "
-                    "must be nonnegative: gaussian responses need a fully observed matrix")
             if k1_impl == "tensor":
                 raise _lib.UnsupportedError("general mode runs K1 on the CUDA cores")
             fam.check_y(data.values[data.mask] if holes else data.values)   # DomainError (families.py:239-241)
@@ -282,8 +278,18 @@ class DeviceFit:
                 eta0 = eta0 + state.gamma[order] @ covs.z.T
             if offset is not None:
                 eta0 = eta0 + np.asarray(offset, dtype=float)[order][:, None]
-            with np.errstate(all="ignore"):
-                yw = np.where(mo, data.values[order], -_mean_of_eta(lnk.kind, eta0))
+            mean0 = _mean_of_eta(lnk.kind, eta0)
+            if general:
+                # general mode: the hole marker is the last mantissa bit (set on
+                # the imputed mean, cleared -- at most one ulp -- on the
+                # observed values), since real-valued responses take the sign
+                ndt, idt = (np.float64, np.int64) if dtype == "f64" else (np.float32, np.int32)
+                yw = np.where(mo, data.values[order], mean0).astype(ndt)
+                bits = yw.view(idt)
+                bits[:] = np.where(mo, bits & ~idt(1), bits | idt(1))
+            else:
+                with np.errstate(all="ignore"):
+                    yw = np.where(mo, data.values[order], -mean0)
             self.y_work = up(yw, self.tdt)
         self.weights = None
         if data.weights is not None:

@@ -65,8 +65,11 @@ def _general_constant(fit, data, fam, phi):
     non-log link, else 0."""
     torch = fit.torch
     n_obs = int(data.n_observed)
-    # unobserved entries carry a negative working response
-    obs = None if data.fully_observed else ~torch.signbit(fit.y_work)
+    # unobserved entries carry the hole marker (last mantissa bit) in y_work
+    obs = None
+    if not data.fully_observed:
+        idt = torch.int64 if fit.y_work.dtype == torch.float64 else torch.int32
+        obs = (fit.y_work.view(idt) & 1) == 0
     kind = fam.kind
     if kind in ("gaussian", "inverse_gaussian"):
         return float(n_obs * np.log(phi))

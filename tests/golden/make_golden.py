@@ -716,12 +716,12 @@ def make_general():
 
 
 def make_general_masked():
-    """Unobserved entries under non-count families (optim.py:368-374, 430-436
-    with families.py:267-396): whole fits of the reference on ~15 % masked
-    responses, nafill_every = 2."""
-    out = {"cases": np.asarray(["gamma_log", "bern_logit", "ig_log"])}
+    """Unobserved entries under non-count families, Gaussian included
+    (optim.py:368-374, 430-436 with families.py:267-396): whole fits of the
+    reference on ~15 % masked responses, nafill_every = 2."""
+    out = {"cases": np.asarray(["gauss_id", "gamma_log", "bern_logit", "ig_log"])}
     for name, fk, lk, disp, (p, q, d), seed in GENERAL_CASES:
-        if name not in ("gamma_log", "bern_logit", "ig_log"):
+        if name not in ("gauss_id", "gamma_log", "bern_logit", "ig_log"):
             continue
         n, m = 300, 40
         y, x, z, init = _general_problem(fk, lk, n, m, p, q, d, seed + 200)

@@ -127,11 +127,10 @@ def test_general_mode_limits():
     bad[3, 4] = -1.0
     with pytest.raises(gk.DomainError):      # gamma responses must be positive
         gk.fit_asgd(gk.ResponseMatrix(bad), covs, gk.Gamma(), gk.Log(), gk.PenaltyConfig(), cfg, st)
-    mask = np.ones((n, m), bool)
-    mask[0, 0] = False
-    yg = rng.normal(0, 1, (n, m))
-    with pytest.raises(_lib.UnsupportedError):   # holes are marked by sign: not for gaussian
-        gk.fit_asgd(gk.ResponseMatrix(np.where(mask, yg, np.nan), mask=mask), covs, gk.Gaussian(),
+    from paper_2412_20509_b200.workloads import dense_to_csr
+    yc = rng.poisson(2.0, (n, m))
+    with pytest.raises(_lib.UnsupportedError):   # general mode needs a dense response
+        gk.fit_asgd(gk.ResponseMatrix(csr=dense_to_csr(yc), shape=yc.shape), covs, gk.Poisson(),
                     gk.Identity(), gk.PenaltyConfig(), cfg, st)
 
 
@@ -212,11 +211,13 @@ def test_model_selection_general_family(name):
     assert gk.rel_deviance(y_test, omu, ybar, fam) == pytest.approx(res.rel_deviance, rel=1e-10)
 
 
-@pytest.mark.parametrize("name", ["gamma_log", "bern_logit", "ig_log"])
-def test_general_fit_with_unobserved_entries(name):
-    """General mode on a masked response (holes marked by sign, imputed on the
-    device every nafill_every steps; optim.py:368-374, 430-436) against the
-    reference's own fits (make_golden.py general_masked)."""
+@pytest.mark.parametrize("name", ["gauss_id", "gamma_log", "bern_logit", "ig_log"])
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-9), ("f32", 1e-3)])
+def test_general_fit_with_unobserved_entries(name, dtype, tol):
+    """General mode on a masked response (a hole is its imputed mean with the
+    last mantissa bit set, refilled on the device every nafill_every steps;
+    optim.py:368-374, 430-436) against the reference's own fits
+    (make_golden.py general_masked)."""
     c = case(golden("general_masked"), name)
     n, m = c["y"].shape
     mask = c["mask"]
@@ -229,12 +230,12 @@ def test_general_fit_with_unobserved_entries(name):
     st = gk.FactorizationState(c["init_b"], c["init_gamma"], c["init_u"], c["init_v"], 1.0, 1.0)
     final, rep = gk.fit_asgd(data, covs, gk.family(str(c["family"])), gk.link(str(c["link"])),
                              gk.PenaltyConfig(), cfg, st, dispersion=str(c["dispersion"]),
-                             identify_mode=None, dtype="f64")
-    assert normwise(rep.objective_trace, c["trace"]) < 1e-9
-    assert normwise(rep.phi_trace, c["phi_trace"]) < 1e-9
-    assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 1e-7
+                             identify_mode=None, dtype=dtype)
+    assert normwise(rep.objective_trace, c["trace"]) < tol
+    assert normwise(rep.phi_trace, c["phi_trace"]) < tol
+    assert normwise(final.u @ final.v.T, c["final_u"] @ c["final_v"].T) < 100 * tol
     fo = float(c["final_objective"])
-    assert abs(rep.final_objective - fo) < 1e-9 * abs(fo)
+    assert abs(rep.final_objective - fo) < tol * abs(fo)
 
 
 def test_cv_rank_select_gamma_matches_reference():
