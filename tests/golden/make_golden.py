@@ -521,6 +521,22 @@ def make_cv_gamma():
                                   rep.chosen["scree"]])}
 
 
+def make_cv_gauss():
+    """cv_rank_select of the reference on Gaussian / identity data (matrix
+    completion with an estimated variance): masked train fits, AIC/BIC with
+    n_obs log phi, held-out relative deviance."""
+    y, x, z, _ = _general_problem("gaussian", "identity", 200, 40, 1, 0, 2, 151)
+    data = gk.ResponseMatrix(y)
+    covs = gk.CovariateSet(x=x, m=40)
+    cfg = gk.SgdConfig(max_epochs=16, mb_rows=50, mb_cols=40, tol=1e-30, seed=2)
+    rep = gk.cv_rank_select(data, covs, gk.Gaussian(), gk.Identity(), [1, 2, 3], folds=2, cfg=cfg,
+                            seed=6)
+    return {"y": y, "x": x, "aic": np.asarray(rep.aic), "bic": np.asarray(rep.bic),
+            "cv": np.asarray(rep.cv_deviance), "failures": np.asarray(str(rep.failures)),
+            "chosen": np.asarray([rep.chosen["cv"], rep.chosen["aic"], rep.chosen["bic"],
+                                  rep.chosen["scree"]])}
+
+
 def make_api():
     """Block helpers of the public API: linear_predictor (model.py:229-256),
     impute_block (optim.py:232-245), update_nb_shape_stochastic (205-229)."""
@@ -768,7 +784,7 @@ def make_init_general():
 
 def main():
     makers = {"general": make_general, "init_general": make_init_general,
-              "general_masked": make_general_masked, "cv_gamma": make_cv_gamma, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
+              "general_masked": make_general_masked, "cv_gamma": make_cv_gamma, "cv_gauss": make_cv_gauss, "c1": make_c1, "nb_offset": make_nb_offset, "nb_cov_s3": make_nb_cov_s3,
               "converge": make_converge, "diverge": make_diverge, "seam": make_seam,
               "project": make_project, "weighted": make_weighted,
               "select": make_select, "init": make_init, "mm": make_mm,

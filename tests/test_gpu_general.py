@@ -238,15 +238,19 @@ def test_general_fit_with_unobserved_entries(name, dtype, tol):
     assert abs(rep.final_objective - fo) < tol * abs(fo)
 
 
-def test_cv_rank_select_gamma_matches_reference():
-    """cv_rank_select for a non-count family: masked general-mode train fits
-    with GLM-SVD starts, AIC/BIC with the Gamma constant, held-out deviance."""
+@pytest.mark.parametrize("gold,fam,lnk", [("cv_gamma", "gamma", "log"),
+                                          ("cv_gauss", "gaussian", "identity")])
+def test_cv_rank_select_general_matches_reference(gold, fam, lnk):
+    """cv_rank_select for non-count families: masked general-mode train fits
+    with GLM-SVD starts, AIC/BIC with the family's dispersion constant over
+    the observed entries, held-out deviance."""
     from paper_2412_20509_b200.select import cv_rank_select
-    g = golden("cv_gamma")
+    g = golden(gold)
     data = gk.ResponseMatrix(g["y"].astype(float))
     covs = gk.CovariateSet(x=g["x"], m=40)
     cfg = gk.SgdConfig(max_epochs=16, mb_rows=50, mb_cols=40, tol=1e-30, seed=2)
-    rep = cv_rank_select(data, covs, gk.Gamma(), gk.Log(), [1, 2, 3], folds=2, cfg=cfg, seed=6)
+    rep = cv_rank_select(data, covs, gk.family(fam), gk.link(lnk), [1, 2, 3], folds=2, cfg=cfg,
+                         seed=6)
     assert str(rep.failures) == str(g["failures"])
     assert normwise(rep.aic, g["aic"]) < 1e-6
     assert normwise(rep.bic, g["bic"]) < 1e-6
