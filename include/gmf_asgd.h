@@ -299,7 +299,8 @@ int gmf_stream_signal(gmf_handle* h, int64_t value, void* stream);
 int gmf_k1_impl(gmf_handle* h);
 /* K1 kernel generation the handle runs: 0 CUDA cores, 1 tensor cores (one
    32-row chunk per step of a 256-thread CTA), 2 tensor cores, warp-specialized
-   tcgen05 pipeline (one 384-thread CTA per SM; the default when eligible) */
+   tcgen05 pipeline (one 320-thread CTA per SM; chosen when a unit is at least
+   512 rows deep, GMF_TC_VERSION=1|2 forces one) */
 int gmf_k1_version(gmf_handle* h);
 /* number of kernels this handle has launched so far (graph nodes counted) */
 int64_t gmf_launch_count(gmf_handle* h);

@@ -28,7 +28,7 @@ template <typename T, int NK> struct MinBlocks {
   static constexpr int v = (sizeof(T) == 8 || NK > 32) ? 1 : 2;
 };
 
-// threads per CTA of the fit kernel: 384 for the warp-specialized K1 v2
+// threads per CTA of the fit kernel: tc2::NT (320) for the warp-specialized K1 v2
 template <int TCM> struct FitNT { static constexpr int v = TCM == 2 ? tc2::NT : kThreads; };
 
 template <typename T, int FAM, int NK, bool TCM>

@@ -1,5 +1,6 @@
 // K1 v2 on the 5th-generation tensor cores (fp32 path): a warp-specialized
-// tcgen05 pipeline, one CTA (384 threads) per SM.
+// tcgen05 pipeline, one CTA (320 threads: 8 elementwise warps, the MMA warp,
+// the loader warp) per SM.
 //
 // Same contract as tc::grad_cta / grad_cta: for every work unit (column tile
 // ct of block J x a balanced contiguous row range rs of block I) it writes
